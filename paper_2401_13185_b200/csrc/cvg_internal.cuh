@@ -1,0 +1,92 @@
+// Internal declarations of the cvgram B200 engine (kernels + host orchestration).
+//
+// HBM layout:
+//   Z      [zrows][kp] fp64   fold-bucketed, shifted rows z = [x - c | y - d | 1 | 0...];
+//                             each owned fold is a contiguous block padded with zero
+//                             rows to a multiple of kRowStep; kp = roundup(k+m+1, 64).
+//   part   [nseg][kp][kp]     per-segment Gram partials (upper 64x64 tiles only);
+//                             a segment is <= kChunkRows rows of one fold.
+//   foldG  [nmulti][kp][kp]   fold Grams of folds with > 1 segment (fixed-order sums).
+//   local  [kp][kp]           this plan's fold-tree node (the cross-rank exchange unit).
+//   total  [kp][kp]           the whole-data Gram in the shifted basis.
+// Column k+m of Z is all ones on real rows, so Gram[j][k+m] is the column sum and
+// Gram[j][j] the sum of squares: the per-fold statistics ride in the Gram pass.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+namespace cvg {
+
+constexpr int kTile = 64;          // Gram / epilogue tile edge (columns)
+constexpr int kRowStep = 32;       // rows per pipeline stage; fold blocks pad to this
+constexpr int64_t kChunkRows = 32768;  // max rows per segment (fixed => deterministic split)
+constexpr int kTileRowsPerWarp = 1024; // rows per warp in the bucketing passes
+
+struct Status {
+  int code = 0;
+  std::string msg;
+  bool ok() const { return code == 0; }
+  static Status Ok() { return {}; }
+  static Status Err(int c, std::string m) { return {c, std::move(m)}; }
+};
+
+// ------------------------------------------------------------------ kernels
+// Bucketing (build_validation_partitions, partition.hpp:61-68) on the device.
+void launch_tile_histogram(const int32_t* labels, int64_t n, int32_t p, int32_t* tile_counts,
+                           unsigned long long* bad_row, cudaStream_t s);
+void launch_tile_scan(int32_t* tile_counts, int64_t ntiles, int32_t p, int64_t* fold_counts, cudaStream_t s);
+void launch_scatter(const int32_t* labels, int64_t n, int32_t p, int32_t fold_begin, int32_t fold_end,
+                    int32_t* tile_offsets, const int64_t* fold_zbase, int64_t* src_row, cudaStream_t s);
+
+// K1: gather + shift + ones column + zero padding (+ finiteness flag).
+void launch_reorder(int dtype, const void* x, int64_t ldx, const void* y, int64_t ldy, int64_t k, int64_t m,
+                    const int64_t* src_row, int64_t zrows, int64_t kp, const double* shift, double* z, int* nonfinite,
+                    cudaStream_t s);
+void launch_shift_from_row0(int dtype, const void* x, const void* y, int64_t k, int64_t m, double* shift,
+                            cudaStream_t s);
+
+// K2: segmented fold Gram, fp64 DMMA.  One CTA per (segment, upper tile).
+struct GramTask {
+  int64_t zrow;  // first Z row of the segment
+  int64_t rows;  // padded row count (multiple of kRowStep)
+};
+void launch_gram_f64(const double* z, int64_t kp, const GramTask* segs, int64_t nseg, const int2* tiles,
+                     int ntiles, double* part, cudaStream_t s);
+
+// K4: fixed-order (midpoint-tree) sums of kp x kp matrices over upper tiles.
+void launch_tree_sum(const double* const* srcs, const int32_t* src_begin, int ngroups, double* const* dsts,
+                     int64_t kp, const int2* tiles, int ntiles, cudaStream_t s);
+
+// K5: epilogue.
+struct FoldStatsDev {
+  double* mz;   // [nfold][w] training mean in the shifted basis
+  double* sT;   // [nfold][w] training column sums (shifted)
+  double* sd;   // [nfold][w] training std (zero -> 1)
+};
+void launch_fold_stats(const double* total, const double* const* foldG, const int64_t* n_val, int nfold, int64_t n,
+                       int64_t k, int64_t m, int64_t kp, const double* shift, FoldStatsDev st, double* mean_x,
+                       double* mean_y, double* std_x, double* std_y, cudaStream_t s);
+void launch_products(const double* total, const double* const* foldG, const int64_t* n_val, int nfold, int64_t n,
+                     int64_t k, int64_t m, int64_t kp, const double* shift, FoldStatsDev st, const int2* tiles,
+                     int ntiles, const uint32_t* cfgs, int ncfg, double* xtx, double* xty, cudaStream_t s);
+void launch_unshift_global(const double* total, int64_t n, int64_t k, int64_t m, int64_t kp, const double* shift,
+                           double* xtx, double* xty, double* sum, double* sumsq, double* mean, cudaStream_t s);
+void launch_training_mean(const double* g, const double* v, int64_t len, int64_t n, int64_t nv, double* out,
+                          cudaStream_t s);
+void launch_training_std(const double* mt, const double* st, const double* qt, int64_t len, int64_t nt,
+                         double* out, cudaStream_t s);
+void launch_hadamard(const double* mat, int64_t rows, int64_t cols, const double* l, const double* r, double* out,
+                     cudaStream_t s);
+
+// Tile list of the symmetric Gram (ti <= tj), plus the diagonal/ones tiles of
+// Y-only column blocks.  Shared by the Gram, the reductions and the epilogue.
+std::vector<int2> gram_tiles(int64_t k, int64_t m, int64_t kp);
+
+inline int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
+inline int64_t padded_cols(int64_t k, int64_t m) { return round_up(k + m + 1, kTile); }
+
+}  // namespace cvg

@@ -1,0 +1,118 @@
+// Host orchestration of the cvgram B200 engine: context, plan, global cache.
+#pragma once
+
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "cvg_internal.cuh"
+
+struct cvg_context;
+
+namespace cvg {
+
+// Grow-only device buffer.
+class DevBuf {
+ public:
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() { release(); }
+  Status ensure(size_t bytes);
+  void release();
+  template <typename T>
+  T* as() const { return static_cast<T*>(p_); }
+  size_t bytes() const { return bytes_; }
+
+ private:
+  void* p_ = nullptr;
+  size_t bytes_ = 0;
+};
+
+Status cuda_status(cudaError_t e, const char* what);
+
+// One partitioning of n rows into p folds, of which folds [fb, fe) are owned.
+class Plan {
+ public:
+  Status create(cvg_context* ctx, int dtype, int64_t n, int64_t k, int64_t m, int32_t p, int32_t fb, int32_t fe,
+                bool validate);
+  // Device labels -> fold-bucketed row order (validates like partition.hpp:21-58 when `validate`).
+  Status bind_labels(const int32_t* d_labels, bool validate, bool require_scalable);
+  // Explicit ascending rows of the single owned fold (fold_products / precompute_global).
+  Status bind_rows(const int64_t* rows, int64_t nrows);
+  // K1 + K2 + K4.  Exactly one of host_shift / dev_shift may be non-null; both null => row 0.
+  Status gram(const void* d_x, int64_t ldx, const void* d_y, int64_t ldy, const double* host_shift,
+              const double* dev_shift);
+  // Cross-rank combine (optional) + K5 for the owned folds into device outputs.
+  Status finish(const double* d_rank_partials, int32_t n_ranks, const double* total_override,
+                const uint32_t* cfgs, int32_t ncfg, double* d_xtx, double* d_xty, double* d_mean_x,
+                double* d_mean_y, double* d_std_x, double* d_std_y);
+
+  const double* local() const { return local_.as<double>(); }
+  const double* shift() const { return shift_.as<double>(); }
+  int64_t kp() const { return kp_; }
+  int64_t partial_count() const { return kp_ * kp_; }
+  int nown() const { return fe_ - fb_; }
+  const std::vector<int64_t>& counts() const { return counts_; }
+  bool owns_all() const { return fb_ == 0 && fe_ == p_; }
+  int64_t n() const { return n_; }
+  int64_t k() const { return k_; }
+  int64_t m() const { return m_; }
+  int32_t p() const { return p_; }
+  int dtype() const { return dtype_; }
+  cvg_context* ctx() const { return ctx_; }
+  int64_t zrows() const { return zrows_; }
+  int64_t nseg() const { return (int64_t)segs_.size(); }
+  int ntiles() const { return (int)tiles_.size(); }
+
+ private:
+  Status plan_segments();
+  Status count_launch(int n = 1);
+
+  cvg_context* ctx_ = nullptr;
+  int dtype_ = 0;
+  int64_t n_ = 0, k_ = 0, m_ = 0, w_ = 0, kp_ = 0;
+  int32_t p_ = 0, fb_ = 0, fe_ = 0;
+  std::vector<int2> tiles_, out_tiles_;
+  std::vector<int64_t> counts_;  // per fold (all p) validation sizes
+  std::vector<GramTask> segs_;
+  std::vector<int32_t> fold_seg_begin_;
+  std::vector<int64_t> fold_zbase_;
+  int64_t zrows_ = 0;
+  bool bound_ = false, grammed_ = false;
+
+  DevBuf tiles_d_, out_tiles_d_, tile_counts_, fold_counts_, bad_, zbase_d_, src_row_, z_, part_, foldbuf_, local_,
+      total_, shift_, flag_, segs_d_, grp_src_, grp_begin_, grp_dst_, foldptr_d_, nval_d_, rankptr_d_, rankbeg_d_,
+      rankdst_d_, st_mz_, st_sT_, st_sd_, cfg_d_;
+  std::vector<const double*> fold_ptrs_;
+};
+
+// Device scratch of the host-buffer entry point (cvg_run_all_folds), reused across calls.
+struct HostScratch {
+  DevBuf x, y, labels, xtx, xty, mx, my, sx, sy;
+  Plan plan;
+};
+
+}  // namespace cvg
+
+struct cvg_context {
+  int device = 0;
+  cudaStream_t own_stream = nullptr;
+  cudaStream_t stream = nullptr;
+  int64_t launches = 0;
+  std::unique_ptr<cvg::HostScratch> scratch;
+};
+
+struct cvg_plan {
+  cvg::Plan plan;
+};
+
+struct cvg_global {
+  cvg_context* ctx = nullptr;
+  int dtype = 0;
+  int64_t n = 0, k = 0, m = 0;
+  cvg::DevBuf x, y;
+  cvg::Plan all;   // one fold = every row: the whole-data Gram
+  cvg::Plan fold;  // scratch plan for fold_products
+  cvg::DevBuf out_xtx, out_xty, out_vec, cfg_d;
+};

@@ -1,0 +1,139 @@
+// K2: segmented fold Gram in fp64 on the B200 FP64 tensor path (DMMA.8x8x4).
+//
+// For every segment s (<= kChunkRows rows of one fold, contiguous in Z) and
+// every upper tile (ti <= tj) of the kp x kp Gram:
+//     part[s][ti*64 + i][tj*64 + j] = sum_{r in s} Z[r][ti*64 + i] * Z[r][tj*64 + j]
+// This is each validation partition's X_pᵀ[X_p | Y_p | 1] — the reference's
+// per-fold `xv.transpose() * xv / * yv` (fast.hpp:91-92) plus its colwise sums
+// and squares (fast.hpp:95-96, 110-119) — and the whole-data products of
+// precompute_global (fast.hpp:23-24) are the fixed-order sum over folds (K4),
+// so the data is contracted exactly once.  Symmetry: only ti <= tj tiles.
+//
+// Tensor path: sm_100 has no fp64 tcgen05 kind; `mma.sync.m8n8k4.f64` lowers to
+// SASS DMMA.8x8x4, measured at 37.1 TFLOP/s on this B200 (profiles/r01_fp64_peaks.txt).
+// CTA = 64x64 output tile, 8 warps (2 x 4), warp tile 32x16 = 4x2 DMMA tiles.
+// Operands: 32-row x 64-col slabs staged by cp.async (16 B) into a 3-stage ring;
+// the smem row pitch of 68 doubles makes the DMMA fragment loads conflict-free
+// (lanes (g, t) read [t][g]: bank = 2(68t + g) mod 32 covers all 32 banks).
+#include "cvg_internal.cuh"
+
+namespace cvg {
+namespace {
+
+constexpr int BT = kTile;      // 64
+constexpr int KC = kRowStep;   // 32 rows per stage
+constexpr int STAGES = 3;
+constexpr int LDS = BT + 4;    // smem pitch in doubles
+constexpr int NT = 256;
+constexpr int kSlab = KC * LDS;                 // doubles per operand slab
+constexpr int kSmemBytes = STAGES * 2 * kSlab * 8;  // 104,448 B -> 2 CTAs / SM
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+__device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
+__global__ void __launch_bounds__(NT, 2)
+    gram_f64_kernel(const double* __restrict__ z, int64_t kp, const GramTask* __restrict__ segs,
+                    const int2* __restrict__ tiles, int ntiles, double* __restrict__ part) {
+  extern __shared__ __align__(128) double smem[];
+  const int seg = blockIdx.x / ntiles;
+  const int2 tile = tiles[blockIdx.x - seg * ntiles];
+  const int ti = tile.x, tj = tile.y;
+  const bool diag = ti == tj;
+  const GramTask task = segs[seg];
+  const double* zb = z + task.zrow * kp;
+  const int nsteps = (int)(task.rows / KC);
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t4 = lane & 3;
+  const int wi = (warp >> 2) * 32, wj = (warp & 3) * 16;
+
+  auto load_stage = [&](int step, int buf) {
+    const double* src = zb + (int64_t)step * KC * kp;
+    double* dA = smem + buf * 2 * kSlab;
+    double* dB = dA + kSlab;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int idx = tid + q * NT;  // 0..1023: 32 rows x 32 16-byte chunks
+      const int r = idx >> 5, c = (idx & 31) * 2;
+      cp_async16(dA + r * LDS + c, src + (int64_t)r * kp + ti * BT + c);
+      if (!diag) cp_async16(dB + r * LDS + c, src + (int64_t)r * kp + tj * BT + c);
+    }
+  };
+
+  double acc[4][2][2];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 2; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < nsteps) load_stage(s, s);
+    cp_async_commit();
+  }
+  for (int step = 0; step < nsteps; ++step) {
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();
+    {
+      const int nxt = step + STAGES - 1;
+      if (nxt < nsteps) load_stage(nxt, nxt % STAGES);
+      cp_async_commit();
+    }
+    const double* sA = smem + (step % STAGES) * 2 * kSlab;
+    const double* sB = diag ? sA : sA + kSlab;
+#pragma unroll
+    for (int kk = 0; kk < KC; kk += 4) {
+      const double* pa = sA + (kk + t4) * LDS + wi + g;
+      const double* pb = sB + (kk + t4) * LDS + wj + g;
+      double a[4], b[2];
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi) a[mi] = pa[mi * 8];
+#pragma unroll
+      for (int ni = 0; ni < 2; ++ni) b[ni] = pb[ni * 8];
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 2; ++ni) dmma(acc[mi][ni], a[mi], b[ni]);
+    }
+  }
+  cp_async_wait<0>();
+
+  double* out = part + (int64_t)seg * kp * kp;
+#pragma unroll
+  for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < 2; ++ni) {
+      const int64_t row = (int64_t)ti * BT + wi + mi * 8 + g;
+      const int64_t col = (int64_t)tj * BT + wj + ni * 8 + 2 * t4;
+      *reinterpret_cast<double2*>(out + row * kp + col) = make_double2(acc[mi][ni][0], acc[mi][ni][1]);
+    }
+}
+
+}  // namespace
+
+void launch_gram_f64(const double* z, int64_t kp, const GramTask* segs, int64_t nseg, const int2* tiles, int ntiles,
+                     double* part, cudaStream_t s) {
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(gram_f64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+    attr_set = true;
+  }
+  const int64_t blocks = nseg * (int64_t)ntiles;
+  if (blocks <= 0) return;
+  gram_f64_kernel<<<(unsigned)blocks, NT, kSmemBytes, s>>>(z, kp, segs, tiles, ntiles, part);
+}
+
+}  // namespace cvg

@@ -1,0 +1,135 @@
+// Fold bucketing on the device: a stable counting sort of rows by fold label.
+// Replaces build_validation_partitions (partition.hpp:61-68) + gather_rows
+// (partition.hpp:85-90, called at fast.hpp:84-85): instead of P row lists and P
+// gathered copies, every owned fold becomes one contiguous, zero-padded block of
+// the Z matrix, rows in ascending original order (the reference's Algorithm 1
+// order), so the Gram reads each fold with plain sequential tiles.
+//
+// Three passes, all integer work, bit-exact by construction:
+//   1. tile histogram: one warp per 1024-row tile counts its labels (warp
+//      __match_any_sync groups equal labels; the group leader owns the update,
+//      so no atomics and no contention).  Out-of-range labels record the first
+//      offending row (validate_partitioning's first violated clause,
+//      partition.hpp:34-38).
+//   2. per-fold exclusive scan over tiles (one CTA per fold).
+//   3. stable scatter: same warp/tile walk, rank = popc(peers below me).
+#include "cvg_internal.cuh"
+
+namespace cvg {
+namespace {
+
+__global__ void tile_histogram_kernel(const int32_t* __restrict__ labels, int64_t n, int32_t p,
+                                      int32_t* __restrict__ tile_counts, unsigned long long* __restrict__ bad) {
+  const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int64_t row0 = warp * kTileRowsPerWarp;
+  if (row0 >= n) return;
+  int32_t* counts = tile_counts + warp * p;
+  const int64_t row_end = min(n, row0 + kTileRowsPerWarp);
+  for (int64_t base = row0; base < row_end; base += 32) {
+    const int64_t row = base + lane;
+    const bool live = row < row_end;
+    int32_t label = live ? labels[row] : 0;
+    const bool good = live && label >= 1 && label <= p;
+    if (live && !good) atomicMin(bad, (unsigned long long)row);
+    const unsigned act = __ballot_sync(0xffffffffu, good);
+    if (good) {
+      const unsigned peers = __match_any_sync(act, label);
+      if (lane == __ffs(peers) - 1) counts[label - 1] += __popc(peers);
+    }
+    __syncwarp();
+  }
+}
+
+// One CTA per fold: exclusive scan of its tile counts (in place) + fold total.
+__global__ void tile_scan_kernel(int32_t* __restrict__ tile_counts, int64_t ntiles, int32_t p,
+                                 int64_t* __restrict__ fold_counts) {
+  const int32_t f = blockIdx.x;
+  __shared__ int64_t warp_sums[32];
+  const int64_t per = (ntiles + blockDim.x - 1) / blockDim.x;
+  const int64_t t0 = threadIdx.x * per, t1 = min(ntiles, t0 + per);
+  int64_t local = 0;
+  for (int64_t t = t0; t < t1; ++t) local += tile_counts[t * p + f];
+  // block exclusive scan of `local`
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int64_t incl = local;
+  for (int o = 1; o < 32; o <<= 1) {
+    int64_t v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  if (lane == 31) warp_sums[wid] = incl;
+  __syncthreads();
+  if (wid == 0) {
+    const int nw = blockDim.x >> 5;
+    int64_t v = lane < nw ? warp_sums[lane] : 0;
+    for (int o = 1; o < 32; o <<= 1) {
+      int64_t u = __shfl_up_sync(0xffffffffu, v, o);
+      if (lane >= o) v += u;
+    }
+    if (lane < nw) warp_sums[lane] = v;  // inclusive over warps
+  }
+  __syncthreads();
+  int64_t run = (wid ? warp_sums[wid - 1] : 0) + incl - local;
+  for (int64_t t = t0; t < t1; ++t) {
+    const int32_t c = tile_counts[t * p + f];
+    tile_counts[t * p + f] = (int32_t)run;
+    run += c;
+  }
+  if (threadIdx.x == blockDim.x - 1) fold_counts[f] = run;
+}
+
+// Consumes tile_offsets: each warp owns its tile's row of per-fold offsets and
+// advances it as it walks the tile, so ranks stay stable without atomics.
+__global__ void scatter_kernel(const int32_t* __restrict__ labels, int64_t n, int32_t p, int32_t fold_begin,
+                               int32_t fold_end, int32_t* __restrict__ tile_offsets,
+                               const int64_t* __restrict__ fold_zbase, int64_t* __restrict__ src_row) {
+  const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int64_t row0 = warp * kTileRowsPerWarp;
+  if (row0 >= n) return;
+  int32_t* run = tile_offsets + warp * p;
+  const int64_t row_end = min(n, row0 + kTileRowsPerWarp);
+  for (int64_t base = row0; base < row_end; base += 32) {
+    const int64_t row = base + lane;
+    const bool live = row < row_end;
+    const int32_t label = live ? labels[row] : 0;
+    const bool own = live && label > fold_begin && label <= fold_end;
+    const unsigned act = __ballot_sync(0xffffffffu, own);
+    int32_t before = 0;
+    unsigned peers = 0;
+    if (own) {
+      peers = __match_any_sync(act, label);
+      before = run[label - 1];
+      const int rank = __popc(peers & ((1u << lane) - 1u));
+      src_row[fold_zbase[label - 1 - fold_begin] + before + rank] = row;
+    }
+    __syncwarp();
+    if (own && lane == __ffs(peers) - 1) run[label - 1] = before + __popc(peers);
+    __syncwarp();
+  }
+}
+
+}  // namespace
+
+void launch_tile_histogram(const int32_t* labels, int64_t n, int32_t p, int32_t* tile_counts,
+                           unsigned long long* bad, cudaStream_t s) {
+  const int64_t ntiles = (n + kTileRowsPerWarp - 1) / kTileRowsPerWarp;
+  const int threads = 256;
+  const int64_t blocks = (ntiles * 32 + threads - 1) / threads;
+  tile_histogram_kernel<<<(unsigned)blocks, threads, 0, s>>>(labels, n, p, tile_counts, bad);
+}
+
+void launch_tile_scan(int32_t* tile_counts, int64_t ntiles, int32_t p, int64_t* fold_counts, cudaStream_t s) {
+  tile_scan_kernel<<<p, 256, 0, s>>>(tile_counts, ntiles, p, fold_counts);
+}
+
+void launch_scatter(const int32_t* labels, int64_t n, int32_t p, int32_t fold_begin, int32_t fold_end,
+                    int32_t* tile_offsets, const int64_t* fold_zbase, int64_t* src_row, cudaStream_t s) {
+  const int64_t ntiles = (n + kTileRowsPerWarp - 1) / kTileRowsPerWarp;
+  const int threads = 256;
+  const int64_t blocks = (ntiles * 32 + threads - 1) / threads;
+  scatter_kernel<<<(unsigned)blocks, threads, 0, s>>>(labels, n, p, fold_begin, fold_end, tile_offsets, fold_zbase,
+                                                      src_row);
+}
+
+}  // namespace cvg

@@ -1,0 +1,144 @@
+"""Device-resident staged engine (cvg_plan_*) and the multi-GPU driver.
+
+A plan owns a contiguous fold range [fold_begin, fold_end) that is a node of
+the canonical fold-sum tree (``fold_range``).  One process per GPU:
+
+    bind_labels -> gram -> partial --all_gather (NCCL)--> finish
+
+Only the partial (kp x kp doubles: the owned folds' shifted-basis Gram with
+column sums and sums of squares riding in the ones column) crosses GPUs —
+one collective per run, as the north star prescribes.  The all-gather + fixed
+tree combine (instead of a rank-count-dependent all-reduce order) keeps
+results bit-identical for 1, 2, 4 and 8 GPUs.
+
+PyTorch is plumbing here: device buffers, the current stream, and
+torch.distributed for the collective.  No torch types cross the C ABI.
+"""
+from __future__ import annotations
+
+import ctypes
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import _lib as L
+from .cvgram import Context, PreprocessConfig, _cfg, _check, get_context
+
+
+def fold_range(p: int, rank: int, world: int):
+    """Canonical folds [begin, end) of `rank` among `world` (cvg_fold_range)."""
+    b, e = ctypes.c_int32(), ctypes.c_int32()
+    rc = L.lib().cvg_fold_range(p, rank, world, ctypes.addressof(b), ctypes.addressof(e))
+    if rc != L.OK:
+        raise ValueError(f"invalid fold_range({p}, {rank}, {world})")
+    return b.value, e.value
+
+
+def _dptr(t) -> Optional[int]:
+    return None if t is None else int(t.data_ptr())
+
+
+class DevicePlan:
+    """Thin owner of a cvg_plan; arguments are torch CUDA tensors."""
+
+    def __init__(self, n: int, k: int, m: int, p: int, fold_begin: int = 0, fold_end: Optional[int] = None,
+                 dtype: str = "f64", ctx: Optional[Context] = None):
+        import torch
+
+        self.ctx = ctx or get_context()
+        self.n, self.k, self.m, self.p = n, k, m, p
+        self.fold_begin = fold_begin
+        self.fold_end = p if fold_end is None else fold_end
+        self.dtype_code = L.DTYPE_F32 if dtype in ("f32", "float32", torch.float32) else L.DTYPE_F64
+        self.ctx.set_stream(torch.cuda.current_stream(self.ctx.device).cuda_stream)
+        h = ctypes.c_void_p()
+        buf = L.err_buf()
+        _check(L.lib().cvg_plan_create(self.ctx.handle, self.dtype_code, n, k, m, p, self.fold_begin, self.fold_end,
+                                       ctypes.byref(h), buf, len(buf)), buf)
+        self._h = h
+        import weakref
+
+        self._fin = weakref.finalize(self, L.lib().cvg_plan_destroy, h)
+        cnt = ctypes.c_int64()
+        L.lib().cvg_plan_partial(self._h, None, ctypes.byref(cnt))
+        self.partial_count = int(cnt.value)
+
+    @property
+    def n_owned(self) -> int:
+        return self.fold_end - self.fold_begin
+
+    def bind_labels(self, labels, require_scalable: bool) -> None:
+        buf = L.err_buf()
+        _check(L.lib().cvg_plan_bind_labels(self._h, _dptr(labels), int(require_scalable), buf, len(buf)), buf)
+
+    def gram(self, x, y, shift: Optional[np.ndarray] = None) -> None:
+        buf = L.err_buf()
+        sh = None if shift is None else np.ascontiguousarray(shift, np.float64)
+        _check(L.lib().cvg_plan_gram(self._h, _dptr(x), x.stride(0), _dptr(y), y.stride(0),
+                                     None if sh is None else sh.ctypes.data, buf, len(buf)), buf)
+
+    def partial_into(self, dst) -> None:
+        cnt = ctypes.c_int64()
+        rc = L.lib().cvg_plan_partial(self._h, _dptr(dst), ctypes.byref(cnt))
+        if rc != L.OK:
+            raise RuntimeError("cvg_plan_partial failed")
+
+    def finish(self, cfg_masks: Sequence[int], rank_partials=None, n_ranks: int = 1, out=None):
+        import torch
+
+        dev = torch.device("cuda", self.ctx.device)
+        masks = np.ascontiguousarray(cfg_masks, np.uint32)
+        nc, no, k, m = masks.size, self.n_owned, self.k, self.m
+        if out is None:
+            f64 = torch.float64
+            out = {"xtx": torch.empty((nc, no, k, k), dtype=f64, device=dev),
+                   "xty": torch.empty((nc, no, k, m), dtype=f64, device=dev),
+                   "mean_x": torch.empty((no, k), dtype=f64, device=dev),
+                   "mean_y": torch.empty((no, m), dtype=f64, device=dev),
+                   "std_x": torch.empty((no, k), dtype=f64, device=dev),
+                   "std_y": torch.empty((no, m), dtype=f64, device=dev)}
+        buf = L.err_buf()
+        _check(L.lib().cvg_plan_finish(self._h, _dptr(rank_partials), n_ranks, masks.ctypes.data, nc,
+                                       _dptr(out["xtx"]), _dptr(out["xty"]), _dptr(out.get("mean_x")),
+                                       _dptr(out.get("mean_y")), _dptr(out.get("std_x")), _dptr(out.get("std_y")),
+                                       buf, len(buf)), buf)
+        return out
+
+    def fold_counts(self) -> np.ndarray:
+        c = np.empty(self.p, np.int64)
+        L.lib().cvg_plan_fold_counts(self._h, c.ctypes.data)
+        return c
+
+
+def run_all_folds_device(x, y, labels, p: int, cfgs, group=None, plan: Optional[DevicePlan] = None,
+                         shift: Optional[np.ndarray] = None):
+    """All folds of `labels` on device-resident x/y/labels (torch CUDA tensors).
+
+    With a torch.distributed process group of size G > 1, this rank computes
+    only its canonical fold range and the ranks exchange one partial Gram by
+    all-gather.  Returns (plan, outputs) where outputs hold the owned folds.
+    Every rank must pass the same `shift` (default: row 0 of the full x | y).
+    """
+    import torch
+    import torch.distributed as dist
+
+    cfgs = [_cfg(c) for c in cfgs]
+    masks = [c.mask for c in cfgs]
+    world = dist.get_world_size(group) if (group is not None or (dist.is_available() and dist.is_initialized())) else 1
+    rank = dist.get_rank(group) if world > 1 else 0
+    n, k = x.shape
+    m = y.shape[1]
+    if plan is None:
+        fb, fe = fold_range(p, rank, world)
+        plan = DevicePlan(n, k, m, p, fb, fe, dtype="f32" if x.dtype == torch.float32 else "f64")
+    plan.bind_labels(labels, require_scalable=any(c.any_scale() for c in cfgs))
+    plan.gram(x, y, shift)
+    if world > 1:
+        mine = torch.empty(plan.partial_count, dtype=torch.float64, device=x.device)
+        plan.partial_into(mine)
+        gathered = torch.empty(world * plan.partial_count, dtype=torch.float64, device=x.device)
+        dist.all_gather_into_tensor(gathered, mine, group=group)
+        out = plan.finish(masks, gathered, world)
+    else:
+        out = plan.finish(masks)
+    return plan, out

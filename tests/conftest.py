@@ -1,0 +1,36 @@
+import os
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+HERE = os.path.dirname(os.path.abspath(__file__))
+if HERE not in sys.path:
+    sys.path.insert(0, HERE)
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a B200 (sm_100a) device")
+    config.addinivalue_line("markers", "slow: long-running parity case")
+
+
+@pytest.fixture(scope="session", autouse=True)
+def _built():
+    """Build the engine and the oracle once (nvcc cross-compiles without a GPU)."""
+    import __graft_entry__
+
+    __graft_entry__.build()
+
+
+def _engine_params():
+    return ["oracle", pytest.param("gpu", marks=pytest.mark.gpu)]
+
+
+@pytest.fixture(params=_engine_params())
+def engine(request):
+    """The same reference-shaped API backed by the CPU oracle or the B200 engine."""
+    import engines
+
+    return engines.make(request.param)
