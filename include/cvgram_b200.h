@@ -55,6 +55,14 @@ void cvg_context_destroy(cvg_context* ctx);
 int cvg_context_set_stream(cvg_context* ctx, void* stream);
 /* Number of kernels this context has launched (for the bench's gpu_launches). */
 int64_t cvg_context_launch_count(const cvg_context* ctx);
+/* Per-kernel-class device timing with CUDA events on the launching stream.
+ * Classes: 0 bucketing, 1 reorder (K1), 2 fold Gram (K2), 3 tree sums (K4),
+ * 4 fold stats, 5 products (K5).  enable != 0 starts recording (and clears);
+ * cvg_context_kernel_times synchronizes and returns total ms and launch counts
+ * per class (arrays of CVG_KERNEL_CLASSES). */
+#define CVG_KERNEL_CLASSES 6
+int cvg_context_enable_timing(cvg_context* ctx, int enable);
+int cvg_context_kernel_times(cvg_context* ctx, double* ms, int64_t* launches);
 
 /* ------------------------------------------------- host validation (no GPU) */
 /* DatasetPair invariants, core.hpp:37-45. */

@@ -27,6 +27,8 @@ SIGNATURES = {
     "cvg_context_destroy": (None, [c_vp]),
     "cvg_context_set_stream": (c_int, [c_vp, c_vp]),
     "cvg_context_launch_count": (c_i64, [c_vp]),
+    "cvg_context_enable_timing": (c_int, [c_vp, c_int]),
+    "cvg_context_kernel_times": (c_int, [c_vp, c_vp, c_vp]),
     "cvg_validate_dataset": (c_int, [c_vp, c_vp, c_i64, c_i64, c_i64, c_i64, c_char_p, c_size_t]),
     "cvg_validate_partitioning": (c_int, [c_vp, c_i64, c_i32, c_char_p, c_size_t]),
     "cvg_check_scalable": (c_int, [c_vp, c_i64, c_i32, c_char_p, c_size_t]),

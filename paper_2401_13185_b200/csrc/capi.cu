@@ -170,6 +170,8 @@ void cvg_context_destroy(cvg_context* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
+  ctx->clear_recs();
+  for (cudaEvent_t e : ctx->event_pool) cudaEventDestroy(e);
   ctx->scratch.reset();
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
   delete ctx;
@@ -182,6 +184,30 @@ int cvg_context_set_stream(cvg_context* ctx, void* stream) {
 }
 
 int64_t cvg_context_launch_count(const cvg_context* ctx) { return ctx ? ctx->launches : 0; }
+
+int cvg_context_enable_timing(cvg_context* ctx, int enable) {
+  if (!ctx) return CVG_E_INVALID_ARG;
+  cudaStreamSynchronize(ctx->stream);
+  ctx->clear_recs();
+  ctx->timing = enable != 0;
+  return CVG_OK;
+}
+
+int cvg_context_kernel_times(cvg_context* ctx, double* ms, int64_t* launches) {
+  if (!ctx) return CVG_E_INVALID_ARG;
+  for (int i = 0; i < CVG_KERNEL_CLASSES; ++i) {
+    if (ms) ms[i] = 0.0;
+    if (launches) launches[i] = 0;
+  }
+  for (auto& r : ctx->recs) {
+    if (cudaEventSynchronize(r.b) != cudaSuccess) return CVG_E_CUDA;
+    float t = 0.f;
+    if (cudaEventElapsedTime(&t, r.a, r.b) != cudaSuccess) return CVG_E_CUDA;
+    if (ms) ms[r.cls] += t;
+    if (launches) launches[r.cls] += 1;
+  }
+  return CVG_OK;
+}
 
 int cvg_validate_dataset(const double* x, const double* y, int64_t n, int64_t k, int64_t m, int64_t y_rows,
                          char* err, size_t errlen) {

@@ -13,6 +13,33 @@
 
 #include "engine.cuh"
 
+cudaEvent_t cvg_context::take_event() {
+  if (!event_pool.empty()) {
+    cudaEvent_t e = event_pool.back();
+    event_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+
+void cvg_context::begin(int cls) {
+  Rec r{cls, take_event(), take_event()};
+  cudaEventRecord(r.a, stream);
+  recs.push_back(r);
+}
+
+void cvg_context::end() { cudaEventRecord(recs.back().b, stream); }
+
+void cvg_context::clear_recs() {
+  for (auto& r : recs) {
+    event_pool.push_back(r.a);
+    event_pool.push_back(r.b);
+  }
+  recs.clear();
+}
+
 namespace cvg {
 
 Status cuda_status(cudaError_t e, const char* what) {
@@ -116,9 +143,15 @@ Status Plan::bind_labels(const int32_t* d_labels, bool validate, bool require_sc
   CVG_TRY(bad_.ensure(sizeof(unsigned long long)));
   CVG_CK(cudaMemsetAsync(tile_counts_.as<void>(), 0, sizeof(int32_t) * ntiles * p_, s));
   CVG_CK(cudaMemsetAsync(bad_.as<void>(), 0xff, sizeof(unsigned long long), s));
-  launch_tile_histogram(d_labels, n_, p_, tile_counts_.as<int32_t>(), bad_.as<unsigned long long>(), s);
+  {
+    Timed t(ctx_, kBucket);
+    launch_tile_histogram(d_labels, n_, p_, tile_counts_.as<int32_t>(), bad_.as<unsigned long long>(), s);
+  }
   CVG_TRY(count_launch());
-  launch_tile_scan(tile_counts_.as<int32_t>(), ntiles, p_, fold_counts_.as<int64_t>(), s);
+  {
+    Timed t(ctx_, kBucket);
+    launch_tile_scan(tile_counts_.as<int32_t>(), ntiles, p_, fold_counts_.as<int64_t>(), s);
+  }
   CVG_TRY(count_launch());
   counts_.assign(p_, 0);
   unsigned long long bad = 0;
@@ -143,8 +176,11 @@ Status Plan::bind_labels(const int32_t* d_labels, bool validate, bool require_sc
   }
   CVG_TRY(plan_segments());
   CVG_CK(cudaMemsetAsync(src_row_.as<void>(), 0xff, sizeof(int64_t) * std::max<int64_t>(zrows_, 1), s));
-  launch_scatter(d_labels, n_, p_, fb_, fe_, tile_counts_.as<int32_t>(), zbase_d_.as<int64_t>(),
-                 src_row_.as<int64_t>(), s);
+  {
+    Timed t(ctx_, kBucket);
+    launch_scatter(d_labels, n_, p_, fb_, fe_, tile_counts_.as<int32_t>(), zbase_d_.as<int64_t>(),
+                   src_row_.as<int64_t>(), s);
+  }
   CVG_TRY(count_launch());
   bound_ = true;
   return Status::Ok();
@@ -254,18 +290,25 @@ Status Plan::gram(const void* d_x, int64_t ldx, const void* d_y, int64_t ldy, co
     CVG_CK(cudaMemcpyAsync(shift, host_shift, sizeof(double) * w_, cudaMemcpyHostToDevice, s));
     CVG_CK(cudaStreamSynchronize(s));
   } else {
+    Timed t(ctx_, kReorder);
     launch_shift_from_row0(dtype_, d_x, d_y, k_, m_, shift, s);
     CVG_TRY(count_launch());
   }
   CVG_CK(cudaMemsetAsync(flag_.as<void>(), 0, sizeof(int), s));
   if (zrows_ > 0) {
-    launch_reorder(dtype_, d_x, ldx, d_y, ldy, k_, m_, src_row_.as<int64_t>(), zrows_, kp_, shift, z_.as<double>(),
-                   flag_.as<int>(), s);
+    {
+      Timed t(ctx_, kReorder);
+      launch_reorder(dtype_, d_x, ldx, d_y, ldy, k_, m_, src_row_.as<int64_t>(), zrows_, kp_, shift,
+                     z_.as<double>(), flag_.as<int>(), s);
+    }
     CVG_TRY(count_launch());
   }
   if (!segs_.empty()) {
-    launch_gram_f64(z_.as<double>(), kp_, segs_d_.as<GramTask>(), (int64_t)segs_.size(), tiles_d_.as<int2>(),
-                    (int)tiles_.size(), part_.as<double>(), s);
+    {
+      Timed t(ctx_, kGram);
+      launch_gram_f64(z_.as<double>(), kp_, segs_d_.as<GramTask>(), (int64_t)segs_.size(), tiles_d_.as<int2>(),
+                      (int)tiles_.size(), part_.as<double>(), s);
+    }
     CVG_TRY(count_launch());
   }
   const int nown = fe_ - fb_;
@@ -276,10 +319,14 @@ Status Plan::gram(const void* d_x, int64_t ldx, const void* d_y, int64_t ldy, co
   double* const* dsts = grp_dst_.as<double*>();
   const int32_t* beg = grp_begin_.as<int32_t>();
   if (nmulti > 0) {
+    Timed t(ctx_, kTree);
     launch_tree_sum(srcs, beg, nmulti, dsts, kp_, tiles_d_.as<int2>(), (int)tiles_.size(), s);
     CVG_TRY(count_launch());
   }
-  launch_tree_sum(srcs, beg + nmulti, 1, dsts + nmulti, kp_, tiles_d_.as<int2>(), (int)tiles_.size(), s);
+  {
+    Timed t(ctx_, kTree);
+    launch_tree_sum(srcs, beg + nmulti, 1, dsts + nmulti, kp_, tiles_d_.as<int2>(), (int)tiles_.size(), s);
+  }
   CVG_TRY(count_launch());
   grammed_ = true;
   return Status::Ok();
@@ -305,8 +352,11 @@ Status Plan::finish(const double* d_rank_partials, int32_t n_ranks, const double
     CVG_CK(cudaMemcpyAsync(rankptr_d_.as<void>(), src.data(), sizeof(void*) * n_ranks, cudaMemcpyHostToDevice, s));
     CVG_CK(cudaMemcpyAsync(rankbeg_d_.as<void>(), beg.data(), sizeof(int32_t) * 2, cudaMemcpyHostToDevice, s));
     CVG_CK(cudaMemcpyAsync(rankdst_d_.as<void>(), &dst, sizeof(void*), cudaMemcpyHostToDevice, s));
-    launch_tree_sum(rankptr_d_.as<const double*>(), rankbeg_d_.as<int32_t>(), 1, rankdst_d_.as<double*>(), kp_,
-                    tiles_d_.as<int2>(), (int)tiles_.size(), s);
+    {
+      Timed t(ctx_, kTree);
+      launch_tree_sum(rankptr_d_.as<const double*>(), rankbeg_d_.as<int32_t>(), 1, rankdst_d_.as<double*>(), kp_,
+                      tiles_d_.as<int2>(), (int)tiles_.size(), s);
+    }
     CVG_TRY(count_launch());
     CVG_CK(cudaStreamSynchronize(s));  // host pointer vectors above are temporaries
     total = dst;
@@ -322,15 +372,21 @@ Status Plan::finish(const double* d_rank_partials, int32_t n_ranks, const double
   CVG_TRY(st_sT_.ensure(sizeof(double) * nown * w_));
   CVG_TRY(st_sd_.ensure(sizeof(double) * nown * w_));
   FoldStatsDev st{st_mz_.as<double>(), st_sT_.as<double>(), st_sd_.as<double>()};
-  launch_fold_stats(total, foldptr_d_.as<const double*>(), nval_d_.as<int64_t>(), nown, n_, k_, m_, kp_,
-                    shift_.as<double>(), st, d_mean_x, d_mean_y, d_std_x, d_std_y, s);
+  {
+    Timed t(ctx_, kStats);
+    launch_fold_stats(total, foldptr_d_.as<const double*>(), nval_d_.as<int64_t>(), nown, n_, k_, m_, kp_,
+                      shift_.as<double>(), st, d_mean_x, d_mean_y, d_std_x, d_std_y, s);
+  }
   CVG_TRY(count_launch());
   if (ncfg > 0) {
     CVG_TRY(cfg_d_.ensure(sizeof(uint32_t) * ncfg));
     CVG_CK(cudaMemcpyAsync(cfg_d_.as<void>(), cfgs, sizeof(uint32_t) * ncfg, cudaMemcpyHostToDevice, s));
-    launch_products(total, foldptr_d_.as<const double*>(), nval_d_.as<int64_t>(), nown, n_, k_, m_, kp_,
-                    shift_.as<double>(), st, out_tiles_d_.as<int2>(), (int)out_tiles_.size(), cfg_d_.as<uint32_t>(),
-                    ncfg, d_xtx, d_xty, s);
+    {
+      Timed t(ctx_, kProducts);
+      launch_products(total, foldptr_d_.as<const double*>(), nval_d_.as<int64_t>(), nown, n_, k_, m_, kp_,
+                      shift_.as<double>(), st, out_tiles_d_.as<int2>(), (int)out_tiles_.size(),
+                      cfg_d_.as<uint32_t>(), ncfg, d_xtx, d_xty, s);
+    }
     CVG_TRY(count_launch());
   }
   int flag = 0;

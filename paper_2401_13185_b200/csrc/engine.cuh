@@ -101,7 +101,36 @@ struct cvg_context {
   cudaStream_t stream = nullptr;
   int64_t launches = 0;
   std::unique_ptr<cvg::HostScratch> scratch;
+  // optional per-class kernel timing (cvg_context_enable_timing)
+  bool timing = false;
+  struct Rec {
+    int cls;
+    cudaEvent_t a, b;
+  };
+  std::vector<Rec> recs;
+  std::vector<cudaEvent_t> event_pool;
+  cudaEvent_t take_event();
+  void begin(int cls);
+  void end();
+  void clear_recs();
 };
+
+namespace cvg {
+enum KernelClass { kBucket = 0, kReorder = 1, kGram = 2, kTree = 3, kStats = 4, kProducts = 5, kClasses = 6 };
+// Records CUDA events around one launch when the context is timing.
+class Timed {
+ public:
+  Timed(cvg_context* c, int cls) : c_(c) {
+    if (c_->timing) c_->begin(cls);
+  }
+  ~Timed() {
+    if (c_->timing) c_->end();
+  }
+
+ private:
+  cvg_context* c_;
+};
+}  // namespace cvg
 
 struct cvg_plan {
   cvg::Plan plan;

@@ -142,3 +142,15 @@ def run_all_folds_device(x, y, labels, p: int, cfgs, group=None, plan: Optional[
     else:
         out = plan.finish(masks)
     return plan, out
+
+
+def gram_tiles(k: int, m: int):
+    """Upper 64x64 tiles the fold Gram computes (mirror of engine.cu gram_tiles)."""
+    kp = -(-(k + m + 1) // 64) * 64
+    nt, tx, to = kp // 64, (k - 1) // 64, (k + m) // 64
+    return [(i, j) for i in range(nt) for j in range(i, nt) if i <= tx or j == i or j == to]
+
+
+def executed_gram_flops(n: int, k: int, m: int, p: int) -> float:
+    """DMMA flops the Gram kernel issues for n rows (fold padding ignored)."""
+    return 2.0 * len(gram_tiles(k, m)) * 64 * 64 * n
