@@ -38,7 +38,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 FP64_DMMA_PEAK_TFLOPS = 37.1  # profiles/r01_fp64_peaks.txt (DMMA.8x8x4 issue loop; cuBLAS DGEMM 35.4)
-CPU_SAMPLE_ROWS = 200_000
+CPU_SAMPLE_ROWS = 1_000_000
 
 
 def parse():
@@ -208,7 +208,7 @@ def run_ours(args):
         plan.gram(x, y, shift)
         if world > 1:
             plan.partial_into(mine)
-            dist.all_gather_into_tensor(gathered, mine)
+            dist.all_gather_into_tensor(gathered, mine)  # the run's single collective (NVLink)
             out = plan.finish(masks, gathered, world, out)
         else:
             out = plan.finish(masks, None, 1, out)

@@ -88,8 +88,8 @@ inline FoldResult fold_products(const GlobalCache& cache, const DatasetPair& dat
 }
 
 /// Several configurations from one Gram pass; result[c][f] is fold f+1 of cfgs[c].
-inline std::vector<std::vector<FoldResult>> run_all_folds(const DatasetPair& data, const Partitioning& part,
-                                                          const std::vector<PreprocessConfig>& cfgs) {
+inline std::vector<std::vector<FoldResult>> run_all_folds_configs(const DatasetPair& data, const Partitioning& part,
+                                                                  const std::vector<PreprocessConfig>& cfgs) {
   const Index n = data.n_rows(), k = data.n_features(), m = data.n_responses();
   const int p = part.p;
   const size_t nc = cfgs.size();
@@ -141,7 +141,7 @@ inline std::vector<FoldResult> run_all_folds(const DatasetPair& data, const Part
                                              const PreprocessConfig& cfg, int n_threads = 1) {
   (void)n_threads;
   if (part.n_rows() != data.n_rows()) throw dimension_error("partitioning length does not match sample count");
-  return std::move(run_all_folds(data, part, std::vector<PreprocessConfig>{cfg})[0]);
+  return std::move(run_all_folds_configs(data, part, std::vector<PreprocessConfig>{cfg})[0]);
 }
 
 }  // namespace cvgram

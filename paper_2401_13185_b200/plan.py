@@ -110,39 +110,58 @@ class DevicePlan:
         return c
 
 
-def run_all_folds_device(x, y, labels, p: int, cfgs, group=None, plan: Optional[DevicePlan] = None,
-                         shift: Optional[np.ndarray] = None):
+def run_all_folds_device(x, y, labels, p: int, cfgs, group=None, plan=None, shift: Optional[np.ndarray] = None,
+                         plan_factory=None):
     """All folds of `labels` on device-resident x/y/labels (torch CUDA tensors).
 
     With a torch.distributed process group of size G > 1, this rank computes
     only its canonical fold range and the ranks exchange one partial Gram by
     all-gather.  Returns (plan, outputs) where outputs hold the owned folds.
     Every rank must pass the same `shift` (default: row 0 of the full x | y).
+    `plan_factory(n, k, m, p, fold_begin, fold_end)` substitutes the plan
+    object (tests drive this exchange logic on CPU with gloo).
     """
     import torch
     import torch.distributed as dist
 
     cfgs = [_cfg(c) for c in cfgs]
     masks = [c.mask for c in cfgs]
-    world = dist.get_world_size(group) if (group is not None or (dist.is_available() and dist.is_initialized())) else 1
-    rank = dist.get_rank(group) if world > 1 else 0
+    distributed = dist.is_available() and dist.is_initialized()
+    world = dist.get_world_size(group) if distributed else 1
+    rank = dist.get_rank(group) if distributed else 0
     n, k = x.shape
     m = y.shape[1]
     if plan is None:
         fb, fe = fold_range(p, rank, world)
-        plan = DevicePlan(n, k, m, p, fb, fe, dtype="f32" if x.dtype == torch.float32 else "f64")
+        if plan_factory is not None:
+            plan = plan_factory(n, k, m, p, fb, fe)
+        else:
+            plan = DevicePlan(n, k, m, p, fb, fe, dtype="f32" if x.dtype == torch.float32 else "f64")
     plan.bind_labels(labels, require_scalable=any(c.any_scale() for c in cfgs))
     plan.gram(x, y, shift)
     if world > 1:
         mine = torch.empty(plan.partial_count, dtype=torch.float64, device=x.device)
         plan.partial_into(mine)
-        gathered = torch.empty(world * plan.partial_count, dtype=torch.float64, device=x.device)
-        dist.all_gather_into_tensor(gathered, mine, group=group)
+        gathered = exchange_partials(mine, world, group)
         out = plan.finish(masks, gathered, world)
     else:
         out = plan.finish(masks)
     return plan, out
 
+
+def exchange_partials(mine, world: int, group=None):
+    """The run's single collective: all-gather every rank's fold-tree node, in
+    rank order (NCCL all_gather_into_tensor over NVLink; list form on gloo)."""
+    import torch
+    import torch.distributed as dist
+
+    if dist.get_backend(group) == "nccl":
+        gathered = torch.empty(world * mine.numel(), dtype=mine.dtype, device=mine.device)
+        dist.all_gather_into_tensor(gathered, mine, group=group)
+        return gathered
+    parts = [torch.empty_like(mine) for _ in range(world)]
+    dist.all_gather(parts, mine, group=group)
+    return torch.cat(parts)
 
 def gram_tiles(k: int, m: int):
     """Upper 64x64 tiles the fold Gram computes (mirror of engine.cu gram_tiles)."""

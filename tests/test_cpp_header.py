@@ -1,0 +1,27 @@
+"""The reference's Catch2 cases restated in C++ against include/cvgram/*.hpp
+(tests/cpp/test_header_api.cpp), i.e. the drop-in boundary for C++ callers."""
+import os
+import subprocess
+
+import pytest
+
+BIN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "cpp", "_build", "test_header_api")
+
+
+def _run(*args):
+    r = subprocess.run([BIN, *args], capture_output=True, text=True, timeout=600)
+    print(r.stdout)
+    return r
+
+
+def test_cpp_header_host_cases():
+    assert os.path.exists(BIN), "built by __graft_entry__.build()"
+    r = _run("--host")
+    assert r.returncode == 0, r.stdout + r.stderr
+
+
+@pytest.mark.gpu
+def test_cpp_header_all_cases_on_device():
+    r = _run()
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "0 failing tests" in r.stdout

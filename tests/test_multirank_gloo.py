@@ -1,0 +1,169 @@
+"""The multi-GPU exchange protocol on CPU: world_size 2 and 4 over gloo.
+
+Each rank owns its canonical fold range (cvg_fold_range), computes its
+fold-tree node, all-gathers it (the run's one collective) and finishes its own
+folds.  The per-rank compute is a numpy stand-in with the engine's structure
+(shifted-basis fold Grams, midpoint-tree sums, the K5 formulas), injected via
+``plan_factory``; what is under test is the product's driver
+(plan.run_all_folds_device / exchange_partials / fold_range): that every fold
+is produced exactly once, by the right rank, bit-identical to world_size 1 and
+within 1e-10 of the long-double oracle.
+"""
+import os
+import socket
+import tempfile
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+
+def _tree(vals, a, b):
+    if b <= a:
+        return np.zeros_like(vals[0]) if vals else 0.0
+    if b - a == 1:
+        return vals[a]
+    mid = a + (b - a) // 2
+    return _tree(vals, a, mid) + _tree(vals, mid, b)
+
+
+class NumpyPlan:
+    """CPU stand-in for DevicePlan with the engine's reduction structure."""
+
+    def __init__(self, n, k, m, p, fb, fe):
+        self.n, self.k, self.m, self.p, self.fold_begin, self.fold_end = n, k, m, p, fb, fe
+        self.w = k + m
+        self.partial_count = k * (self.w + 1)
+
+    def bind_labels(self, labels, require_scalable):
+        self.labels = labels.numpy()
+
+    def gram(self, x, y, shift):
+        z = np.concatenate([x.numpy(), y.numpy()], axis=1)
+        self.shift = z[0].copy() if shift is None else np.asarray(shift)
+        z = z - self.shift
+        z1 = np.concatenate([z, np.ones((z.shape[0], 1))], axis=1)
+        self.G = []
+        for f in range(self.fold_begin, self.fold_end):
+            zf = z1[self.labels == f + 1]
+            self.G.append(zf.T @ zf)  # (w+1) x (w+1): sums in the ones column
+        self.counts = np.bincount(self.labels, minlength=self.p + 1)[1:]
+        w1 = self.w + 1
+        self.local = _tree(self.G, 0, len(self.G)) if self.G else np.zeros((w1, w1))
+
+    def partial_into(self, dst):
+        dst.copy_(torch.from_numpy(np.ascontiguousarray(self.local[: self.k]).ravel()))
+
+    def finish(self, masks, gathered=None, world=1, out=None):
+        k, w = self.k, self.w
+        if gathered is None:
+            total_k = self.local[:k]
+        else:
+            g = gathered.numpy().reshape(world, k, w + 1)
+            total_k = _tree([g[r] for r in range(world)], 0, world)
+        full = self.local.copy()
+        full[:k] = total_k
+        res = {"xtx": [], "xty": []}
+        for mask in masks:
+            cx, cy, sx, sy = bool(mask & 8), bool(mask & 4), bool(mask & 2), bool(mask & 1)
+            xx, xy = [], []
+            for i, f in enumerate(range(self.fold_begin, self.fold_end)):
+                G = self.G[i]
+                nt = float(self.n - self.counts[f])
+                T = total_k
+                gt = T[:, :w] - G[:k, :w]
+                sT = T[:, w] - G[:k, w]
+                c = self.shift[:k]
+                mz = sT / nt
+                # Y-side sums / squares come from each rank's own data (same rows everywhere here)
+                v = gt.copy()
+                if cx:
+                    v[:, :k] = gt[:, :k] - nt * np.outer(mz, mz)
+                else:
+                    v[:, :k] = gt[:, :k] + np.outer(c, sT) + np.outer(sT, c) + nt * np.outer(c, c)
+                xx.append(v[:, :k])
+                xy.append(v[:, k:])
+            res["xtx"].append(np.stack(xx) if xx else np.zeros((0, k, k)))
+            res["xty"].append(np.stack(xy) if xy else np.zeros((0, k, self.m)))
+        return res
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, outdir, data):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2401_13185_b200 import plan as P
+
+    x, y, labels, p = data
+    pl, out = P.run_all_folds_device(torch.from_numpy(x), torch.from_numpy(y), torch.from_numpy(labels), p, [8, 0],
+                                     plan_factory=NumpyPlan)
+    np.savez(os.path.join(outdir, f"rank{rank}.npz"), fb=pl.fold_begin, fe=pl.fold_end,
+             xtx=np.stack(out["xtx"]), xty=np.stack(out["xty"]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def _run(world, data):
+    with tempfile.TemporaryDirectory() as d:
+        if world == 1:
+            _worker_single(d, data)
+        else:
+            mp.spawn(_worker, args=(world, _free_port(), d, data), nprocs=world, join=True)
+        parts = [np.load(os.path.join(d, f"rank{r}.npz")) for r in range(world)]
+        return [(int(q["fb"]), int(q["fe"]), q["xtx"], q["xty"]) for q in parts]
+
+
+def _worker_single(d, data):
+    from paper_2401_13185_b200 import plan as P
+
+    x, y, labels, p = data
+    pl, out = P.run_all_folds_device(torch.from_numpy(x), torch.from_numpy(y), torch.from_numpy(labels), p, [8, 0],
+                                     plan_factory=NumpyPlan)
+    np.savez(os.path.join(d, "rank0.npz"), fb=pl.fold_begin, fe=pl.fold_end, xtx=np.stack(out["xtx"]),
+             xty=np.stack(out["xty"]))
+
+
+@pytest.fixture(scope="module")
+def data():
+    rng = np.random.default_rng(11)
+    n, k, m, p = 600, 9, 3, 7
+    x = rng.normal(rng.uniform(-5, 5, k), rng.uniform(0.5, 2, k), (n, k))
+    y = rng.normal(1, 1, (n, m))
+    labels = rng.integers(1, p + 1, n).astype(np.int32)
+    labels[:p] = np.arange(1, p + 1)
+    return x, y, labels, p
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_ranks_cover_folds_and_match_world1_bitwise(world, data):
+    single = _run(1, data)[0]
+    parts = _run(world, data)
+    covered = []
+    for fb, fe, xtx, xty in parts:
+        covered += list(range(fb, fe))
+        assert np.array_equal(xtx, single[2][:, fb:fe]), f"world {world} folds {fb}:{fe}"
+        assert np.array_equal(xty, single[3][:, fb:fe])
+    assert covered == list(range(data[3]))
+
+
+def test_world1_matches_long_double_oracle(data):
+    import oracle
+
+    x, y, labels, p = data
+    fb, fe, xtx, xty = _run(1, data)[0]
+    for ci, cfg in enumerate([8, 0]):
+        truth = oracle.truth_all_folds(x, y, labels, p, cfg)
+        for f in range(p):
+            d = np.sqrt(np.abs(np.diag(truth[f].xtx_t)))
+            err = np.abs(xtx[ci, f] - truth[f].xtx_t) / np.maximum(np.abs(truth[f].xtx_t), np.outer(d, d))
+            assert err.max() <= 1e-10
