@@ -82,7 +82,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "20"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
         except Exception:
@@ -213,6 +213,7 @@ def run_ours(args):
         else:
             out = plan.finish(masks, None, 1, out)
 
+    clocks = ClockSampler(local).__enter__()  # sampled over warm-up + timed steps (GPU busy throughout)
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize(dev)
@@ -221,13 +222,14 @@ def run_ours(args):
     L.lib().cvg_context_enable_timing(ctx.handle, 1)
     launches0 = ctx.launches
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clocks:
+    if True:
         torch.cuda.synchronize(dev)
         e0.record(stream)
         for _ in range(args.steps):
             step()
         e1.record(stream)
         torch.cuda.synchronize(dev)
+    clocks.__exit__()
     ms = e0.elapsed_time(e1) / args.steps
     launches = ctx.launches - launches0
     kms = np.zeros(6)

@@ -57,9 +57,14 @@ struct GramTask {
 void launch_gram_f64(const double* z, int64_t kp, const GramTask* segs, int64_t nseg, const int2* tiles,
                      int ntiles, double* part, cudaStream_t s);
 
-// K4: fixed-order (midpoint-tree) sums of kp x kp matrices over upper tiles.
-void launch_tree_sum(const double* const* srcs, const int32_t* src_begin, int ngroups, double* const* dsts,
-                     int64_t kp, const int2* tiles, int ntiles, cudaStream_t s);
+// K4: fixed-order (midpoint-tree) sums of kp x kp matrices over upper tiles,
+// one launch per tree level.  d = a + b; b == null copies a; a == null zeroes d.
+struct PairOp {
+  const double* a;
+  const double* b;
+  double* d;
+};
+void launch_pair_sums(const PairOp* ops, int nops, int64_t kp, const int2* tiles, int ntiles, cudaStream_t s);
 
 // K5: epilogue.
 struct FoldStatsDev {
@@ -69,7 +74,7 @@ struct FoldStatsDev {
 };
 void launch_fold_stats(const double* total, const double* const* foldG, const int64_t* n_val, int nfold, int64_t n,
                        int64_t k, int64_t m, int64_t kp, const double* shift, FoldStatsDev st, double* mean_x,
-                       double* mean_y, double* std_x, double* std_y, cudaStream_t s);
+                       double* mean_y, double* std_x, double* std_y, int* nonfinite, cudaStream_t s);
 void launch_products(const double* total, const double* const* foldG, const int64_t* n_val, int nfold, int64_t n,
                      int64_t k, int64_t m, int64_t kp, const double* shift, FoldStatsDev st, const int2* tiles,
                      int ntiles, const uint32_t* cfgs, int ncfg, double* xtx, double* xty, cudaStream_t s);

@@ -91,6 +91,58 @@ std::vector<int2> gram_tiles(int64_t k, int64_t m, int64_t kp) {
   return t;
 }
 
+const double* TreeProgram::emit(const std::vector<const double*>& leaves, int a, int b, int depth, double* root_dst,
+                                std::vector<std::vector<PairOp>>& by_depth, int64_t kp) {
+  if ((int)by_depth.size() <= depth) by_depth.resize(depth + 1);
+  if (b - a <= 1 && !root_dst) return leaves[a];  // interior leaf: read in place
+  double* out = root_dst ? root_dst : scratch_.as<double>() + (next_slot_++) * kp * kp;
+  if (b - a == 0) {
+    by_depth[depth].push_back(PairOp{nullptr, nullptr, out});
+  } else if (b - a == 1) {
+    by_depth[depth].push_back(PairOp{leaves[a], nullptr, out});
+  } else {
+    const int mid = a + (b - a) / 2;
+    const double* l = emit(leaves, a, mid, depth + 1, nullptr, by_depth, kp);
+    const double* r = emit(leaves, mid, b, depth + 1, nullptr, by_depth, kp);
+    by_depth[depth].push_back(PairOp{l, r, out});
+  }
+  return out;
+}
+
+Status TreeProgram::build(const std::vector<TreeGroup>& groups, int64_t kp, cudaStream_t s) {
+  int64_t slots = 0;  // internal nodes other than each group's root
+  for (const auto& g : groups) slots += std::max<int64_t>((int64_t)g.leaves.size() - 2, 0);
+  CVG_TRY(scratch_.ensure(sizeof(double) * std::max<int64_t>(slots, 1) * kp * kp));
+  next_slot_ = 0;
+  std::vector<std::vector<PairOp>> by_depth;
+  for (const auto& g : groups) emit(g.leaves, 0, (int)g.leaves.size(), 0, g.dst, by_depth, kp);
+  flat_.clear();
+  level_off_.assign(1, 0);
+  for (int d = (int)by_depth.size() - 1; d >= 0; --d) {  // deepest level first
+    if (by_depth[d].empty()) continue;
+    flat_.insert(flat_.end(), by_depth[d].begin(), by_depth[d].end());
+    level_off_.push_back((int)flat_.size());
+  }
+  CVG_TRY(ops_d_.ensure(sizeof(PairOp) * std::max<size_t>(flat_.size(), 1)));
+  if (!flat_.empty())
+    CVG_CK(cudaMemcpyAsync(ops_d_.as<PairOp>(), flat_.data(), sizeof(PairOp) * flat_.size(), cudaMemcpyHostToDevice,
+                           s));
+  return Status::Ok();
+}
+
+Status TreeProgram::run(cvg_context* ctx, const int2* tiles, int ntiles, int64_t kp) const {
+  for (int l = 0; l + 1 < (int)level_off_.size(); ++l) {
+    {
+      Timed t(ctx, kTree);
+      launch_pair_sums(ops_d_.as<PairOp>() + level_off_[l], level_off_[l + 1] - level_off_[l], kp, tiles, ntiles,
+                       ctx->stream);
+    }
+    ctx->launches += 1;
+    CVG_CK(cudaGetLastError());
+  }
+  return Status::Ok();
+}
+
 Status Plan::count_launch(int n) {
   ctx_->launches += n;
   return cuda_status(cudaGetLastError(), "kernel launch");
@@ -131,6 +183,7 @@ Status Plan::create(cvg_context* ctx, int dtype, int64_t n, int64_t k, int64_t m
                          cudaMemcpyHostToDevice, ctx->stream));
   CVG_TRY(local_.ensure(sizeof(double) * kp_ * kp_));
   CVG_TRY(shift_.ensure(sizeof(double) * kp_));
+  CVG_CK(cudaMemsetAsync(shift_.as<void>(), 0, sizeof(double) * kp_, ctx->stream));  // ones/padding columns
   CVG_TRY(flag_.ensure(sizeof(int)));
   return Status::Ok();
 }
@@ -230,15 +283,13 @@ Status Plan::plan_segments() {
     CVG_CK(cudaMemcpyAsync(segs_d_.as<GramTask>(), segs_.data(), sizeof(GramTask) * segs_.size(),
                            cudaMemcpyHostToDevice, s));
   // Fold Gram pointers: the segment partial itself for single-segment folds,
-  // otherwise a fixed-order sum into foldbuf (K4).
+  // otherwise a fixed-order sum of its segments into foldbuf (K4, phase 1).
   int nmulti = 0;
   for (int f = 0; f < nown; ++f)
     if (fold_seg_begin_[f + 1] - fold_seg_begin_[f] != 1) ++nmulti;
   CVG_TRY(foldbuf_.ensure(sizeof(double) * std::max(nmulti, 1) * kp_ * kp_));
   fold_ptrs_.assign(nown, nullptr);
-  std::vector<const double*> gsrc;
-  std::vector<int32_t> gbeg{0};
-  std::vector<double*> gdst;
+  std::vector<TreeGroup> phase1;
   int slot = 0;
   for (int f = 0; f < nown; ++f) {
     const int a = fold_seg_begin_[f], b = fold_seg_begin_[f + 1];
@@ -247,30 +298,17 @@ Status Plan::plan_segments() {
     } else {
       double* dst = foldbuf_.as<double>() + (int64_t)slot++ * kp_ * kp_;
       fold_ptrs_[f] = dst;
-      for (int sgi = a; sgi < b; ++sgi) gsrc.push_back(part_.as<double>() + (int64_t)sgi * kp_ * kp_);
-      gbeg.push_back((int32_t)gsrc.size());
-      gdst.push_back(dst);
+      TreeGroup g{{}, dst};
+      for (int sgi = a; sgi < b; ++sgi) g.leaves.push_back(part_.as<double>() + (int64_t)sgi * kp_ * kp_);
+      phase1.push_back(std::move(g));
     }
   }
-  // group list: [multi-segment folds...] then the local fold-tree node in a
-  // second launch (it depends on the first).
-  std::vector<const double*> all_src = gsrc;
-  all_src.insert(all_src.end(), fold_ptrs_.begin(), fold_ptrs_.end());
-  std::vector<int32_t> all_beg = gbeg;
-  all_beg.push_back((int32_t)all_src.size());
-  std::vector<double*> all_dst = gdst;
-  all_dst.push_back(local_.as<double>());
-  CVG_TRY(grp_src_.ensure(sizeof(void*) * std::max<size_t>(all_src.size(), 1)));
-  CVG_TRY(grp_begin_.ensure(sizeof(int32_t) * all_beg.size()));
-  CVG_TRY(grp_dst_.ensure(sizeof(void*) * all_dst.size()));
+  CVG_TRY(fold_tree_.build(phase1, kp_, s));
+  // Phase 2: this plan's node of the fold tree, over the owned folds in order.
+  std::vector<TreeGroup> phase2{TreeGroup{std::vector<const double*>(fold_ptrs_.begin(), fold_ptrs_.end()),
+                                          local_.as<double>()}};
+  CVG_TRY(local_tree_.build(phase2, kp_, s));
   CVG_TRY(foldptr_d_.ensure(sizeof(void*) * std::max(nown, 1)));
-  if (!all_src.empty())
-    CVG_CK(cudaMemcpyAsync(grp_src_.as<void>(), all_src.data(), sizeof(void*) * all_src.size(),
-                           cudaMemcpyHostToDevice, s));
-  CVG_CK(cudaMemcpyAsync(grp_begin_.as<void>(), all_beg.data(), sizeof(int32_t) * all_beg.size(),
-                         cudaMemcpyHostToDevice, s));
-  CVG_CK(cudaMemcpyAsync(grp_dst_.as<void>(), all_dst.data(), sizeof(void*) * all_dst.size(), cudaMemcpyHostToDevice,
-                         s));
   if (nown > 0)
     CVG_CK(cudaMemcpyAsync(foldptr_d_.as<void>(), fold_ptrs_.data(), sizeof(void*) * nown, cudaMemcpyHostToDevice,
                            s));
@@ -295,6 +333,9 @@ Status Plan::gram(const void* d_x, int64_t ldx, const void* d_y, int64_t ldy, co
     CVG_TRY(count_launch());
   }
   CVG_CK(cudaMemsetAsync(flag_.as<void>(), 0, sizeof(int), s));
+  // K1 builds the fold-bucketed, shifted copy Z.  (Gathering X rows straight
+  // into the Gram's shared-memory stages was measured slower: random 512-byte
+  // row chunks over the whole matrix are latency-bound — DESIGN.md §4.)
   if (zrows_ > 0) {
     {
       Timed t(ctx_, kReorder);
@@ -311,23 +352,8 @@ Status Plan::gram(const void* d_x, int64_t ldx, const void* d_y, int64_t ldy, co
     }
     CVG_TRY(count_launch());
   }
-  const int nown = fe_ - fb_;
-  int nmulti = 0;
-  for (int f = 0; f < nown; ++f)
-    if (fold_seg_begin_[f + 1] - fold_seg_begin_[f] != 1) ++nmulti;
-  const double* const* srcs = grp_src_.as<const double*>();
-  double* const* dsts = grp_dst_.as<double*>();
-  const int32_t* beg = grp_begin_.as<int32_t>();
-  if (nmulti > 0) {
-    Timed t(ctx_, kTree);
-    launch_tree_sum(srcs, beg, nmulti, dsts, kp_, tiles_d_.as<int2>(), (int)tiles_.size(), s);
-    CVG_TRY(count_launch());
-  }
-  {
-    Timed t(ctx_, kTree);
-    launch_tree_sum(srcs, beg + nmulti, 1, dsts + nmulti, kp_, tiles_d_.as<int2>(), (int)tiles_.size(), s);
-  }
-  CVG_TRY(count_launch());
+  CVG_TRY(fold_tree_.run(ctx_, tiles_d_.as<int2>(), (int)tiles_.size(), kp_));
+  CVG_TRY(local_tree_.run(ctx_, tiles_d_.as<int2>(), (int)tiles_.size(), kp_));
   grammed_ = true;
   return Status::Ok();
 }
@@ -342,24 +368,11 @@ Status Plan::finish(const double* d_rank_partials, int32_t n_ranks, const double
     total = total_override;
   } else if (d_rank_partials && n_ranks > 1) {
     CVG_TRY(total_.ensure(sizeof(double) * kp_ * kp_));
-    std::vector<const double*> src(n_ranks);
-    for (int r = 0; r < n_ranks; ++r) src[r] = d_rank_partials + (int64_t)r * kp_ * kp_;
-    std::vector<int32_t> beg{0, n_ranks};
-    double* dst = total_.as<double>();
-    CVG_TRY(rankptr_d_.ensure(sizeof(void*) * n_ranks));
-    CVG_TRY(rankbeg_d_.ensure(sizeof(int32_t) * 2));
-    CVG_TRY(rankdst_d_.ensure(sizeof(void*)));
-    CVG_CK(cudaMemcpyAsync(rankptr_d_.as<void>(), src.data(), sizeof(void*) * n_ranks, cudaMemcpyHostToDevice, s));
-    CVG_CK(cudaMemcpyAsync(rankbeg_d_.as<void>(), beg.data(), sizeof(int32_t) * 2, cudaMemcpyHostToDevice, s));
-    CVG_CK(cudaMemcpyAsync(rankdst_d_.as<void>(), &dst, sizeof(void*), cudaMemcpyHostToDevice, s));
-    {
-      Timed t(ctx_, kTree);
-      launch_tree_sum(rankptr_d_.as<const double*>(), rankbeg_d_.as<int32_t>(), 1, rankdst_d_.as<double*>(), kp_,
-                      tiles_d_.as<int2>(), (int)tiles_.size(), s);
-    }
-    CVG_TRY(count_launch());
-    CVG_CK(cudaStreamSynchronize(s));  // host pointer vectors above are temporaries
-    total = dst;
+    TreeGroup g{{}, total_.as<double>()};
+    for (int r = 0; r < n_ranks; ++r) g.leaves.push_back(d_rank_partials + (int64_t)r * kp_ * kp_);
+    CVG_TRY(rank_tree_.build({g}, kp_, s));
+    CVG_TRY(rank_tree_.run(ctx_, tiles_d_.as<int2>(), (int)tiles_.size(), kp_));
+    total = total_.as<double>();
   } else if (d_rank_partials && n_ranks == 1) {
     total = d_rank_partials;
   } else {
@@ -375,7 +388,7 @@ Status Plan::finish(const double* d_rank_partials, int32_t n_ranks, const double
   {
     Timed t(ctx_, kStats);
     launch_fold_stats(total, foldptr_d_.as<const double*>(), nval_d_.as<int64_t>(), nown, n_, k_, m_, kp_,
-                      shift_.as<double>(), st, d_mean_x, d_mean_y, d_std_x, d_std_y, s);
+                      shift_.as<double>(), st, d_mean_x, d_mean_y, d_std_x, d_std_y, flag_.as<int>(), s);
   }
   CVG_TRY(count_launch());
   if (ncfg > 0) {

@@ -31,6 +31,27 @@ class DevBuf {
 
 Status cuda_status(cudaError_t e, const char* what);
 
+// A set of midpoint-tree sums flattened into levels of independent pairwise
+// adds (K4).  Group g: dst = S(leaves[0..n)); n == 1 copies, n == 0 zeroes.
+struct TreeGroup {
+  std::vector<const double*> leaves;
+  double* dst;
+};
+class TreeProgram {
+ public:
+  Status build(const std::vector<TreeGroup>& groups, int64_t kp, cudaStream_t s);
+  Status run(cvg_context* ctx, const int2* tiles, int ntiles, int64_t kp) const;
+  int levels() const { return (int)level_off_.size() - 1; }
+
+ private:
+  const double* emit(const std::vector<const double*>& leaves, int a, int b, int depth, double* root_dst,
+                     std::vector<std::vector<PairOp>>& by_depth, int64_t kp);
+  std::vector<int> level_off_;
+  std::vector<PairOp> flat_;
+  DevBuf scratch_, ops_d_;
+  int64_t next_slot_ = 0;
+};
+
 // One partitioning of n rows into p folds, of which folds [fb, fe) are owned.
 class Plan {
  public:
@@ -82,8 +103,8 @@ class Plan {
   bool bound_ = false, grammed_ = false;
 
   DevBuf tiles_d_, out_tiles_d_, tile_counts_, fold_counts_, bad_, zbase_d_, src_row_, z_, part_, foldbuf_, local_,
-      total_, shift_, flag_, segs_d_, grp_src_, grp_begin_, grp_dst_, foldptr_d_, nval_d_, rankptr_d_, rankbeg_d_,
-      rankdst_d_, st_mz_, st_sT_, st_sd_, cfg_d_;
+      total_, shift_, flag_, segs_d_, foldptr_d_, nval_d_, st_mz_, st_sT_, st_sd_, cfg_d_;
+  TreeProgram fold_tree_, local_tree_, rank_tree_;
   std::vector<const double*> fold_ptrs_;
 };
 

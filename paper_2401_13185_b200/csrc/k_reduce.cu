@@ -10,41 +10,42 @@
 // tree's top levels.  This keeps the reference's bitwise thread-count
 // invariance (threading.hpp:8-10, test_fast.cpp:217-229).  No float atomics.
 //
-// Only the tiles the Gram wrote are touched.  One CTA per (tile, group).
+// The host flattens the trees into levels of independent pairwise adds
+// (TreeProgram, engine.cu); each level is one launch over (tile, op) with
+// 16-byte loads, so a level streams at HBM speed instead of walking the tree
+// per element.  Only the tiles the Gram wrote are touched.
 #include "cvg_internal.cuh"
 
 namespace cvg {
 namespace {
 
-__device__ double tree_sum(const double* const* __restrict__ src, int a, int b, int64_t off) {
-  if (b <= a) return 0.0;
-  if (b - a == 1) return src[a][off];
-  const int mid = a + (b - a) / 2;
-  return __dadd_rn(tree_sum(src, a, mid, off), tree_sum(src, mid, b, off));
-}
-
-__global__ void __launch_bounds__(256) tree_sum_kernel(const double* const* __restrict__ srcs,
-                                                       const int32_t* __restrict__ src_begin,
-                                                       double* const* __restrict__ dsts, int64_t kp,
+__global__ void __launch_bounds__(256) pair_sum_kernel(const PairOp* __restrict__ ops, int64_t kp,
                                                        const int2* __restrict__ tiles) {
   const int2 tile = tiles[blockIdx.x];
-  const int grp = blockIdx.y;
-  const int a = src_begin[grp], b = src_begin[grp + 1];
-  double* dst = dsts[grp];
-  const int c = threadIdx.x & 63;
-  for (int r = threadIdx.x >> 6; r < kTile; r += 4) {
-    const int64_t off = ((int64_t)tile.x * kTile + r) * kp + (int64_t)tile.y * kTile + c;
-    dst[off] = tree_sum(srcs, a, b, off);
+  const PairOp op = ops[blockIdx.y];
+  const int c2 = (threadIdx.x & 31) * 2;  // column pair within the tile
+#pragma unroll 4
+  for (int r = threadIdx.x >> 5; r < kTile; r += 8) {
+    const int64_t off = ((int64_t)tile.x * kTile + r) * kp + (int64_t)tile.y * kTile + c2;
+    double2 v = make_double2(0.0, 0.0);
+    if (op.a) {
+      v = *reinterpret_cast<const double2*>(op.a + off);
+      if (op.b) {
+        const double2 w = *reinterpret_cast<const double2*>(op.b + off);
+        v.x = __dadd_rn(v.x, w.x);
+        v.y = __dadd_rn(v.y, w.y);
+      }
+    }
+    *reinterpret_cast<double2*>(op.d + off) = v;
   }
 }
 
 }  // namespace
 
-void launch_tree_sum(const double* const* srcs, const int32_t* src_begin, int ngroups, double* const* dsts,
-                     int64_t kp, const int2* tiles, int ntiles, cudaStream_t s) {
-  if (ngroups <= 0 || ntiles <= 0) return;
-  dim3 grid((unsigned)ntiles, (unsigned)ngroups);
-  tree_sum_kernel<<<grid, 256, 0, s>>>(srcs, src_begin, dsts, kp, tiles);
+void launch_pair_sums(const PairOp* ops, int nops, int64_t kp, const int2* tiles, int ntiles, cudaStream_t s) {
+  if (nops <= 0 || ntiles <= 0) return;
+  dim3 grid((unsigned)ntiles, (unsigned)nops);
+  pair_sum_kernel<<<grid, 256, 0, s>>>(ops, kp, tiles);
 }
 
 }  // namespace cvg
