@@ -38,6 +38,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 FP64_DMMA_PEAK_TFLOPS = 37.1  # profiles/r01_fp64_peaks.txt (DMMA.8x8x4 issue loop; cuBLAS DGEMM 35.4)
+TF32_PEAK_TFLOPS = 623.3      # profiles/r01_fp64_peaks.txt (cuBLAS TF32 8192^3 sustained; burst 744.6)
 CPU_SAMPLE_ROWS = 1_000_000
 
 
@@ -187,7 +188,7 @@ def run_ours(args):
     cid = args.config
     n, k, m, p = workloads.SHAPES[cid]
     x, y, labels, p, cfgs = workloads.make_device(cid, dev)
-    masks = [cfgs[0]]
+    masks = list(cfgs)  # every configuration the BASELINE config names, from one Gram pass
     flops = 2.0 * n * k * (k + m)
     fb, fe = P.fold_range(p, rank, world)
     plan = P.DevicePlan(n, k, m, p, fb, fe, dtype="f32" if x.dtype == torch.float32 else "f64", ctx=ctx)
@@ -258,9 +259,10 @@ def run_ours(args):
         plan = None
         out = None
         torch.cuda.empty_cache()
-        hxtx = torch.empty((1, p, k, k), dtype=torch.float64, pin_memory=True)
-        hxty = torch.empty((1, p, k, m), dtype=torch.float64, pin_memory=True)
-        hv = {nm: torch.empty((1, p, d), dtype=torch.float64, pin_memory=True)
+        nc = len(masks)
+        hxtx = torch.empty((nc, p, k, k), dtype=torch.float64, pin_memory=True)
+        hxty = torch.empty((nc, p, k, m), dtype=torch.float64, pin_memory=True)
+        hv = {nm: torch.empty((nc, p, d), dtype=torch.float64, pin_memory=True)
               for nm, d in (("mx", k), ("my", m), ("sx", k), ("sy", m))}
         hnt = np.empty(p, np.int64)
         hnv = np.empty(p, np.int64)
@@ -271,7 +273,7 @@ def run_ours(args):
         def e2e_step():
             buf = L.err_buf()
             rc = L.lib().cvg_run_all_folds(ctx.handle, dtype_code, hx.data_ptr(), hy.data_ptr(), n, k, m,
-                                           hl.data_ptr(), n, p, cm.ctypes.data, 1, hxtx.data_ptr(), hxty.data_ptr(),
+                                           hl.data_ptr(), n, p, cm.ctypes.data, nc, hxtx.data_ptr(), hxty.data_ptr(),
                                            hv["mx"].data_ptr(), hv["my"].data_ptr(), hv["sx"].data_ptr(),
                                            hv["sy"].data_ptr(), hnt.ctypes.data, hnv.ctypes.data, buf, len(buf))
             if rc:
@@ -285,7 +287,7 @@ def run_ours(args):
         e2e_ms = (time.perf_counter() - t0) * 1e3 / e_steps
         elt = hx.element_size()
         h2d = n * k * elt + n * m * elt + n * 4
-        d2h = p * k * k * 8 + p * k * m * 8 + p * (2 * k + 2 * m) * 8
+        d2h = nc * (p * k * k * 8 + p * k * m * 8 + p * (2 * k + 2 * m) * 8)
         e2e = {"value": round(flops / (e2e_ms * 1e-3) / 1e9, 3), "unit": "GFLOP/s", "ms_per_step": round(e2e_ms, 3),
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                "path": "cvg_run_all_folds (C ABI) from pinned host buffers, wall clock around the synchronous call"}
@@ -301,10 +303,21 @@ def run_ours(args):
     # executed DMMA flops: 64x64 tiles actually issued (symmetry + padding)
     from paper_2401_13185_b200.plan import executed_gram_flops
 
-    executed = executed_gram_flops(n, k, m, p) / max(world, 1) / (gram_ms * 1e-3) / 1e12
+    f32 = not x_dtype_is_f64(cid)
+    executed = executed_gram_flops(n, k, m, p, f32) / max(world, 1) / (gram_ms * 1e-3) / 1e12
+    if f32:
+        gram_kernel = "gram_tf32_kernel (tcgen05.mma kind::tf32, 3xTF32, TMEM accumulators)"
+        peak = TF32_PEAK_TFLOPS
+        peak_source = ("measured cuBLAS TF32 GEMM (8192^3, sustained) on this pool's B200 "
+                       "(profiles/r01_fp64_peaks.txt); executed counts the 3 TF32 products")
+    else:
+        gram_kernel = "gram_f64_kernel (DMMA.8x8x4)"
+        peak = FP64_DMMA_PEAK_TFLOPS
+        peak_source = ("measured DMMA issue-loop peak on this pool's B200 (profiles/r01_fp64_peaks.txt); "
+                       "MEASURED_PEAKS.json has no fp64 figure")
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "r01_gram_ncu.json")
-    if os.path.exists(tpath):
+    if os.path.exists(tpath) and cid == 1:
         try:
             traffic = json.load(open(tpath)).get("dram_bytes_per_launch")
         except Exception:
@@ -313,25 +326,26 @@ def run_ours(args):
     per_kernel = {nm: round(float(kms[i]) / args.steps, 4) for i, nm in enumerate(kernel_names)}
     pk = peaks()
     hbm = pk.get("hbm_gbs", 6554.2)
-    reorder_bytes = n * (k + m) * 8 + (n + 32 * p) * (-(-(k + m + 1) // 64) * 64) * 8
-    epi_bytes = 2 * p * k * (k + m) * 8 + k * (k + m) * 8
+    tile = 128 if f32 else 64
+    reorder_bytes = n * (k + m) * x.element_size() + (n + 32 * p) * (-(-(k + m + 1) // tile) * tile) * (8 if f32 else 8)
+    epi_bytes = len(masks) * (2 * p * k * (k + m) * 8) + k * (k + m) * 8
     line = {
         "metric": "all_fold_cv_gram_gflops", "value": round(value, 3), "unit": "GFLOP/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64" if x_dtype_is_f64(cid) else "f32",
         "data": "synthetic",
-        "config": {"workload": f"configs[{cid}] N={n} K={k} M={m} P={p} cfg mask {masks[0]} "
-                               f"(center+scale X and Y), near-equal folds via random_partitioning(seed "
-                               f"{workloads.SEEDS[cid]})", "global_batch": n, "parallelism": f"folds/{world} ranks",
-                   "l2": "inputs 4.1 GB > 126 MB L2: no flush needed", "seed": workloads.SEEDS[cid]},
-        "roofline": {"bound": "tensor", "kernel": "gram_f64_kernel (DMMA.8x8x4)", "achieved": round(achieved, 3),
-                     "peak": FP64_DMMA_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": round(achieved / FP64_DMMA_PEAK_TFLOPS, 4),
+        "config": {"workload": f"configs[{cid}] N={n} K={k} M={m} P={p} cfg masks {masks} "
+                               f"({workloads.DESCRIPTIONS[cid]})", "global_batch": n,
+                   "parallelism": f"folds/{world} ranks",
+                   "l2": f"inputs {x.numel() * x.element_size() / 1e9:.1f} GB > 126 MB L2: no flush needed",
+                   "seed": workloads.SEEDS[cid]},
+        "roofline": {"bound": "tensor", "kernel": gram_kernel, "achieved": round(achieved, 3),
+                     "peak": peak, "unit": "TFLOP/s", "frac": round(achieved / peak, 4),
                      "traffic": traffic,
-                     "peak_source": "measured DMMA issue-loop peak on this pool's B200 (profiles/r01_fp64_peaks.txt); "
-                                    "MEASURED_PEAKS.json has no fp64 figure",
+                     "peak_source": peak_source,
                      "algorithmic_flops_per_launch": gram_flops_per_launch,
                      "executed_tflops": round(executed, 3),
-                     "executed_frac": round(executed / FP64_DMMA_PEAK_TFLOPS, 4),
+                     "executed_frac": round(executed / peak, 4),
                      "note": "algorithmic flops = 2NK(K+M) (BASELINE metric); the kernel computes only the "
                              "upper 64x64 tiles, so executed < algorithmic"},
         "kernels_ms_per_step": per_kernel,

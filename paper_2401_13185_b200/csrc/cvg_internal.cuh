@@ -23,7 +23,9 @@ namespace cvg {
 
 constexpr int kTile = 64;          // Gram / epilogue tile edge (columns)
 constexpr int kRowStep = 32;       // rows per pipeline stage; fold blocks pad to this
-constexpr int64_t kChunkRows = 32768;  // max rows per segment (fixed => deterministic split)
+constexpr int64_t kChunkRows = 32768;     // max rows per fp64 segment (fixed => deterministic split)
+constexpr int64_t kChunkRowsF32 = 32768;  // fp32 segments (the tcgen05 Gram drains fp32 to fp64 every 512 rows)
+constexpr int kTileF32 = 128;             // tcgen05 tile edge (M = N = 128)
 constexpr int kTileRowsPerWarp = 1024; // rows per warp in the bucketing passes
 
 struct Status {
@@ -88,10 +90,21 @@ void launch_hadamard(const double* mat, int64_t rows, int64_t cols, const double
                      cudaStream_t s);
 
 // Tile list of the symmetric Gram (ti <= tj), plus the diagonal/ones tiles of
-// Y-only column blocks.  Shared by the Gram, the reductions and the epilogue.
-std::vector<int2> gram_tiles(int64_t k, int64_t m, int64_t kp);
+// Y-only column blocks, for tile edge `edge`.  The 64-tile list drives the
+// reductions and the epilogue; the fp32 Gram uses the 128-tile list.
+std::vector<int2> gram_tiles(int64_t k, int64_t m, int64_t kp, int edge = kTile);
+
+// K1T + K2' (fp32 inputs): bucket/shift/split into TF32 hi + lo, transposed;
+// then the tcgen05 kind::tf32 Gram (3 products: hi·hi + hi·lo + lo·hi).
+void launch_reorder_split_t(int dtype, const void* x, int64_t ldx, const void* y, int64_t ldy, int64_t k, int64_t m,
+                            const int64_t* src_row, int64_t zrows, int64_t kp, const double* shift, float* zt_hi,
+                            float* zt_lo, int* nonfinite, cudaStream_t s);
+bool launch_gram_tf32(const float* zt_hi, const float* zt_lo, int64_t zrows, int64_t kp, const GramTask* segs,
+                      int64_t nseg, const int2* tiles128, int ntiles, double* part, int nterms, cudaStream_t s);
 
 inline int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
-inline int64_t padded_cols(int64_t k, int64_t m) { return round_up(k + m + 1, kTile); }
+inline int64_t padded_cols(int64_t k, int64_t m, int dtype = 0) {
+  return round_up(k + m + 1, dtype == 1 ? kTileF32 : kTile);
+}
 
 }  // namespace cvg

@@ -80,10 +80,10 @@ void DevBuf::release() {
   bytes_ = 0;
 }
 
-std::vector<int2> gram_tiles(int64_t k, int64_t m, int64_t kp) {
-  const int nt = (int)(kp / kTile);
-  const int tx = (int)((k - 1) / kTile);  // last tile holding X columns
-  const int to = (int)((k + m) / kTile);  // tile holding the ones column
+std::vector<int2> gram_tiles(int64_t k, int64_t m, int64_t kp, int edge) {
+  const int nt = (int)(kp / edge);
+  const int tx = (int)((k - 1) / edge);  // last tile holding X columns
+  const int to = (int)((k + m) / edge);  // tile holding the ones column
   std::vector<int2> t;
   for (int i = 0; i < nt; ++i)
     for (int j = i; j < nt; ++j)
@@ -169,8 +169,9 @@ Status Plan::create(cvg_context* ctx, int dtype, int64_t n, int64_t k, int64_t m
       return Status::Err(2, "fold count " + std::to_string(p) + " exceeds sample count " + std::to_string(n));
   }
   if (fb < 0 || fe > p || fb > fe) return Status::Err(4, "owned fold range is outside [0, p]");
-  kp_ = padded_cols(k, m);
+  kp_ = padded_cols(k, m, dtype);
   tiles_ = gram_tiles(k, m, kp_);
+  tiles128_ = dtype == 1 ? gram_tiles(k, m, kp_, kTileF32) : std::vector<int2>{};
   out_tiles_.clear();
   for (const int2& t : tiles_)
     if ((int64_t)t.x * kTile < k) out_tiles_.push_back(t);
@@ -181,6 +182,11 @@ Status Plan::create(cvg_context* ctx, int dtype, int64_t n, int64_t k, int64_t m
                          ctx->stream));
   CVG_CK(cudaMemcpyAsync(out_tiles_d_.as<int2>(), out_tiles_.data(), out_tiles_.size() * sizeof(int2),
                          cudaMemcpyHostToDevice, ctx->stream));
+  if (!tiles128_.empty()) {
+    CVG_TRY(tiles128_d_.ensure(tiles128_.size() * sizeof(int2)));
+    CVG_CK(cudaMemcpyAsync(tiles128_d_.as<int2>(), tiles128_.data(), tiles128_.size() * sizeof(int2),
+                           cudaMemcpyHostToDevice, ctx->stream));
+  }
   CVG_TRY(local_.ensure(sizeof(double) * kp_ * kp_));
   CVG_TRY(shift_.ensure(sizeof(double) * kp_));
   CVG_CK(cudaMemsetAsync(shift_.as<void>(), 0, sizeof(double) * kp_, ctx->stream));  // ones/padding columns
@@ -260,8 +266,9 @@ Status Plan::plan_segments() {
   for (int32_t f = fb_; f < fe_; ++f) {
     const int64_t padded = round_up(counts_[f], kRowStep);
     fold_zbase_.push_back(zrows_);
-    for (int64_t off = 0; off < padded; off += kChunkRows)
-      segs_.push_back(GramTask{zrows_ + off, std::min<int64_t>(kChunkRows, padded - off)});
+    const int64_t chunk = dtype_ == 1 ? kChunkRowsF32 : kChunkRows;
+    for (int64_t off = 0; off < padded; off += chunk)
+      segs_.push_back(GramTask{zrows_ + off, std::min<int64_t>(chunk, padded - off)});
     zrows_ += padded;
     fold_seg_begin_.push_back((int32_t)segs_.size());
   }
@@ -269,7 +276,12 @@ Status Plan::plan_segments() {
   cudaStream_t s = ctx_->stream;
   CVG_TRY(zbase_d_.ensure(sizeof(int64_t) * std::max(nown, 1)));
   CVG_TRY(src_row_.ensure(sizeof(int64_t) * std::max<int64_t>(zrows_, 1)));
-  CVG_TRY(z_.ensure(sizeof(double) * std::max<int64_t>(zrows_, 1) * kp_));
+  if (dtype_ == 1) {  // transposed TF32 hi / lo operands for the tcgen05 Gram
+    CVG_TRY(zt_hi_.ensure(sizeof(float) * std::max<int64_t>(zrows_, 32) * kp_));
+    CVG_TRY(zt_lo_.ensure(sizeof(float) * std::max<int64_t>(zrows_, 32) * kp_));
+  } else {
+    CVG_TRY(z_.ensure(sizeof(double) * std::max<int64_t>(zrows_, 1) * kp_));
+  }
   CVG_TRY(part_.ensure(sizeof(double) * std::max<size_t>(segs_.size(), 1) * kp_ * kp_));
   CVG_TRY(segs_d_.ensure(sizeof(GramTask) * std::max<size_t>(segs_.size(), 1)));
   CVG_TRY(nval_d_.ensure(sizeof(int64_t) * std::max(nown, 1)));
@@ -333,24 +345,47 @@ Status Plan::gram(const void* d_x, int64_t ldx, const void* d_y, int64_t ldy, co
     CVG_TRY(count_launch());
   }
   CVG_CK(cudaMemsetAsync(flag_.as<void>(), 0, sizeof(int), s));
-  // K1 builds the fold-bucketed, shifted copy Z.  (Gathering X rows straight
-  // into the Gram's shared-memory stages was measured slower: random 512-byte
-  // row chunks over the whole matrix are latency-bound — DESIGN.md §4.)
-  if (zrows_ > 0) {
-    {
-      Timed t(ctx_, kReorder);
-      launch_reorder(dtype_, d_x, ldx, d_y, ldy, k_, m_, src_row_.as<int64_t>(), zrows_, kp_, shift,
-                     z_.as<double>(), flag_.as<int>(), s);
+  if (dtype_ == 1) {
+    // fp32: K1T (bucket, shift, TF32 split, transpose) then the tcgen05 Gram.
+    if (zrows_ > 0) {
+      {
+        Timed t(ctx_, kReorder);
+        launch_reorder_split_t(dtype_, d_x, ldx, d_y, ldy, k_, m_, src_row_.as<int64_t>(), zrows_, kp_, shift,
+                               zt_hi_.as<float>(), zt_lo_.as<float>(), flag_.as<int>(), s);
+      }
+      CVG_TRY(count_launch());
     }
-    CVG_TRY(count_launch());
-  }
-  if (!segs_.empty()) {
-    {
-      Timed t(ctx_, kGram);
-      launch_gram_f64(z_.as<double>(), kp_, segs_d_.as<GramTask>(), (int64_t)segs_.size(), tiles_d_.as<int2>(),
-                      (int)tiles_.size(), part_.as<double>(), s);
+    if (!segs_.empty()) {
+      bool ok;
+      {
+        Timed t(ctx_, kGram);
+        ok = launch_gram_tf32(zt_hi_.as<float>(), zt_lo_.as<float>(), zrows_, kp_, segs_d_.as<GramTask>(),
+                              (int64_t)segs_.size(), tiles128_d_.as<int2>(), (int)tiles128_.size(), part_.as<double>(),
+                              3, s);
+      }
+      if (!ok) return Status::Err(5, "cuTensorMapEncodeTiled unavailable or rejected the operand layout");
+      CVG_TRY(count_launch());
     }
-    CVG_TRY(count_launch());
+  } else {
+    // fp64: K1 builds the fold-bucketed, shifted copy Z.  (Gathering X rows
+    // straight into the Gram's shared-memory stages was measured slower: random
+    // 512-byte row chunks over the whole matrix are latency-bound — DESIGN.md §4.)
+    if (zrows_ > 0) {
+      {
+        Timed t(ctx_, kReorder);
+        launch_reorder(dtype_, d_x, ldx, d_y, ldy, k_, m_, src_row_.as<int64_t>(), zrows_, kp_, shift,
+                       z_.as<double>(), flag_.as<int>(), s);
+      }
+      CVG_TRY(count_launch());
+    }
+    if (!segs_.empty()) {
+      {
+        Timed t(ctx_, kGram);
+        launch_gram_f64(z_.as<double>(), kp_, segs_d_.as<GramTask>(), (int64_t)segs_.size(), tiles_d_.as<int2>(),
+                        (int)tiles_.size(), part_.as<double>(), s);
+      }
+      CVG_TRY(count_launch());
+    }
   }
   CVG_TRY(fold_tree_.run(ctx_, tiles_d_.as<int2>(), (int)tiles_.size(), kp_));
   CVG_TRY(local_tree_.run(ctx_, tiles_d_.as<int2>(), (int)tiles_.size(), kp_));

@@ -94,7 +94,7 @@ class Plan {
   int dtype_ = 0;
   int64_t n_ = 0, k_ = 0, m_ = 0, w_ = 0, kp_ = 0;
   int32_t p_ = 0, fb_ = 0, fe_ = 0;
-  std::vector<int2> tiles_, out_tiles_;
+  std::vector<int2> tiles_, out_tiles_, tiles128_;
   std::vector<int64_t> counts_;  // per fold (all p) validation sizes
   std::vector<GramTask> segs_;
   std::vector<int32_t> fold_seg_begin_;
@@ -102,7 +102,7 @@ class Plan {
   int64_t zrows_ = 0;
   bool bound_ = false, grammed_ = false;
 
-  DevBuf tiles_d_, out_tiles_d_, tile_counts_, fold_counts_, bad_, zbase_d_, src_row_, z_, part_, foldbuf_, local_,
+  DevBuf tiles_d_, out_tiles_d_, tiles128_d_, zt_hi_, zt_lo_, tile_counts_, fold_counts_, bad_, zbase_d_, src_row_, z_, part_, foldbuf_, local_,
       total_, shift_, flag_, segs_d_, foldptr_d_, nval_d_, st_mz_, st_sT_, st_sd_, cfg_d_;
   TreeProgram fold_tree_, local_tree_, rank_tree_;
   std::vector<const double*> fold_ptrs_;

@@ -1,0 +1,337 @@
+// K1T + K2': the fp32-input fold Gram on the 5th-generation tensor cores
+// (tcgen05.mma kind::tf32, TMEM accumulators, TMA-fed shared-memory ring).
+//
+// BASELINE.json configs[3] (fp32 inputs, fp32 accumulation on tensor cores,
+// 1e-4 against the fp64 oracle).  TF32 keeps 11 significant bits, so each
+// shifted value is split z = hi + lo with hi, lo TF32-exact (round to
+// nearest) and every product is formed as hi·hi + hi·lo + lo·hi ("3xTF32",
+// ~2^-22 relative per term) into an fp32 TMEM accumulator.  The tensor core's
+// fp32 accumulation drifts linearly with chain length (measured: 3e-5 relative
+// after 16384 rows, 5e-6 after 512), so the accumulator is double-buffered in
+// TMEM and drained into fp64 registers every 128 rows while the MMAs continue
+// in the other buffer; partials leave as fp64 and all later sums (K4) and the
+// epilogue (K5) are fp64.
+//
+// K1T writes the bucketed, shifted, split operand TRANSPOSED (Zt[col][row]) so
+// both MMA operands are K-major (contraction over rows is the contiguous axis):
+// one TMA box = 128 columns x 32 rows = 128 rows of 128 B, 128B-swizzled, the
+// canonical K-major SWIZZLE_128B UMMA layout (SBO = 1024 B).
+//
+// K2' roles (10 warps, 1 CTA per SM, 192 KB of stages, 256 TMEM columns):
+//   warp 0      TMA producer: hi/lo slabs of both column tiles per 32-row stage
+//   warp 1      TMEM owner + MMA issuer (one elected thread), ping-pong accumulators
+//   warps 2..9  drain every 128 rows: tcgen05.ld 128 lanes x 64 columns each, fp64 sums,
+//               write the fp64 partial at the end
+#include <cuda.h>
+
+#include "cvg_internal.cuh"
+
+namespace cvg {
+namespace {
+
+constexpr int TT = 128;                       // tile edge (M = N = 128)
+constexpr int KS = 32;                        // rows per stage = 128 B of fp32
+constexpr int NST = 3;                        // pipeline stages
+constexpr int kOpBytes = TT * KS * 4;         // 16 KB per operand slab
+constexpr int kStageBytes = 4 * kOpBytes;     // A_hi, A_lo, B_hi, B_lo
+constexpr int kSmemTf32 = NST * kStageBytes + 1024;  // + alignment slack
+constexpr int kDrainSteps = 4;                // 128 rows per fp32 accumulation chunk
+constexpr int kEpiWarps = 8;                  // 4 TMEM lane quarters x 2 column halves
+constexpr int kThreads = 64 + 32 * kEpiWarps;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra DONE;\n"
+      "bra WAIT;\n"
+      "DONE:\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];\n" ::
+          "r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+// K-major, 128B-swizzled operand: 8-row atoms of 1024 B (SBO), version 1 (sm_100).
+__device__ __forceinline__ uint64_t kmajor_sw128_desc(const void* tile) {
+  const uint64_t addr = smem_u32(tile);
+  return ((addr >> 4) & 0x3FFFull) | (1ull << 16) | ((1024ull >> 4) << 32) | (1ull << 46) | (2ull << 61);
+}
+
+// kind::tf32, fp32 accumulate, both operands K-major, M = N = 128.
+constexpr uint32_t kIdescTf32 = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(TT >> 3) << 17) |
+                                ((uint32_t)(TT >> 4) << 24);
+
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(kIdescTf32), "r"(accumulate));
+}
+
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    gram_tf32_kernel(const __grid_constant__ CUtensorMap map_hi, const __grid_constant__ CUtensorMap map_lo,
+                     const GramTask* __restrict__ segs, const int2* __restrict__ tiles, int ntiles, int64_t kp,
+                     double* __restrict__ part, int nterms) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ __align__(8) uint64_t full_bar[NST], empty_bar[NST], acc_full[2], acc_empty[2];
+  __shared__ uint32_t tmem_base;
+
+  const int seg = blockIdx.x / ntiles;
+  const int2 tile = tiles[blockIdx.x - seg * ntiles];
+  const bool diag = tile.x == tile.y;
+  const GramTask task = segs[seg];
+  const int nsteps = (int)(task.rows / KS);
+  const int nchunks = (nsteps + kDrainSteps - 1) / kDrainSteps;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NST; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&acc_full[b], 1);
+      mbar_init(&acc_empty[b], kEpiWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(&tmem_base)),
+                 "r"(2 * TT));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  const uint32_t tmem_d = tmem_base;
+
+  auto op = [&](int s, int which) { return smem + s * kStageBytes + which * kOpBytes; };  // 0 Ahi 1 Alo 2 Bhi 3 Blo
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---- TMA producer
+      const uint32_t bytes = (uint32_t)kOpBytes * (nterms == 3 ? 2u : 1u) * (diag ? 1u : 2u);
+      for (int it = 0; it < nsteps; ++it) {
+        const int s = it % NST;
+        const uint32_t ph = (uint32_t)(it / NST) & 1u;
+        mbar_wait(&empty_bar[s], ph ^ 1u);
+        mbar_expect_tx(&full_bar[s], bytes);
+        const int r0 = (int)(task.zrow + (int64_t)it * KS);
+        tma_load_2d(op(s, 0), &map_hi, &full_bar[s], r0, tile.x * TT);
+        if (nterms == 3) tma_load_2d(op(s, 1), &map_lo, &full_bar[s], r0, tile.x * TT);
+        if (!diag) {
+          tma_load_2d(op(s, 2), &map_hi, &full_bar[s], r0, tile.y * TT);
+          if (nterms == 3) tma_load_2d(op(s, 3), &map_lo, &full_bar[s], r0, tile.y * TT);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---- MMA issuer, accumulator b = chunk & 1
+      for (int it = 0; it < nsteps; ++it) {
+        const int chunk = it / kDrainSteps, b = chunk & 1;
+        const bool first = it % kDrainSteps == 0;
+        if (first && chunk >= 2) mbar_wait(&acc_empty[b], (uint32_t)((chunk >> 1) - 1) & 1u);  // drained
+        const int s = it % NST;
+        const uint32_t ph = (uint32_t)(it / NST) & 1u;
+        mbar_wait(&full_bar[s], ph);
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+        const uint32_t acc = tmem_d + (uint32_t)(b * TT);
+        const uint64_t a_hi = kmajor_sw128_desc(op(s, 0)), a_lo = kmajor_sw128_desc(op(s, 1));
+        const uint64_t b_hi = diag ? a_hi : kmajor_sw128_desc(op(s, 2));
+        const uint64_t b_lo = diag ? a_lo : kmajor_sw128_desc(op(s, 3));
+#pragma unroll
+        for (int k = 0; k < KS / 8; ++k) {  // K = 8 tf32 = 32 B per MMA: +2 in 16-byte descriptor units
+          const uint64_t dk = 2ull * k;
+          mma_tf32(acc, a_hi + dk, b_hi + dk, (first && k == 0) ? 0u : 1u);
+          if (nterms == 3) {
+            mma_tf32(acc, a_hi + dk, b_lo + dk, 1u);
+            mma_tf32(acc, a_lo + dk, b_hi + dk, 1u);
+          }
+        }
+        mma_commit(&empty_bar[s]);  // frees the stage once these MMAs have read it
+        if (it % kDrainSteps == kDrainSteps - 1 || it == nsteps - 1) mma_commit(&acc_full[b]);
+      }
+    }
+  } else {  // ---- drain warps: fp32 TMEM chunks -> fp64 registers -> fp64 partial
+    const int q = warp & 3;            // TMEM lanes [32q, 32q + 32) (hardware: warp id mod 4)
+    const int h = (warp - 2) >> 2;     // columns [64h, 64h + 64)
+    double acc64[64];
+#pragma unroll
+    for (int j = 0; j < 64; ++j) acc64[j] = 0.0;
+    for (int chunk = 0; chunk < nchunks; ++chunk) {
+      const int b = chunk & 1;
+      mbar_wait(&acc_full[b], (uint32_t)(chunk >> 1) & 1u);
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+#pragma unroll
+      for (int c0 = 0; c0 < 64; c0 += 32) {
+        uint32_t r[32];
+        tmem_ld32(tmem_d + ((uint32_t)(32 * q) << 16) + (uint32_t)(b * TT + 64 * h + c0), r);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) acc64[c0 + j] += (double)__uint_as_float(r[j]);
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+      __syncwarp();
+      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(&acc_empty[b])) : "memory");
+    }
+    const int64_t row = (int64_t)tile.x * TT + 32 * q + lane;
+    double* out = part + (int64_t)seg * kp * kp + row * kp + (int64_t)tile.y * TT + 64 * h;
+#pragma unroll
+    for (int j = 0; j < 64; j += 2) *reinterpret_cast<double2*>(out + j) = make_double2(acc64[j], acc64[j + 1]);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem_d), "r"(2 * TT));
+  }
+}
+
+// TF32 round-to-nearest of an fp32 value (low 13 mantissa bits cleared).
+__device__ __forceinline__ float tf32_rn(float v) {
+  uint32_t u = __float_as_uint(v);
+  if ((u & 0x7f800000u) != 0x7f800000u) u = (u + 0x1000u) & 0xffffe000u;
+  return __uint_as_float(u);
+}
+
+// K1T: bucket, shift, split, transpose.  One CTA per (32 bucketed rows, 32 columns).
+template <typename T>
+__global__ void __launch_bounds__(256) reorder_split_t_kernel(const T* __restrict__ x, int64_t ldx,
+                                                              const T* __restrict__ y, int64_t ldy, int64_t k,
+                                                              int64_t m, const int64_t* __restrict__ src_row,
+                                                              int64_t zrows, int64_t kp,
+                                                              const double* __restrict__ shift,
+                                                              float* __restrict__ zt_hi, float* __restrict__ zt_lo,
+                                                              int* __restrict__ nonfinite) {
+  __shared__ float s_hi[32][33], s_lo[32][33];
+  const int64_t r0 = (int64_t)blockIdx.x * 32;
+  const int64_t c0 = (int64_t)blockIdx.y * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+  const int64_t w = k + m;
+  bool bad = false;
+  for (int rr = ty; rr < 32; rr += 8) {
+    const int64_t zr = r0 + rr;
+    const int64_t src = zr < zrows ? src_row[zr] : -1;
+    const int64_t c = c0 + tx;
+    float hi = 0.f, lo = 0.f;
+    if (src >= 0 && c <= w) {
+      double z;
+      if (c < w) {
+        const double v = c < k ? (double)x[src * ldx + c] : (double)y[src * ldy + (c - k)];
+        bad |= !isfinite(v);
+        z = v - shift[c];  // exact for fp32 inputs and an fp32 shift
+      } else {
+        z = 1.0;  // ones column: column sums ride in the Gram
+      }
+      hi = tf32_rn((float)z);
+      lo = tf32_rn((float)(z - (double)hi));
+    }
+    s_hi[rr][tx] = hi;
+    s_lo[rr][tx] = lo;
+  }
+  __syncthreads();
+  for (int cc = ty; cc < 32; cc += 8) {
+    const int64_t c = c0 + cc;
+    if (c < kp && r0 + tx < zrows) {
+      zt_hi[c * zrows + r0 + tx] = s_hi[tx][cc];
+      zt_lo[c * zrows + r0 + tx] = s_lo[tx][cc];
+    }
+  }
+  if (__any_sync(0xffffffffu, bad) && tx == 0) atomicExch(nonfinite, 1);
+}
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+bool make_map(CUtensorMap* map, const float* base, int64_t zrows, int64_t kp) {
+  EncodeTiledFn enc = encode_fn();
+  if (!enc) return false;
+  const cuuint64_t dims[2] = {(cuuint64_t)zrows, (cuuint64_t)kp};
+  const cuuint64_t strides[1] = {(cuuint64_t)zrows * sizeof(float)};
+  const cuuint32_t box[2] = {KS, TT};
+  const cuuint32_t estr[2] = {1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+}  // namespace
+
+void launch_reorder_split_t(int dtype, const void* x, int64_t ldx, const void* y, int64_t ldy, int64_t k, int64_t m,
+                            const int64_t* src_row, int64_t zrows, int64_t kp, const double* shift, float* zt_hi,
+                            float* zt_lo, int* nonfinite, cudaStream_t s) {
+  dim3 grid((unsigned)((zrows + 31) / 32), (unsigned)((kp + 31) / 32));
+  if (dtype == 0)
+    reorder_split_t_kernel<double><<<grid, 256, 0, s>>>((const double*)x, ldx, (const double*)y, ldy, k, m, src_row,
+                                                        zrows, kp, shift, zt_hi, zt_lo, nonfinite);
+  else
+    reorder_split_t_kernel<float><<<grid, 256, 0, s>>>((const float*)x, ldx, (const float*)y, ldy, k, m, src_row,
+                                                       zrows, kp, shift, zt_hi, zt_lo, nonfinite);
+}
+
+bool launch_gram_tf32(const float* zt_hi, const float* zt_lo, int64_t zrows, int64_t kp, const GramTask* segs,
+                      int64_t nseg, const int2* tiles128, int ntiles, double* part, int nterms, cudaStream_t s) {
+  CUtensorMap mh, ml;
+  if (!make_map(&mh, zt_hi, zrows, kp) || !make_map(&ml, zt_lo, zrows, kp)) return false;
+  cudaFuncSetAttribute(gram_tf32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemTf32);
+  const int64_t blocks = nseg * (int64_t)ntiles;
+  if (blocks > 0) gram_tf32_kernel<<<(unsigned)blocks, kThreads, kSmemTf32, s>>>(mh, ml, segs, tiles128, ntiles, kp, part, nterms);
+  return true;
+}
+
+}  // namespace cvg

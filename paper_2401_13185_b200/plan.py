@@ -163,13 +163,16 @@ def exchange_partials(mine, world: int, group=None):
     dist.all_gather(parts, mine, group=group)
     return torch.cat(parts)
 
-def gram_tiles(k: int, m: int):
-    """Upper 64x64 tiles the fold Gram computes (mirror of engine.cu gram_tiles)."""
-    kp = -(-(k + m + 1) // 64) * 64
-    nt, tx, to = kp // 64, (k - 1) // 64, (k + m) // 64
+def gram_tiles(k: int, m: int, edge: int = 64):
+    """Upper tiles the fold Gram computes (mirror of engine.cu gram_tiles)."""
+    kp = -(-(k + m + 1) // edge) * edge
+    nt, tx, to = kp // edge, (k - 1) // edge, (k + m) // edge
     return [(i, j) for i in range(nt) for j in range(i, nt) if i <= tx or j == i or j == to]
 
 
-def executed_gram_flops(n: int, k: int, m: int, p: int) -> float:
-    """DMMA flops the Gram kernel issues for n rows (fold padding ignored)."""
+def executed_gram_flops(n: int, k: int, m: int, p: int, f32: bool = False) -> float:
+    """Tensor-core flops the Gram kernel issues for n rows (fold padding ignored):
+    64x64 DMMA tiles for fp64; 128x128 tcgen05 tiles x 3 TF32 products for fp32."""
+    if f32:
+        return 3 * 2.0 * len(gram_tiles(k, m, 128)) * 128 * 128 * n
     return 2.0 * len(gram_tiles(k, m)) * 64 * 64 * n

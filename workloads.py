@@ -22,6 +22,11 @@ SHAPES = {0: (10_000, 50, 5, 10), 1: (1_000_000, 500, 10, 100), 2: (100_000, 200
           3: (4_000_000, 1024, 16, 20), 4: (10_000_000, 256, 32, 5)}
 CONFIGS = {0: list(range(16)), 1: [15], 2: [12, 10], 3: [0, 1, 2, 3, 4, 5, 6, 7, 8, 10, 12, 14], 4: [15]}
 DTYPES = {0: np.float64, 1: np.float64, 2: np.float64, 3: np.float32, 4: np.float64}
+DESCRIPTIONS = {0: "all 16 flag combinations, labels U[1,P]",
+                1: "center+scale X and Y, near-equal folds via random_partitioning",
+                2: "Dirichlet(2) fold sizes, 10% of columns sigma=1e-3; center X,Y then center+scale X",
+                3: "fp32 inputs, X = mu + sigma*t5, 12 distinct flag combinations, tcgen05 3xTF32",
+                4: "contiguous fold blocks, center+scale X and Y"}
 
 
 @dataclass
