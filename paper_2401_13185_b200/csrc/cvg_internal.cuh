@@ -94,7 +94,8 @@ void launch_hadamard(const double* mat, int64_t rows, int64_t cols, const double
 // reductions and the epilogue; the fp32 Gram uses the 128-tile list.
 std::vector<int2> gram_tiles(int64_t k, int64_t m, int64_t kp, int edge = kTile);
 
-// K1T + K2' (fp32 inputs): bucket/shift/split into TF32 hi + lo, transposed;
+// K1T + K2' (fp32 inputs): bucket/shift/split into TF32 hi + lo, transposed in
+// 32-row blocks;
 // then the tcgen05 kind::tf32 Gram (3 products: hi·hi + hi·lo + lo·hi).
 void launch_reorder_split_t(int dtype, const void* x, int64_t ldx, const void* y, int64_t ldy, int64_t k, int64_t m,
                             const int64_t* src_row, int64_t zrows, int64_t kp, const double* shift, float* zt_hi,

@@ -276,7 +276,7 @@ Status Plan::plan_segments() {
   cudaStream_t s = ctx_->stream;
   CVG_TRY(zbase_d_.ensure(sizeof(int64_t) * std::max(nown, 1)));
   CVG_TRY(src_row_.ensure(sizeof(int64_t) * std::max<int64_t>(zrows_, 1)));
-  if (dtype_ == 1) {  // transposed TF32 hi / lo operands for the tcgen05 Gram
+  if (dtype_ == 1) {  // blocked-transposed TF32 hi / lo operands for the tcgen05 Gram
     CVG_TRY(zt_hi_.ensure(sizeof(float) * std::max<int64_t>(zrows_, 32) * kp_));
     CVG_TRY(zt_lo_.ensure(sizeof(float) * std::max<int64_t>(zrows_, 32) * kp_));
   } else {
@@ -346,7 +346,7 @@ Status Plan::gram(const void* d_x, int64_t ldx, const void* d_y, int64_t ldy, co
   }
   CVG_CK(cudaMemsetAsync(flag_.as<void>(), 0, sizeof(int), s));
   if (dtype_ == 1) {
-    // fp32: K1T (bucket, shift, TF32 split, transpose) then the tcgen05 Gram.
+    // fp32: K1T (bucket, shift, TF32 split, blocked transpose) then the tcgen05 Gram.
     if (zrows_ > 0) {
       {
         Timed t(ctx_, kReorder);

@@ -59,6 +59,9 @@ __global__ void __launch_bounds__(NT, 2)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t4 = lane & 3;
   const int wi = (warp >> 2) * 32, wj = (warp & 3) * 16;
+  // In diagonal tiles the warps whose 32x16 block lies strictly below the
+  // diagonal skip the MMA loop (warp-uniform; the epilogue reads j >= i only).
+  const bool idle = diag && wi >= wj + 16;
 
   auto load_stage = [&](int step, int buf) {
     const double* src = zb + (int64_t)step * KC * kp;
@@ -92,6 +95,7 @@ __global__ void __launch_bounds__(NT, 2)
       if (nxt < nsteps) load_stage(nxt, nxt % STAGES);
       cp_async_commit();
     }
+    if (idle) continue;
     const double* sA = smem + (step % STAGES) * 2 * kSlab;
     const double* sB = diag ? sA : sA + kSlab;
 #pragma unroll

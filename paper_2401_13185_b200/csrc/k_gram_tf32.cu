@@ -12,10 +12,14 @@
 // in the other buffer; partials leave as fp64 and all later sums (K4) and the
 // epilogue (K5) are fp64.
 //
-// K1T writes the bucketed, shifted, split operand TRANSPOSED (Zt[col][row]) so
-// both MMA operands are K-major (contraction over rows is the contiguous axis):
-// one TMA box = 128 columns x 32 rows = 128 rows of 128 B, 128B-swizzled, the
-// canonical K-major SWIZZLE_128B UMMA layout (SBO = 1024 B).
+// K1T writes the bucketed, shifted, split operand transposed in 32-row blocks,
+// Zt[row / 32][col][row % 32], so both MMA operands are K-major (contraction
+// over rows is the contiguous axis) and every 32-row block is one contiguous
+// run of kp x 128 B.  One 3-D TMA box {32 rows, 128 columns, 1 block} = 128
+// rows of 128 B, 128B-swizzled: the canonical K-major SWIZZLE_128B UMMA layout
+// (SBO = 1024 B).  Measured alternatives: a [col][row] transpose (multi-MB
+// column pitch) halves the Gram's speed; row-major Z with MN-major operands
+// (SWIZZLE_128B_BASE32B) costs the Gram 9%.
 //
 // K2' roles (10 warps, 1 CTA per SM, 192 KB of stages, 256 TMEM columns):
 //   warp 0      TMA producer: hi/lo slabs of both column tiles per 32-row stage
@@ -38,6 +42,7 @@ constexpr int kSmemTf32 = NST * kStageBytes + 1024;  // + alignment slack
 constexpr int kDrainSteps = 4;                // 128 rows per fp32 accumulation chunk
 constexpr int kEpiWarps = 8;                  // 4 TMEM lane quarters x 2 column halves
 constexpr int kThreads = 64 + 32 * kEpiWarps;
+
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -66,11 +71,12 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
                : "memory");
 }
 
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                                            int c2) {
   asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];\n" ::
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];\n" ::
           "r"(smem_u32(dst)),
-      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
       : "memory");
 }
 
@@ -159,12 +165,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t ph = (uint32_t)(it / NST) & 1u;
         mbar_wait(&empty_bar[s], ph ^ 1u);
         mbar_expect_tx(&full_bar[s], bytes);
-        const int r0 = (int)(task.zrow + (int64_t)it * KS);
-        tma_load_2d(op(s, 0), &map_hi, &full_bar[s], r0, tile.x * TT);
-        if (nterms == 3) tma_load_2d(op(s, 1), &map_lo, &full_bar[s], r0, tile.x * TT);
+        const int blk = (int)(task.zrow / KS) + it;  // 32-row block index
+        tma_load_3d(op(s, 0), &map_hi, &full_bar[s], 0, tile.x * TT, blk);
+        if (nterms == 3) tma_load_3d(op(s, 1), &map_lo, &full_bar[s], 0, tile.x * TT, blk);
         if (!diag) {
-          tma_load_2d(op(s, 2), &map_hi, &full_bar[s], r0, tile.y * TT);
-          if (nterms == 3) tma_load_2d(op(s, 3), &map_lo, &full_bar[s], r0, tile.y * TT);
+          tma_load_3d(op(s, 2), &map_hi, &full_bar[s], 0, tile.y * TT, blk);
+          if (nterms == 3) tma_load_3d(op(s, 3), &map_lo, &full_bar[s], 0, tile.y * TT, blk);
         }
       }
     }
@@ -236,7 +242,15 @@ __device__ __forceinline__ float tf32_rn(float v) {
   return __uint_as_float(u);
 }
 
-// K1T: bucket, shift, split, transpose.  One CTA per (32 bucketed rows, 32 columns).
+// K1T: bucket, shift, TF32-split, transpose into Zt[block][col][32] (HBM-bound).
+// One CTA per 32 bucketed rows, 128-column chunks through a padded shared-memory
+// transpose.  Each thread owns 4 columns (shifts in registers for the chunk) and
+// issues its 4 row loads (float4, 512 B per warp) before using any; each
+// column's 32 rows leave as 128 B, a warp covering 4 adjacent columns = 512
+// contiguous bytes.  The split is pure fp32: fl(x - c) is within 2^-24 of z and
+// hi / lo are exact (an fp64 convert chain made this pass compute-bound, ~2.6 TB/s).
+constexpr int kK1tCols = 128;
+
 template <typename T>
 __global__ void __launch_bounds__(256) reorder_split_t_kernel(const T* __restrict__ x, int64_t ldx,
                                                               const T* __restrict__ y, int64_t ldy, int64_t k,
@@ -245,41 +259,91 @@ __global__ void __launch_bounds__(256) reorder_split_t_kernel(const T* __restric
                                                               const double* __restrict__ shift,
                                                               float* __restrict__ zt_hi, float* __restrict__ zt_lo,
                                                               int* __restrict__ nonfinite) {
-  __shared__ float s_hi[32][33], s_lo[32][33];
-  const int64_t r0 = (int64_t)blockIdx.x * 32;
-  const int64_t c0 = (int64_t)blockIdx.y * 32;
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+  __shared__ float s_hi[kK1tCols][33], s_lo[kK1tCols][33];
+  __shared__ int64_t s_src[32];
+  const int64_t blk = blockIdx.x;
+  const int t = threadIdx.x;
   const int64_t w = k + m;
-  bool bad = false;
-  for (int rr = ty; rr < 32; rr += 8) {
-    const int64_t zr = r0 + rr;
-    const int64_t src = zr < zrows ? src_row[zr] : -1;
-    const int64_t c = c0 + tx;
-    float hi = 0.f, lo = 0.f;
-    if (src >= 0 && c <= w) {
-      double z;
-      if (c < w) {
-        const double v = c < k ? (double)x[src * ldx + c] : (double)y[src * ldy + (c - k)];
-        bad |= !isfinite(v);
-        z = v - shift[c];  // exact for fp32 inputs and an fp32 shift
-      } else {
-        z = 1.0;  // ones column: column sums ride in the Gram
-      }
-      hi = tf32_rn((float)z);
-      lo = tf32_rn((float)(z - (double)hi));
-    }
-    s_hi[rr][tx] = hi;
-    s_lo[rr][tx] = lo;
-  }
+  if (t < 32) s_src[t] = blk * 32 + t < zrows ? src_row[blk * 32 + t] : -1;
   __syncthreads();
-  for (int cc = ty; cc < 32; cc += 8) {
-    const int64_t c = c0 + cc;
-    if (c < kp && r0 + tx < zrows) {
-      zt_hi[c * zrows + r0 + tx] = s_hi[tx][cc];
-      zt_lo[c * zrows + r0 + tx] = s_lo[tx][cc];
+  const bool vec = (k % 4 == 0) && (ldx % 4 == 0) && sizeof(T) == 4;
+  const int q4 = (t & 31) * 4;  // this thread's 4 columns within the chunk
+  const int r_lo = t >> 5;      // rows r_lo + 8j, j = 0..3
+  bool bad = false;
+  for (int64_t c0 = 0; c0 < kp; c0 += kK1tCols) {
+    const int64_t c = c0 + q4;
+    float sh[4];
+    int kind[4];  // 0 data, 1 ones column, 2 padding
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int64_t ce = c + e;
+      sh[e] = ce < w ? (float)shift[ce] : 0.f;
+      kind[e] = ce < w ? 0 : (ce == w ? 1 : 2);
     }
+    const bool fast = vec && c + 3 < k;
+    float v[4][4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int64_t src = s_src[r_lo + 8 * j];
+      if (fast) {
+        float4 f = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (src >= 0) f = *reinterpret_cast<const float4*>(reinterpret_cast<const float*>(x) + src * ldx + c);
+        v[j][0] = f.x;
+        v[j][1] = f.y;
+        v[j][2] = f.z;
+        v[j][3] = f.w;
+      } else {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int64_t ce = c + e;
+          float val = 0.f;
+          if (src >= 0) {
+            if (ce < k)
+              val = (float)x[src * ldx + ce];
+            else if (ce < w)
+              val = (float)y[src * ldy + (ce - k)];
+          }
+          v[j][e] = val;
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int rr = r_lo + 8 * j;
+      const bool live = s_src[rr] >= 0;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        float z = 0.f;
+        if (live) {
+          if (kind[e] == 0) {
+            bad |= !isfinite(v[j][e]);
+            z = v[j][e] - sh[e];
+          } else if (kind[e] == 1) {
+            z = 1.f;  // ones column: column sums ride in the Gram
+          }
+        }
+        const float hi = tf32_rn(z);
+        s_hi[q4 + e][rr] = hi;
+        s_lo[q4 + e][rr] = tf32_rn(z - hi);
+      }
+    }
+    __syncthreads();
+    // write: 8 threads per column (16 B each), 32 columns per pass
+#pragma unroll
+    for (int cc = t >> 3; cc < kK1tCols; cc += 32) {
+      const int64_t col = c0 + cc;
+      const int r4 = (t & 7) * 4;
+      if (col < kp) {
+        const int64_t off = (blk * kp + col) * 32 + r4;  // Zt[block][col][row % 32]
+        *reinterpret_cast<float4*>(zt_hi + off) =
+            make_float4(s_hi[cc][r4], s_hi[cc][r4 + 1], s_hi[cc][r4 + 2], s_hi[cc][r4 + 3]);
+        *reinterpret_cast<float4*>(zt_lo + off) =
+            make_float4(s_lo[cc][r4], s_lo[cc][r4 + 1], s_lo[cc][r4 + 2], s_lo[cc][r4 + 3]);
+      }
+    }
+    __syncthreads();
   }
-  if (__any_sync(0xffffffffu, bad) && tx == 0) atomicExch(nonfinite, 1);
+  if (__any_sync(0xffffffffu, bad) && (t & 31) == 0) atomicExch(nonfinite, 1);
 }
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -301,11 +365,11 @@ EncodeTiledFn encode_fn() {
 bool make_map(CUtensorMap* map, const float* base, int64_t zrows, int64_t kp) {
   EncodeTiledFn enc = encode_fn();
   if (!enc) return false;
-  const cuuint64_t dims[2] = {(cuuint64_t)zrows, (cuuint64_t)kp};
-  const cuuint64_t strides[1] = {(cuuint64_t)zrows * sizeof(float)};
-  const cuuint32_t box[2] = {KS, TT};
-  const cuuint32_t estr[2] = {1, 1};
-  return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, estr,
+  const cuuint64_t dims[3] = {(cuuint64_t)KS, (cuuint64_t)kp, (cuuint64_t)(zrows / KS)};  // Zt[block][col][32]
+  const cuuint64_t strides[2] = {(cuuint64_t)KS * sizeof(float), (cuuint64_t)kp * KS * sizeof(float)};
+  const cuuint32_t box[3] = {KS, TT, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims, strides, box, estr,
              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
@@ -315,7 +379,7 @@ bool make_map(CUtensorMap* map, const float* base, int64_t zrows, int64_t kp) {
 void launch_reorder_split_t(int dtype, const void* x, int64_t ldx, const void* y, int64_t ldy, int64_t k, int64_t m,
                             const int64_t* src_row, int64_t zrows, int64_t kp, const double* shift, float* zt_hi,
                             float* zt_lo, int* nonfinite, cudaStream_t s) {
-  dim3 grid((unsigned)((zrows + 31) / 32), (unsigned)((kp + 31) / 32));
+  dim3 grid((unsigned)((zrows + 31) / 32));
   if (dtype == 0)
     reorder_split_t_kernel<double><<<grid, 256, 0, s>>>((const double*)x, ldx, (const double*)y, ldy, k, m, src_row,
                                                         zrows, kp, shift, zt_hi, zt_lo, nonfinite);
