@@ -190,8 +190,8 @@ def run_ours(args):
     x, y, labels, p, cfgs = workloads.make_device(cid, dev)
     masks = list(cfgs)  # every configuration the BASELINE config names, from one Gram pass
     flops = 2.0 * n * k * (k + m)
-    fb, fe = P.fold_range(p, rank, world)
-    plan = P.DevicePlan(n, k, m, p, fb, fe, dtype="f32" if x.dtype == torch.float32 else "f64", ctx=ctx)
+    plan = P.DevicePlan(n, k, m, p, dtype="f32" if x.dtype == torch.float32 else "f64", ctx=ctx, rank=rank,
+                        world=world)
     stream = torch.cuda.current_stream(dev)
     ctx.set_stream(stream.cuda_stream)
 

@@ -95,6 +95,16 @@ int cvg_run_all_folds(cvg_context* ctx, int dtype, const void* x, const void* y,
 int cvg_plan_create(cvg_context* ctx, int dtype, int64_t n, int64_t k, int64_t m, int32_t p, int32_t fold_begin,
                     int32_t fold_end, cvg_plan** out, char* err, size_t errlen);
 void cvg_plan_destroy(cvg_plan* plan);
+/* Rank mode: this plan is rank `rank` of `world` and owns its node of the
+ * canonical fold tree (cvg_fold_range's descent; when more ranks than folds
+ * remain, one fold's segment range is split further — P < G).  Decided at
+ * bind time; query it with cvg_plan_assignment.  Outputs are bit-identical to
+ * one GPU for power-of-two world sizes. */
+int cvg_plan_create_rank(cvg_context* ctx, int dtype, int64_t n, int64_t k, int64_t m, int32_t p, int32_t rank,
+                         int32_t world, cvg_plan** out, char* err, size_t errlen);
+/* Folds this plan emits after bind: [fold_begin, fold_end) (empty when this
+ * rank shares a fold whose outputs another rank of its group emits). */
+int cvg_plan_assignment(const cvg_plan* plan, int32_t* fold_begin, int32_t* fold_end);
 /* Device labels (n int32, 1-based).  Validates them (partition.hpp:21-45, and
  * check_scalable when require_scalable != 0) and builds the fold-bucketed row
  * order on the device (build_validation_partitions, partition.hpp:61-68). */

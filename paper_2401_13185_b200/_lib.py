@@ -36,6 +36,9 @@ SIGNATURES = {
     "cvg_run_all_folds": (c_int, [c_vp, c_int, c_vp, c_vp, c_i64, c_i64, c_i64, c_vp, c_i64, c_i32, c_vp, c_i32]
                           + [c_vp] * 8 + [c_char_p, c_size_t]),
     "cvg_plan_create": (c_int, [c_vp, c_int, c_i64, c_i64, c_i64, c_i32, c_i32, c_i32, c_vpp, c_char_p, c_size_t]),
+    "cvg_plan_create_rank": (c_int, [c_vp, c_int, c_i64, c_i64, c_i64, c_i32, c_i32, c_i32, c_vpp, c_char_p,
+                                     c_size_t]),
+    "cvg_plan_assignment": (c_int, [c_vp, c_vp, c_vp]),
     "cvg_plan_destroy": (None, [c_vp]),
     "cvg_plan_bind_labels": (c_int, [c_vp, c_vp, c_int, c_char_p, c_size_t]),
     "cvg_plan_gram": (c_int, [c_vp, c_vp, c_i64, c_vp, c_i64, c_vp, c_char_p, c_size_t]),

@@ -344,6 +344,29 @@ int cvg_plan_create(cvg_context* ctx, int dtype, int64_t n, int64_t k, int64_t m
   });
 }
 
+int cvg_plan_create_rank(cvg_context* ctx, int dtype, int64_t n, int64_t k, int64_t m, int32_t p, int32_t rank,
+                         int32_t world, cvg_plan** out, char* err, size_t errlen) {
+  return guarded(err, errlen, [&]() -> Status {
+    if (!ctx || !out) return Status::Err(CVG_E_INVALID_ARG, "null argument");
+    *out = nullptr;
+    auto* pl = new cvg_plan();
+    Status s = pl->plan.create_rank(ctx, dtype, n, k, m, p, rank, world);
+    if (!s.ok()) {
+      delete pl;
+      return s;
+    }
+    *out = pl;
+    return Status::Ok();
+  });
+}
+
+int cvg_plan_assignment(const cvg_plan* plan, int32_t* fold_begin, int32_t* fold_end) {
+  if (!plan || !fold_begin || !fold_end) return CVG_E_INVALID_ARG;
+  *fold_begin = plan->plan.fold_begin();
+  *fold_end = plan->plan.fold_end();
+  return CVG_OK;
+}
+
 void cvg_plan_destroy(cvg_plan* plan) {
   if (!plan) return;
   cudaStreamSynchronize(plan->plan.ctx()->stream);

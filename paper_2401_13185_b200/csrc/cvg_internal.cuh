@@ -41,8 +41,11 @@ struct Status {
 void launch_tile_histogram(const int32_t* labels, int64_t n, int32_t p, int32_t* tile_counts,
                            unsigned long long* bad_row, cudaStream_t s);
 void launch_tile_scan(int32_t* tile_counts, int64_t ntiles, int32_t p, int64_t* fold_counts, cudaStream_t s);
+// Rows at fold-relative bucketed positions outside [win_lo, win_hi) are dropped
+// (a rank owning only part of one fold's segments).
 void launch_scatter(const int32_t* labels, int64_t n, int32_t p, int32_t fold_begin, int32_t fold_end,
-                    int32_t* tile_offsets, const int64_t* fold_zbase, int64_t* src_row, cudaStream_t s);
+                    int32_t* tile_offsets, const int64_t* fold_zbase, int64_t win_lo, int64_t win_hi, int64_t* src_row,
+                    cudaStream_t s);
 
 // K1: gather + shift + ones column + zero padding (+ finiteness flag).
 void launch_reorder(int dtype, const void* x, int64_t ldx, const void* y, int64_t ldy, int64_t k, int64_t m,

@@ -169,6 +169,9 @@ Status Plan::create(cvg_context* ctx, int dtype, int64_t n, int64_t k, int64_t m
       return Status::Err(2, "fold count " + std::to_string(p) + " exceeds sample count " + std::to_string(n));
   }
   if (fb < 0 || fe > p || fb > fe) return Status::Err(4, "owned fold range is outside [0, p]");
+  rank_mode_ = false;
+  emits_ = true;
+  seg_lo_ = seg_hi_ = -1;
   kp_ = padded_cols(k, m, dtype);
   tiles_ = gram_tiles(k, m, kp_);
   tiles128_ = dtype == 1 ? gram_tiles(k, m, kp_, kTileF32) : std::vector<int2>{};
@@ -192,6 +195,57 @@ Status Plan::create(cvg_context* ctx, int dtype, int64_t n, int64_t k, int64_t m
   CVG_CK(cudaMemsetAsync(shift_.as<void>(), 0, sizeof(double) * kp_, ctx->stream));  // ones/padding columns
   CVG_TRY(flag_.ensure(sizeof(int)));
   return Status::Ok();
+}
+
+Status Plan::create_rank(cvg_context* ctx, int dtype, int64_t n, int64_t k, int64_t m, int32_t p, int32_t rank,
+                         int32_t world) {
+  if (world < 1 || rank < 0 || rank >= world) return Status::Err(4, "rank outside [0, world)");
+  CVG_TRY(create(ctx, dtype, n, k, m, p, 0, p, true));
+  rank_mode_ = true;
+  rank_ = rank;
+  world_ = world;
+  return Status::Ok();
+}
+
+void Plan::assign_rank() {
+  int32_t lo = 0, hi = world_, a = 0, b = p_;
+  int64_t s0 = -1, s1 = -1;
+  int32_t glo = 0, ghi = 0;
+  while (hi - lo > 1) {
+    const int32_t rmid = lo + (hi - lo) / 2;
+    if (b - a == 1) {  // one fold, several ranks: split its segments
+      if (s0 < 0) {
+        s0 = 0;
+        s1 = (round_up(counts_[a], kRowStep) + chunk_rows() - 1) / chunk_rows();
+        glo = lo;
+        ghi = hi;
+      }
+      const int64_t smid = s0 + (s1 - s0) / 2;
+      if (rank_ < rmid) {
+        hi = rmid;
+        s1 = smid;
+      } else {
+        lo = rmid;
+        s0 = smid;
+      }
+    } else {
+      const int32_t fmid = a + (b - a) / 2;
+      if (rank_ < rmid) {
+        hi = rmid;
+        b = fmid;
+      } else {
+        lo = rmid;
+        a = fmid;
+      }
+    }
+  }
+  fb_ = a;
+  fe_ = b;
+  seg_lo_ = s0;
+  seg_hi_ = s1;
+  group_lo_ = glo;
+  group_hi_ = ghi;
+  emits_ = s0 < 0 || rank_ == glo;
 }
 
 Status Plan::bind_labels(const int32_t* d_labels, bool validate, bool require_scalable) {
@@ -233,11 +287,14 @@ Status Plan::bind_labels(const int32_t* d_labels, bool validate, bool require_sc
           return Status::Err(3, "fold " + std::to_string(f + 1) + " leaves a training partition of " +
                                     std::to_string(n_ - counts_[f]) + " rows; scaling needs at least 2");
   }
+  if (rank_mode_) assign_rank();
   CVG_TRY(plan_segments());
   CVG_CK(cudaMemsetAsync(src_row_.as<void>(), 0xff, sizeof(int64_t) * std::max<int64_t>(zrows_, 1), s));
   {
     Timed t(ctx_, kBucket);
-    launch_scatter(d_labels, n_, p_, fb_, fe_, tile_counts_.as<int32_t>(), zbase_d_.as<int64_t>(),
+    const int64_t win_lo = seg_lo_ >= 0 ? seg_lo_ * chunk_rows() : 0;
+    const int64_t win_hi = seg_lo_ >= 0 ? win_lo + zrows_ : INT64_MAX;
+    launch_scatter(d_labels, n_, p_, fb_, fe_, tile_counts_.as<int32_t>(), zbase_d_.as<int64_t>(), win_lo, win_hi,
                    src_row_.as<int64_t>(), s);
   }
   CVG_TRY(count_launch());
@@ -263,13 +320,16 @@ Status Plan::plan_segments() {
   fold_seg_begin_.assign(1, 0);
   fold_zbase_.clear();
   zrows_ = 0;
+  const int64_t chunk = chunk_rows();
   for (int32_t f = fb_; f < fe_; ++f) {
     const int64_t padded = round_up(counts_[f], kRowStep);
+    // Owned window of the fold's bucketed rows: all of it, or (shared fold) segments [seg_lo_, seg_hi_).
+    const int64_t w0 = seg_lo_ >= 0 ? std::min(padded, seg_lo_ * chunk) : 0;
+    const int64_t w1 = seg_lo_ >= 0 ? std::min(padded, seg_hi_ * chunk) : padded;
     fold_zbase_.push_back(zrows_);
-    const int64_t chunk = dtype_ == 1 ? kChunkRowsF32 : kChunkRows;
-    for (int64_t off = 0; off < padded; off += chunk)
-      segs_.push_back(GramTask{zrows_ + off, std::min<int64_t>(chunk, padded - off)});
-    zrows_ += padded;
+    for (int64_t off = w0; off < w1; off += chunk)
+      segs_.push_back(GramTask{zrows_ + (off - w0), std::min<int64_t>(chunk, w1 - off)});
+    zrows_ += w1 - w0;
     fold_seg_begin_.push_back((int32_t)segs_.size());
   }
   const int nown = fe_ - fb_;
@@ -302,6 +362,20 @@ Status Plan::plan_segments() {
   CVG_TRY(foldbuf_.ensure(sizeof(double) * std::max(nmulti, 1) * kp_ * kp_));
   fold_ptrs_.assign(nown, nullptr);
   std::vector<TreeGroup> phase1;
+  if (seg_lo_ >= 0) {
+    // Shared fold: this plan's node is the sum over its segment range; the
+    // fold's full Gram is rebuilt from the group's partials in finish().
+    TreeGroup g{{}, local_.as<double>()};
+    for (size_t sgi = 0; sgi < segs_.size(); ++sgi) g.leaves.push_back(part_.as<double>() + (int64_t)sgi * kp_ * kp_);
+    phase1.push_back(std::move(g));
+    fold_ptrs_[0] = foldbuf_.as<double>();
+    CVG_TRY(fold_tree_.build(phase1, kp_, s));
+    CVG_TRY(local_tree_.build({}, kp_, s));
+    CVG_TRY(foldptr_d_.ensure(sizeof(void*)));
+    CVG_CK(cudaMemcpyAsync(foldptr_d_.as<void>(), fold_ptrs_.data(), sizeof(void*), cudaMemcpyHostToDevice, s));
+    CVG_CK(cudaStreamSynchronize(s));
+    return Status::Ok();
+  }
   int slot = 0;
   for (int f = 0; f < nown; ++f) {
     const int a = fold_seg_begin_[f], b = fold_seg_begin_[f + 1];
@@ -414,8 +488,19 @@ Status Plan::finish(const double* d_rank_partials, int32_t n_ranks, const double
     if (!owns_all()) return Status::Err(4, "plan owns a subset of folds: pass every rank's partial");
     total = local_.as<double>();
   }
-  const int nown = fe_ - fb_;
-  if (nown == 0) return Status::Ok();
+  if (seg_lo_ >= 0) {
+    // Shared fold: its Gram is the group's node of the canonical tree.
+    if (!d_rank_partials || n_ranks != world_) return Status::Err(4, "shared fold: pass every rank's partial");
+    TreeGroup g{{}, foldbuf_.as<double>()};
+    for (int r = group_lo_; r < group_hi_; ++r) g.leaves.push_back(d_rank_partials + (int64_t)r * kp_ * kp_);
+    CVG_TRY(group_tree_.build({g}, kp_, s));
+    CVG_TRY(group_tree_.run(ctx_, tiles_d_.as<int2>(), (int)tiles_.size(), kp_));
+  }
+  const int nown = this->nown();
+  if (nown == 0) {
+    CVG_CK(cudaStreamSynchronize(s));
+    return Status::Ok();
+  }
   CVG_TRY(st_mz_.ensure(sizeof(double) * nown * w_));
   CVG_TRY(st_sT_.ensure(sizeof(double) * nown * w_));
   CVG_TRY(st_sd_.ensure(sizeof(double) * nown * w_));

@@ -57,6 +57,11 @@ class Plan {
  public:
   Status create(cvg_context* ctx, int dtype, int64_t n, int64_t k, int64_t m, int32_t p, int32_t fb, int32_t fe,
                 bool validate);
+  // Rank mode: the owned part of the canonical fold tree is decided at bind time
+  // (cvg_fold_range's descent, continued into one fold's segment range when
+  // more ranks than folds remain — SURVEY.md §8e's P < G case).
+  Status create_rank(cvg_context* ctx, int dtype, int64_t n, int64_t k, int64_t m, int32_t p, int32_t rank,
+                     int32_t world);
   // Device labels -> fold-bucketed row order (validates like partition.hpp:21-58 when `validate`).
   Status bind_labels(const int32_t* d_labels, bool validate, bool require_scalable);
   // Explicit ascending rows of the single owned fold (fold_products / precompute_global).
@@ -73,7 +78,9 @@ class Plan {
   const double* shift() const { return shift_.as<double>(); }
   int64_t kp() const { return kp_; }
   int64_t partial_count() const { return kp_ * kp_; }
-  int nown() const { return fe_ - fb_; }
+  int nown() const { return emits_ ? fe_ - fb_ : 0; }  // folds this plan emits
+  int32_t fold_begin() const { return fb_; }
+  int32_t fold_end() const { return emits_ ? fe_ : fb_; }
   const std::vector<int64_t>& counts() const { return counts_; }
   bool owns_all() const { return fb_ == 0 && fe_ == p_; }
   int64_t n() const { return n_; }
@@ -89,6 +96,8 @@ class Plan {
  private:
   Status plan_segments();
   Status count_launch(int n = 1);
+  void assign_rank();  // rank mode: fb_/fe_, segment window, fold group
+  int64_t chunk_rows() const { return dtype_ == 1 ? kChunkRowsF32 : kChunkRows; }
 
   cvg_context* ctx_ = nullptr;
   int dtype_ = 0;
@@ -101,6 +110,11 @@ class Plan {
   std::vector<int64_t> fold_zbase_;
   int64_t zrows_ = 0;
   bool bound_ = false, grammed_ = false;
+  bool rank_mode_ = false, emits_ = true;
+  int32_t rank_ = 0, world_ = 1;
+  int64_t seg_lo_ = -1, seg_hi_ = -1;   // shared fold: owned segment range (else -1)
+  int32_t group_lo_ = 0, group_hi_ = 0; // ranks sharing the fold
+  TreeProgram group_tree_;
 
   DevBuf tiles_d_, out_tiles_d_, tiles128_d_, zt_hi_, zt_lo_, tile_counts_, fold_counts_, bad_, zbase_d_, src_row_, z_, part_, foldbuf_, local_,
       total_, shift_, flag_, segs_d_, foldptr_d_, nval_d_, st_mz_, st_sT_, st_sd_, cfg_d_;

@@ -39,10 +39,16 @@ def _dptr(t) -> Optional[int]:
 
 
 class DevicePlan:
-    """Thin owner of a cvg_plan; arguments are torch CUDA tensors."""
+    """Thin owner of a cvg_plan; arguments are torch CUDA tensors.
+
+    Either an explicit fold range, or ``rank``/``world``: the canonical fold-
+    tree node is then chosen at bind time (shared folds when world > p) and
+    ``fold_begin``/``fold_end`` give the folds this plan emits.
+    """
 
     def __init__(self, n: int, k: int, m: int, p: int, fold_begin: int = 0, fold_end: Optional[int] = None,
-                 dtype: str = "f64", ctx: Optional[Context] = None):
+                 dtype: str = "f64", ctx: Optional[Context] = None, rank: Optional[int] = None,
+                 world: Optional[int] = None):
         import torch
 
         self.ctx = ctx or get_context()
@@ -53,8 +59,12 @@ class DevicePlan:
         self.ctx.set_stream(torch.cuda.current_stream(self.ctx.device).cuda_stream)
         h = ctypes.c_void_p()
         buf = L.err_buf()
-        _check(L.lib().cvg_plan_create(self.ctx.handle, self.dtype_code, n, k, m, p, self.fold_begin, self.fold_end,
-                                       ctypes.byref(h), buf, len(buf)), buf)
+        if rank is not None:
+            _check(L.lib().cvg_plan_create_rank(self.ctx.handle, self.dtype_code, n, k, m, p, rank, world,
+                                                ctypes.byref(h), buf, len(buf)), buf)
+        else:
+            _check(L.lib().cvg_plan_create(self.ctx.handle, self.dtype_code, n, k, m, p, self.fold_begin,
+                                           self.fold_end, ctypes.byref(h), buf, len(buf)), buf)
         self._h = h
         import weakref
 
@@ -70,6 +80,9 @@ class DevicePlan:
     def bind_labels(self, labels, require_scalable: bool) -> None:
         buf = L.err_buf()
         _check(L.lib().cvg_plan_bind_labels(self._h, _dptr(labels), int(require_scalable), buf, len(buf)), buf)
+        b, e = ctypes.c_int32(), ctypes.c_int32()
+        L.lib().cvg_plan_assignment(self._h, ctypes.addressof(b), ctypes.addressof(e))
+        self.fold_begin, self.fold_end = b.value, e.value
 
     def gram(self, x, y, shift: Optional[np.ndarray] = None) -> None:
         buf = L.err_buf()
@@ -132,11 +145,11 @@ def run_all_folds_device(x, y, labels, p: int, cfgs, group=None, plan=None, shif
     n, k = x.shape
     m = y.shape[1]
     if plan is None:
-        fb, fe = fold_range(p, rank, world)
         if plan_factory is not None:
+            fb, fe = fold_range(p, rank, world)
             plan = plan_factory(n, k, m, p, fb, fe)
         else:
-            plan = DevicePlan(n, k, m, p, fb, fe, dtype="f32" if x.dtype == torch.float32 else "f64")
+            plan = DevicePlan(n, k, m, p, dtype="f32" if x.dtype == torch.float32 else "f64", rank=rank, world=world)
     plan.bind_labels(labels, require_scalable=any(c.any_scale() for c in cfgs))
     plan.gram(x, y, shift)
     if world > 1:
