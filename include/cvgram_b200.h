@@ -144,6 +144,23 @@ int cvg_global_fold_products(cvg_global* g, const int64_t* v_rows, int64_t n_val
                              double* xty_t, double* mean_x_t, double* mean_y_t, double* std_x_t, double* std_y_t,
                              int64_t* n_train, char* err, size_t errlen);
 
+/* ------------------------------------------ baseline engine (baseline.hpp) */
+/* baseline_fold_products (baseline.hpp:79-97) on the device: every fold's
+ * training rows are contracted directly in their own mean-centered basis (two
+ * passes: training means, then the Gram of x - mean), with no downdate; the
+ * independent engine `cvgram verify` checks the fast path against.
+ * Same argument layout as cvg_run_all_folds.  Cost: Θ(P·N·K(K+M)). */
+int cvg_baseline_fold_products(cvg_context* ctx, int dtype, const void* x, const void* y, int64_t n, int64_t k,
+                               int64_t m, const int32_t* labels, int64_t n_labels, int32_t p,
+                               const uint32_t* cfg_masks, int32_t n_cfg, double* xtx, double* xty, double* mean_x,
+                               double* mean_y, double* std_x, double* std_y, int64_t* n_train, int64_t* n_val,
+                               char* err, size_t errlen);
+/* baseline_single_fold (baseline.hpp:42-76) for validation rows v_rows (0-based, ascending). */
+int cvg_baseline_single_fold(cvg_context* ctx, int dtype, const void* x, const void* y, int64_t n, int64_t k,
+                             int64_t m, const int64_t* v_rows, int64_t n_val, uint32_t cfg, double* xtx_t,
+                             double* xty_t, double* mean_x_t, double* mean_y_t, double* std_x_t, double* std_y_t,
+                             int64_t* n_train, char* err, size_t errlen);
+
 /* ------------------------------------------ seeded test data (random.hpp) */
 /* An opaque std::mt19937_64 stream (random.hpp:14-18; standard-specified, so
  * seeds reproduce the reference's test data bit for bit). */

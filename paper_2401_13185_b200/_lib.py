@@ -49,6 +49,10 @@ SIGNATURES = {
     "cvg_global_destroy": (None, [c_vp]),
     "cvg_global_export": (c_int, [c_vp, c_u32] + [c_vp] * 8 + [c_char_p, c_size_t]),
     "cvg_global_fold_products": (c_int, [c_vp, c_vp, c_i64, c_u32] + [c_vp] * 7 + [c_char_p, c_size_t]),
+    "cvg_baseline_fold_products": (c_int, [c_vp, c_int, c_vp, c_vp, c_i64, c_i64, c_i64, c_vp, c_i64, c_i32, c_vp,
+                                           c_i32] + [c_vp] * 8 + [c_char_p, c_size_t]),
+    "cvg_baseline_single_fold": (c_int, [c_vp, c_int, c_vp, c_vp, c_i64, c_i64, c_i64, c_vp, c_i64, c_u32] + [c_vp] * 7
+                                 + [c_char_p, c_size_t]),
     "cvg_rng_create": (c_vp, [c_u64]),
     "cvg_rng_destroy": (None, [c_vp]),
     "cvg_rng_next": (c_u64, [c_vp]),

@@ -106,6 +106,33 @@ Status small_vector_op(cvg_context* ctx, std::initializer_list<std::pair<const d
   return cvg::cuda_status(cudaStreamSynchronize(ctx->stream), "stream synchronize");
 }
 
+// One fold of the baseline engine: training rows t_rows of (d_x, d_y), two
+// Gram passes (any shift -> training means; then the exact-mean basis), the
+// direct epilogue per configuration.  Device outputs for this fold:
+// xtx[c] at xtx + c*cstride_xx, xty likewise; stats [k|m] (may be null).
+Status baseline_rows(cvg_context* ctx, int dtype, const void* d_x, const void* d_y, int64_t k, int64_t m,
+                     const std::vector<int64_t>& t_rows, const uint32_t* cfgs, int32_t ncfg, double* d_xtx,
+                     int64_t cstride_xx, double* d_xty, int64_t cstride_xy, double* d_mx, double* d_my,
+                     double* d_sx, double* d_sy, cvg::DevBuf& mean_buf) {
+  cvg::Plan pl;
+  const int64_t nt = (int64_t)t_rows.size();
+  Status s = pl.create(ctx, dtype, std::max<int64_t>(nt, 2), k, m, 1, 0, 1, false);
+  if (!s.ok()) return s;
+  if (!(s = pl.bind_rows(t_rows.data(), nt)).ok()) return s;
+  if (!(s = pl.gram(d_x, k, d_y, m, nullptr, nullptr)).ok()) return s;  // pass 1: means
+  if (!(s = mean_buf.ensure(sizeof(double) * (k + m))).ok()) return s;
+  if (!(s = pl.direct_means(mean_buf.as<double>())).ok()) return s;
+  if (!(s = pl.gram(d_x, k, d_y, m, nullptr, mean_buf.as<double>())).ok()) return s;  // pass 2: centered
+  for (int32_t c = 0; c < ncfg; ++c) {
+    const bool first = c == 0;
+    if (!(s = pl.finish_direct(&cfgs[c], 1, d_xtx + c * cstride_xx, d_xty + c * cstride_xy, first ? d_mx : nullptr,
+                               first ? d_my : nullptr, first ? d_sx : nullptr, first ? d_sy : nullptr))
+             .ok())
+      return s;
+  }
+  return Status::Ok();
+}
+
 }  // namespace
 
 extern "C" {
@@ -325,6 +352,133 @@ int cvg_run_all_folds(cvg_context* ctx, int dtype, const void* x, const void* y,
     }
 #undef TRY
     return Status::Ok();
+  });
+}
+
+int cvg_baseline_fold_products(cvg_context* ctx, int dtype, const void* x, const void* y, int64_t n, int64_t k,
+                               int64_t m, const int32_t* labels, int64_t n_labels, int32_t p,
+                               const uint32_t* cfg_masks, int32_t n_cfg, double* xtx, double* xty, double* mean_x,
+                               double* mean_y, double* std_x, double* std_y, int64_t* n_train, int64_t* n_val,
+                               char* err, size_t errlen) {
+  return guarded(err, errlen, [&]() -> Status {
+    if (!ctx) return Status::Err(CVG_E_INVALID_ARG, "null context");
+    if (n < 2) return Status::Err(CVG_E_DIMENSION, "need at least 2 samples");
+    if (k < 1 || m < 1) return Status::Err(CVG_E_DIMENSION, "x and y must each have at least one column");
+    if (n_cfg < 1 || !cfg_masks) return Status::Err(CVG_E_INVALID_ARG, "need at least one configuration");
+    for (int32_t c = 0; c < n_cfg; ++c)
+      if (cfg_masks[c] > 15u) return Status::Err(CVG_E_INVALID_ARG, "configuration mask outside 0..15");
+    // baseline.hpp:82-87
+    if (n_labels != n) return Status::Err(CVG_E_DIMENSION, "partitioning length does not match sample count");
+    std::vector<int64_t> counts;
+    Status s = validate_partitioning(labels, n, p, &counts);
+    if (!s.ok()) return s;
+    if (any_scale(cfg_masks, n_cfg) && !(s = check_scalable(counts, n)).ok()) return s;
+    if (!(s = cvg::cuda_status(cudaSetDevice(ctx->device), "cudaSetDevice")).ok()) return s;
+    if (!ctx->scratch) ctx->scratch.reset(new cvg::HostScratch());
+    cvg::HostScratch& sc = *ctx->scratch;
+    cudaStream_t st = ctx->stream;
+    const size_t e = elt(dtype);
+    if (!(s = sc.x.ensure(e * n * k)).ok() || !(s = sc.y.ensure(e * n * m)).ok()) return s;
+    if (!(s = cvg::cuda_status(cudaMemcpyAsync(sc.x.as<void>(), x, e * n * k, cudaMemcpyHostToDevice, st), "H2D x"))
+             .ok() ||
+        !(s = cvg::cuda_status(cudaMemcpyAsync(sc.y.as<void>(), y, e * n * m, cudaMemcpyHostToDevice, st), "H2D y"))
+             .ok())
+      return s;
+    const size_t nxx = (size_t)n_cfg * p * k * k, nxy = (size_t)n_cfg * p * k * m;
+    if (!(s = sc.xtx.ensure(sizeof(double) * nxx)).ok() || !(s = sc.xty.ensure(sizeof(double) * nxy)).ok() ||
+        !(s = sc.mx.ensure(sizeof(double) * p * k)).ok() || !(s = sc.my.ensure(sizeof(double) * p * m)).ok() ||
+        !(s = sc.sx.ensure(sizeof(double) * p * k)).ok() || !(s = sc.sy.ensure(sizeof(double) * p * m)).ok())
+      return s;
+    // per-fold training rows (complement_rows, partition.hpp:71-83): host index bookkeeping
+    std::vector<std::vector<int64_t>> t_rows(p);
+    for (int32_t f = 0; f < p; ++f) t_rows[f].reserve(n - counts[f]);
+    for (int64_t i = 0; i < n; ++i)
+      for (int32_t f = 0; f < p; ++f)
+        if (labels[i] != f + 1) t_rows[f].push_back(i);
+    cvg::DevBuf mean_buf;
+    for (int32_t f = 0; f < p; ++f) {
+      s = baseline_rows(ctx, dtype, sc.x.as<void>(), sc.y.as<void>(), k, m, t_rows[f], cfg_masks, n_cfg,
+                        sc.xtx.as<double>() + (size_t)f * k * k, (int64_t)p * k * k,
+                        sc.xty.as<double>() + (size_t)f * k * m, (int64_t)p * k * m, sc.mx.as<double>() + f * k,
+                        sc.my.as<double>() + f * m, sc.sx.as<double>() + f * k, sc.sy.as<double>() + f * m, mean_buf);
+      if (!s.ok()) return s;
+    }
+    if (!(s = d2h(xtx, sc.xtx.as<void>(), sizeof(double) * nxx, st)).ok()) return s;
+    if (!(s = d2h(xty, sc.xty.as<void>(), sizeof(double) * nxy, st)).ok()) return s;
+    for (int32_t c = 0; c < n_cfg; ++c) {
+      const uint32_t cf = cfg_masks[c];
+      if (cf) {
+        if (mean_x && !(s = d2h(mean_x + (size_t)c * p * k, sc.mx.as<void>(), sizeof(double) * p * k, st)).ok()) return s;
+        if (mean_y && !(s = d2h(mean_y + (size_t)c * p * m, sc.my.as<void>(), sizeof(double) * p * m, st)).ok()) return s;
+      }
+      if ((cf & CVG_SCALE_X) && std_x &&
+          !(s = d2h(std_x + (size_t)c * p * k, sc.sx.as<void>(), sizeof(double) * p * k, st)).ok())
+        return s;
+      if ((cf & CVG_SCALE_Y) && std_y &&
+          !(s = d2h(std_y + (size_t)c * p * m, sc.sy.as<void>(), sizeof(double) * p * m, st)).ok())
+        return s;
+    }
+    if (!(s = cvg::cuda_status(cudaStreamSynchronize(st), "stream synchronize")).ok()) return s;
+    for (int32_t f = 0; f < p; ++f) {
+      if (n_train) n_train[f] = n - counts[f];
+      if (n_val) n_val[f] = counts[f];
+    }
+    return Status::Ok();
+  });
+}
+
+int cvg_baseline_single_fold(cvg_context* ctx, int dtype, const void* x, const void* y, int64_t n, int64_t k,
+                             int64_t m, const int64_t* v_rows, int64_t n_val, uint32_t cfg, double* xtx_t,
+                             double* xty_t, double* mean_x_t, double* mean_y_t, double* std_x_t, double* std_y_t,
+                             int64_t* n_train, char* err, size_t errlen) {
+  return guarded(err, errlen, [&]() -> Status {
+    if (!ctx) return Status::Err(CVG_E_INVALID_ARG, "null context");
+    if (cfg > 15u) return Status::Err(CVG_E_INVALID_ARG, "configuration mask outside 0..15");
+    for (int64_t i = 0; i < n_val; ++i)
+      if (v_rows[i] < 0 || v_rows[i] >= n || (i && v_rows[i] <= v_rows[i - 1]))
+        return Status::Err(CVG_E_INVALID_ARG, "v_rows must be ascending row indices in [0, n)");
+    std::vector<int64_t> t_rows;  // complement_rows, partition.hpp:71-83
+    for (int64_t i = 0, next = 0; i < n; ++i) {
+      if (next < n_val && v_rows[next] == i)
+        ++next;
+      else
+        t_rows.push_back(i);
+    }
+    // baseline.hpp:47-50
+    if (n_val == 0 || t_rows.empty())
+      return Status::Err(CVG_E_PARTITION, "a fold needs both validation and training rows");
+    if ((cfg & (CVG_SCALE_X | CVG_SCALE_Y)) && t_rows.size() < 2)
+      return Status::Err(CVG_E_SCALABILITY, "scaling needs at least 2 training rows");
+    Status s = cvg::cuda_status(cudaSetDevice(ctx->device), "cudaSetDevice");
+    if (!s.ok()) return s;
+    const size_t e = elt(dtype);
+    cvg::DevBuf dx, dy, oxx, oxy, ost, mean_buf;
+    if (!(s = dx.ensure(e * n * k)).ok() || !(s = dy.ensure(e * n * m)).ok() ||
+        !(s = oxx.ensure(sizeof(double) * k * k)).ok() || !(s = oxy.ensure(sizeof(double) * k * m)).ok() ||
+        !(s = ost.ensure(sizeof(double) * 2 * (k + m))).ok())
+      return s;
+    cudaStream_t st = ctx->stream;
+    if (!(s = cvg::cuda_status(cudaMemcpyAsync(dx.as<void>(), x, e * n * k, cudaMemcpyHostToDevice, st), "H2D x"))
+             .ok() ||
+        !(s = cvg::cuda_status(cudaMemcpyAsync(dy.as<void>(), y, e * n * m, cudaMemcpyHostToDevice, st), "H2D y"))
+             .ok())
+      return s;
+    double* stv = ost.as<double>();
+    const int64_t w = k + m;
+    if (!(s = baseline_rows(ctx, dtype, dx.as<void>(), dy.as<void>(), k, m, t_rows, &cfg, 1, oxx.as<double>(), 0,
+                            oxy.as<double>(), 0, stv, stv + k, stv + w, stv + w + k, mean_buf))
+             .ok())
+      return s;
+    if (!(s = d2h(xtx_t, oxx.as<void>(), sizeof(double) * k * k, st)).ok()) return s;
+    if (!(s = d2h(xty_t, oxy.as<void>(), sizeof(double) * k * m, st)).ok()) return s;
+    if (cfg & 15u) {
+      if (!(s = d2h(mean_x_t, stv, sizeof(double) * k, st)).ok()) return s;
+      if (!(s = d2h(mean_y_t, stv + k, sizeof(double) * m, st)).ok()) return s;
+    }
+    if ((cfg & CVG_SCALE_X) && !(s = d2h(std_x_t, stv + w, sizeof(double) * k, st)).ok()) return s;
+    if ((cfg & CVG_SCALE_Y) && !(s = d2h(std_y_t, stv + w + k, sizeof(double) * m, st)).ok()) return s;
+    if (n_train) *n_train = (int64_t)t_rows.size();
+    return cvg::cuda_status(cudaStreamSynchronize(st), "stream synchronize");
   });
 }
 

@@ -529,4 +529,51 @@ Status Plan::finish(const double* d_rank_partials, int32_t n_ranks, const double
   return Status::Ok();
 }
 
+Status Plan::finish_direct(const uint32_t* cfgs, int32_t ncfg, double* d_xtx, double* d_xty, double* d_mean_x,
+                           double* d_mean_y, double* d_std_x, double* d_std_y) {
+  if (!grammed_ || p_ != 1) return Status::Err(4, "finish_direct needs a grammed single-fold plan");
+  cudaStream_t s = ctx_->stream;
+  CVG_TRY(zero_g_.ensure(sizeof(double) * kp_ * kp_));
+  CVG_TRY(zero_nval_.ensure(sizeof(int64_t)));
+  CVG_TRY(zero_ptr_.ensure(sizeof(void*)));
+  CVG_CK(cudaMemsetAsync(zero_g_.as<void>(), 0, sizeof(double) * kp_ * kp_, s));
+  CVG_CK(cudaMemsetAsync(zero_nval_.as<void>(), 0, sizeof(int64_t), s));
+  const double* zp = zero_g_.as<double>();
+  CVG_CK(cudaMemcpyAsync(zero_ptr_.as<void>(), &zp, sizeof(void*), cudaMemcpyHostToDevice, s));
+  const int64_t n_saved = n_;
+  n_ = counts_[0];  // the training set is exactly the bound rows
+  CVG_TRY(st_mz_.ensure(sizeof(double) * w_));
+  CVG_TRY(st_sT_.ensure(sizeof(double) * w_));
+  CVG_TRY(st_sd_.ensure(sizeof(double) * w_));
+  FoldStatsDev st{st_mz_.as<double>(), st_sT_.as<double>(), st_sd_.as<double>()};
+  {
+    Timed t(ctx_, kStats);
+    launch_fold_stats(local_.as<double>(), zero_ptr_.as<const double*>(), zero_nval_.as<int64_t>(), 1, n_, k_, m_,
+                      kp_, shift_.as<double>(), st, d_mean_x, d_mean_y, d_std_x, d_std_y, flag_.as<int>(), s);
+  }
+  Status rc = count_launch();
+  if (rc.ok() && ncfg > 0) {
+    rc = cfg_d_.ensure(sizeof(uint32_t) * ncfg);
+    if (rc.ok()) rc = cuda_status(cudaMemcpyAsync(cfg_d_.as<void>(), cfgs, sizeof(uint32_t) * ncfg,
+                                                  cudaMemcpyHostToDevice, s), "H2D cfgs");
+    if (rc.ok()) {
+      {
+        Timed t(ctx_, kProducts);
+        launch_products(local_.as<double>(), zero_ptr_.as<const double*>(), zero_nval_.as<int64_t>(), 1, n_, k_, m_,
+                        kp_, shift_.as<double>(), st, out_tiles_d_.as<int2>(), (int)out_tiles_.size(),
+                        cfg_d_.as<uint32_t>(), ncfg, d_xtx, d_xty, s);
+      }
+      rc = count_launch();
+    }
+  }
+  n_ = n_saved;
+  CVG_TRY(rc);
+  return cuda_status(cudaStreamSynchronize(s), "stream synchronize");
+}
+
+Status Plan::direct_means(double* d_mean) {
+  // mean = shift + column sums / count (the stats kernel's mean outputs, [x | y]).
+  return finish_direct(nullptr, 0, nullptr, nullptr, d_mean, d_mean + k_, nullptr, nullptr);
+}
+
 }  // namespace cvg

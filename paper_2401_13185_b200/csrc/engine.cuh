@@ -74,6 +74,12 @@ class Plan {
                 const uint32_t* cfgs, int32_t ncfg, double* d_xtx, double* d_xty, double* d_mean_x,
                 double* d_mean_y, double* d_std_x, double* d_std_y);
 
+  // Baseline (direct) epilogue for a bind_rows plan: the bound rows ARE the
+  // training set (no downdate): total = their Gram, fold Gram = 0, n_val = 0.
+  Status finish_direct(const uint32_t* cfgs, int32_t ncfg, double* d_xtx, double* d_xty, double* d_mean_x,
+                       double* d_mean_y, double* d_std_x, double* d_std_y);
+  // Training means of the bound rows (shift + column sums / count), on the device.
+  Status direct_means(double* d_mean);
   const double* local() const { return local_.as<double>(); }
   const double* shift() const { return shift_.as<double>(); }
   int64_t kp() const { return kp_; }
@@ -115,6 +121,7 @@ class Plan {
   int64_t seg_lo_ = -1, seg_hi_ = -1;   // shared fold: owned segment range (else -1)
   int32_t group_lo_ = 0, group_hi_ = 0; // ranks sharing the fold
   TreeProgram group_tree_;
+  DevBuf zero_g_, zero_nval_, zero_ptr_;
 
   DevBuf tiles_d_, out_tiles_d_, tiles128_d_, zt_hi_, zt_lo_, tile_counts_, fold_counts_, bad_, zbase_d_, src_row_, z_, part_, foldbuf_, local_,
       total_, shift_, flag_, segs_d_, foldptr_d_, nval_d_, st_mz_, st_sT_, st_sd_, cfg_d_;

@@ -499,3 +499,187 @@ def random_partitioning(n: int, p: int, rng) -> Partitioning:
     labels = np.empty(n, np.int32)
     L.lib().cvg_random_partitioning(rng.handle, n, p, _ptr(labels))
     return Partitioning(labels, p)
+
+
+# ---------------------------------------------------------------- baseline.hpp
+def baseline_fold_products_configs(data: DatasetPair, part: Partitioning, cfgs, ctx: Optional[Context] = None):
+    """The baseline engine (baseline.hpp:79-97) on the device for several
+    configurations: per fold, the training rows are contracted directly in
+    their own mean-centered basis — no downdate.  Θ(P·N·K(K+M))."""
+    cfgs = [_cfg(c) for c in cfgs]
+    ctx = ctx or get_context()
+    if part.n_rows() != data.n_rows():
+        raise DimensionError("partitioning length does not match sample count")
+    n, k, m, p = data.n_rows(), data.n_features(), data.n_responses(), part.p
+    nc, pp = len(cfgs), max(p, 0)
+    masks = np.array([c.mask for c in cfgs], np.uint32)
+    xtx, xty = np.empty((nc, pp, k, k)), np.empty((nc, pp, k, m))
+    mx, my, sx, sy = np.empty((nc, pp, k)), np.empty((nc, pp, m)), np.empty((nc, pp, k)), np.empty((nc, pp, m))
+    nt, nv = np.empty(pp, np.int64), np.empty(pp, np.int64)
+    buf = L.err_buf()
+    _check(L.lib().cvg_baseline_fold_products(ctx.handle, data.dtype_code, _ptr(data.x()), _ptr(data.y()), n, k, m,
+                                              _ptr(part.labels), part.labels.size, p, _ptr(masks), nc, _ptr(xtx),
+                                              _ptr(xty), _ptr(mx), _ptr(my), _ptr(sx), _ptr(sy), _ptr(nt), _ptr(nv),
+                                              buf, len(buf)), buf)
+    out = []
+    for ci, cfg in enumerate(cfgs):
+        runs = []
+        for f in range(p):
+            st = FoldStats(n_train=int(nt[f]), n_val=int(nv[f]))
+            if cfg.any():
+                st.mean_x_t, st.mean_y_t = mx[ci, f], my[ci, f]
+            if cfg.scale_x:
+                st.std_x_t = sx[ci, f]
+            if cfg.scale_y:
+                st.std_y_t = sy[ci, f]
+            runs.append(FoldResult(f + 1, xtx[ci, f], xty[ci, f], st))
+        out.append(runs)
+    return out
+
+
+def baseline_fold_products(data: DatasetPair, part: Partitioning, cfg=None, n_threads: int = 1,
+                           ctx: Optional[Context] = None) -> List[FoldResult]:
+    """baseline.hpp:79-97 (n_threads accepted for signature parity)."""
+    return baseline_fold_products_configs(data, part, [_cfg(cfg)], ctx)[0]
+
+
+def baseline_single_fold(data: DatasetPair, v_rows: Sequence[int], cfg=None, fold_id: int = 0,
+                         ctx: Optional[Context] = None) -> FoldResult:
+    """baseline.hpp:42-76."""
+    cfg = _cfg(cfg)
+    ctx = ctx or get_context()
+    k, m = data.n_features(), data.n_responses()
+    v = np.ascontiguousarray(v_rows, np.int64)
+    xtx, xty = np.empty((k, k)), np.empty((k, m))
+    mx, my, sx, sy = np.empty(k), np.empty(m), np.empty(k), np.empty(m)
+    nt = ctypes.c_int64(0)
+    buf = L.err_buf()
+    _check(L.lib().cvg_baseline_single_fold(ctx.handle, data.dtype_code, _ptr(data.x()), _ptr(data.y()),
+                                            data.n_rows(), k, m, _ptr(v), v.size, cfg.mask, _ptr(xtx), _ptr(xty),
+                                            _ptr(mx), _ptr(my), _ptr(sx), _ptr(sy), ctypes.addressof(nt), buf,
+                                            len(buf)), buf)
+    stats = FoldStats(n_train=int(nt.value), n_val=int(v.size))
+    if cfg.any():
+        stats.mean_x_t, stats.mean_y_t = mx, my
+    if cfg.scale_x:
+        stats.std_x_t = sx
+    if cfg.scale_y:
+        stats.std_y_t = sy
+    return FoldResult(fold_id, xtx, xty, stats)
+
+
+# ------------------------------------------------------------------ combos.hpp
+@dataclass
+class ComboClassReport:
+    """combos.hpp:21-31."""
+
+    configs: List[PreprocessConfig]
+    xty_class: List[int]
+    pair_class: List[int]
+    n_xty_classes: int
+    n_pair_classes: int
+    min_xty_separation: float
+    min_pair_separation: float
+    tol: float
+    degenerate: bool
+
+
+def _group_classes(runs, tol, dist):
+    """combos.hpp:69-94: first-fit grouping in canonical order."""
+    reps, cls, min_sep = [], [], float("inf")
+    for c in range(16):
+        assigned = -1
+        for kidx, rep in enumerate(reps):
+            d = dist(runs[c], runs[rep])
+            if d <= tol and assigned < 0:
+                assigned = kidx
+            elif d > tol:
+                min_sep = min(min_sep, d)
+        if assigned < 0:
+            assigned = len(reps)
+            reps.append(c)
+        cls.append(assigned)
+    if len(reps) <= 1:
+        min_sep = 0.0
+    return len(reps), cls, min_sep
+
+
+def classify_combos(data: DatasetPair, part: Partitioning, tol: float = 1e-9,
+                    ctx: Optional[Context] = None) -> ComboClassReport:
+    """Certify the 8 XᵀY / 12 (XᵀX, XᵀY) configuration classes (combos.hpp:98-120)
+    over the engine's outputs; all 16 configurations come from one Gram pass."""
+    err = check_scalable(part)
+    if err:
+        raise ScalabilityError(err)
+    configs = enumerate_configs()
+    runs = run_all_folds_configs(data, part, configs, ctx)
+
+    def d_xty(a, b):
+        return max(rel_frobenius_dist(x.xty_t, y.xty_t) for x, y in zip(a, b))
+
+    def d_pair(a, b):
+        return max(d_xty(a, b), max(rel_frobenius_dist(x.xtx_t, y.xtx_t) for x, y in zip(a, b)))
+
+    nx, cx, sx = _group_classes(runs, tol, d_xty)
+    np_, cp, sp = _group_classes(runs, tol, d_pair)
+    return ComboClassReport(configs, cx, cp, nx, np_, sx, sp, tol, nx != 8 or np_ != 12)
+
+
+def format_combo_table(report: ComboClassReport) -> str:
+    """combos.hpp:124-161 (same text layout)."""
+    centers = ["no centering", "center X", "center Y", "center both"]
+    scales = ["no scaling", "scale X", "scale Y", "scale both"]
+
+    def idx(ci, si):
+        cx = 1 if ci in (1, 3) else 0
+        cy = 1 if ci in (2, 3) else 0
+        sx = 1 if si in (1, 3) else 0
+        sy = 1 if si in (2, 3) else 0
+        return (cx << 3) | (cy << 2) | (sx << 1) | sy
+
+    lines = []
+
+    def grid(title, cls):
+        lines.append(title)
+        lines.append("centering \\ scaling" + "".join("\t" + s for s in scales))
+        for ci in range(4):
+            lines.append(centers[ci] + "".join("\t" + str(cls[idx(ci, si)]) for si in range(4)))
+
+    grid("XtY classes", report.xty_class)
+    lines.append("")
+    grid("(XtX, XtY) pair classes", report.pair_class)
+    g = lambda v: "%g" % v  # noqa: E731  (std::ostream default formatting)
+    text = "\n".join(lines) + "\n"
+    text += (f"\ndistinct XtY classes: {report.n_xty_classes}\ndistinct pair classes: {report.n_pair_classes}"
+             f"\nmin inter-class separation (xty): {g(report.min_xty_separation)}"
+             f"\nmin inter-class separation (pair): {g(report.min_pair_separation)}\ntolerance: {g(report.tol)}\n")
+    if report.degenerate:
+        text += "warning: class counts are degenerate for this input; expected 8 xty and 12 pair classes\n"
+    return text
+
+
+# ---------------------------------------------------------------------- io.hpp
+def format_double(v: float) -> str:
+    """%.17g, the reference's round-trip format (io.hpp:24-28)."""
+    return "%.17g" % v
+
+
+def config_to_string(cfg) -> str:
+    """4-bit token cx cy sx sy (io.hpp:115-122)."""
+    c = _cfg(cfg)
+    return "".join("1" if b else "0" for b in (c.center_x, c.center_y, c.scale_x, c.scale_y))
+
+
+def parse_config(s: str) -> PreprocessConfig:
+    """io.hpp:126-149."""
+    if s == "none":
+        return PreprocessConfig()
+    if s == "center":
+        return PreprocessConfig(True, True, False, False)
+    if s == "scale":
+        return PreprocessConfig(False, False, True, True)
+    if s in ("center+scale", "center_scale"):
+        return PreprocessConfig(True, True, True, True)
+    if len(s) == 4 and set(s) <= {"0", "1"}:
+        return PreprocessConfig(*(ch == "1" for ch in s))
+    raise IOError(f"unknown preprocessing config '{s}'")

@@ -60,6 +60,12 @@ class OracleEngine:
     def run_all_folds_configs(self, x, y, labels, p, cfgs):
         return [self.run_all_folds(x, y, labels, p, c) for c in cfgs]
 
+    def baseline_all_folds(self, x, y, labels, p, cfg):
+        return [_flat(r) for r in self._call(self.o.baseline_all_folds, x, y, labels, p, cfg)]
+
+    def baseline_single_fold(self, x, y, v_rows, cfg, fold_id=0):
+        return _flat(self._call(self.o.baseline_single_fold, x, y, v_rows, cfg, fold_id))
+
     def training_mean(self, g, v, n, n_val):
         return self._call(self.o.training_mean, g, v, n, n_val)
 
@@ -86,6 +92,12 @@ class GpuEngine:
     def run_all_folds_configs(self, x, y, labels, p, cfgs):
         runs = cv.run_all_folds_configs(cv.DatasetPair(x, y), cv.Partitioning(labels, p), cfgs)
         return [[_flat(r) for r in run] for run in runs]
+
+    def baseline_all_folds(self, x, y, labels, p, cfg):
+        return [_flat(r) for r in cv.baseline_fold_products(cv.DatasetPair(x, y), cv.Partitioning(labels, p), cfg)]
+
+    def baseline_single_fold(self, x, y, v_rows, cfg, fold_id=0):
+        return _flat(cv.baseline_single_fold(cv.DatasetPair(x, y), v_rows, cfg, fold_id))
 
     def training_mean(self, g, v, n, n_val):
         return cv.training_mean(g, v, n, n_val)

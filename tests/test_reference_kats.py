@@ -176,33 +176,35 @@ def test_thread_count_does_not_change_a_bit(engine):  # test_fast.cpp:217-229
         assert s.xtx_t.tobytes() == p.xtx_t.tobytes() and s.xty_t.tobytes() == p.xty_t.tobytes()
 
 
-def test_baseline_micro_case(engine):  # test_baseline.cpp:23-53, acceptance.cpp:86-116
+def test_baseline_micro_case(engine):  # test_baseline.cpp:23-53, acceptance.cpp:86-116 (both engines)
     x, y = micro()
     b = KATS["baseline_micro"]
     labels = np.array(b["labels"], np.int32)
-    for c in b["fold2"]:
-        res = engine.run_all_folds(x, y, labels, b["p"], c["cfg"])
-        assert res[1].fold_id == 2
-        assert abs(res[1].xtx_t[0, 0] - c["xtx"]) <= 1e-12 and abs(res[1].xty_t[0, 0] - c["xty"]) <= 1e-12
-    with pytest.raises(ERR_BY_NAME[b["all_on_full_run_error"]]):
-        engine.run_all_folds(x, y, labels, b["p"], 15)
+    for run in (engine.run_all_folds, engine.baseline_all_folds):
+        for c in b["fold2"]:
+            res = run(x, y, labels, b["p"], c["cfg"])
+            assert res[1].fold_id == 2
+            assert abs(res[1].xtx_t[0, 0] - c["xtx"]) <= 1e-12 and abs(res[1].xty_t[0, 0] - c["xty"]) <= 1e-12
+        with pytest.raises(ERR_BY_NAME[b["all_on_full_run_error"]]):
+            run(x, y, labels, b["p"], 15)
     s = b["all_on_single_fold"]
-    r = engine.fold_products(engine.precompute_global(x, y, s["cfg"]), x, y, s["v_rows"], s["cfg"], 2)
-    assert abs(r.xtx_t[0, 0] - s["xtx"]) <= 1e-12 and abs(r.xty_t[0, 0] - s["xty"]) <= 1e-12
-    assert abs(r.std_x_t[0] - s["std_x"]) <= 1e-15 and abs(r.std_y_t[0] - s["std_y"]) <= 1e-15
+    for r in (engine.fold_products(engine.precompute_global(x, y, s["cfg"]), x, y, s["v_rows"], s["cfg"], 2),
+              engine.baseline_single_fold(x, y, s["v_rows"], s["cfg"], 2)):
+        assert abs(r.xtx_t[0, 0] - s["xtx"]) <= 1e-12 and abs(r.xty_t[0, 0] - s["xty"]) <= 1e-12
+        assert abs(r.std_x_t[0] - s["std_x"]) <= 1e-15 and abs(r.std_y_t[0] - s["std_y"]) <= 1e-15
 
 
 @pytest.mark.parametrize("key", ["zero_variance", "zero_variance_acceptance"])
 def test_zero_variance_training_column(engine, key):  # test_baseline.cpp:55-66, acceptance.cpp:254-263
     z = KATS[key]
-    res = engine.run_all_folds(np.array(z["x"], float), np.array(z["y"], float), np.array(z["labels"], np.int32),
-                               z["p"], z["cfg"])
-    if key == "zero_variance":
-        assert res[0].std_x_t[0] == z["fold1"]["std_x"]
-        assert abs(res[0].xtx_t[0, 0]) <= z["fold1"]["xtx_margin"]
-    else:
-        for r in res:
-            assert r.std_x_t[0] == z["std_x0"]
+    for run in (engine.run_all_folds, engine.baseline_all_folds):
+        res = run(np.array(z["x"], float), np.array(z["y"], float), np.array(z["labels"], np.int32), z["p"], z["cfg"])
+        if key == "zero_variance":
+            assert res[0].std_x_t[0] == z["fold1"]["std_x"]
+            assert abs(res[0].xtx_t[0, 0]) <= z["fold1"]["xtx_margin"]
+        else:
+            for r in res:
+                assert r.std_x_t[0] == z["std_x0"]
 
 
 def test_raw_fold_plus_validation_is_total(engine):  # test_baseline.cpp:68-81
@@ -210,7 +212,7 @@ def test_raw_fold_plus_validation_is_total(engine):  # test_baseline.cpp:68-81
     data = cv.random_dataset(35, 4, 2, rng)
     part = cv.random_partitioning(35, 6, rng)
     x = data.x()
-    res = engine.run_all_folds(x, data.y(), part.labels, 6, 0)
+    res = engine.baseline_all_folds(x, data.y(), part.labels, 6, 0)
     idx = cv.build_validation_partitions(part)
     for r, rows in zip(res, idx.sets):
         xv = x[rows]
@@ -222,7 +224,7 @@ def test_xtx_symmetric_every_config(engine):  # test_baseline.cpp:83-93
     data = cv.random_dataset(25, 5, 2, rng)
     part = cv.random_partitioning(25, 4, rng)
     for bits in range(16):
-        for r in engine.run_all_folds(data.x(), data.y(), part.labels, 4, bits):
+        for r in engine.baseline_all_folds(data.x(), data.y(), part.labels, 4, bits):
             assert np.abs(r.xtx_t - r.xtx_t.T).max() <= 1e-12
 
 
@@ -247,7 +249,7 @@ def test_preprocessed_training_has_mean0_std1(engine):  # test_baseline.cpp:114-
     rng = cv.MT19937_64(6)
     data = cv.random_dataset(30, 4, 2, rng)
     part = cv.random_partitioning(30, 3, rng)
-    res = engine.run_all_folds(data.x(), data.y(), part.labels, 3, 15)
+    res = engine.baseline_all_folds(data.x(), data.y(), part.labels, 3, 15)
     idx = cv.build_validation_partitions(part)
     for r, rows in zip(res, idx.sets):
         xt = data.x()[cv.complement_rows(rows, 30)]
@@ -256,16 +258,17 @@ def test_preprocessed_training_has_mean0_std1(engine):  # test_baseline.cpp:114-
         assert np.allclose(z.std(axis=0, ddof=1), 1.0, atol=1e-10, rtol=0)
 
 
-def test_scaling_non_scalable_rejected(engine):  # test_baseline.cpp:136-148
+def test_scaling_non_scalable_rejected(engine):  # test_baseline.cpp:136-148 (both engines)
     x, y = np.full((2, 1), 2.0), np.ones((2, 1))
-    with pytest.raises(cv.ScalabilityError):
-        engine.run_all_folds(x, y, np.array([1, 2], np.int32), 2, 2)
-    engine.run_all_folds(x, y, np.array([1, 2], np.int32), 2, 0)
     mx, my = micro()
-    with pytest.raises(cv.PartitionError):
-        engine.run_all_folds(mx, my, np.array([1, 1, 3], np.int32), 3, 0)
-    with pytest.raises(cv.DimensionError):
-        engine.run_all_folds(mx, my, np.array([1, 2], np.int32), 2, 0)
+    for run in (engine.run_all_folds, engine.baseline_all_folds):
+        with pytest.raises(cv.ScalabilityError):
+            run(x, y, np.array([1, 2], np.int32), 2, 2)
+        run(x, y, np.array([1, 2], np.int32), 2, 0)
+        with pytest.raises(cv.PartitionError):
+            run(mx, my, np.array([1, 1, 3], np.int32), 3, 0)
+        with pytest.raises(cv.DimensionError):
+            run(mx, my, np.array([1, 2], np.int32), 2, 0)
 
 
 def test_hadamard_outer_divide(engine):  # test_core.cpp:9-67
