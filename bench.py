@@ -245,6 +245,8 @@ def run_ours(args):
         dist.all_reduce(kt, op=dist.ReduceOp.MAX)
         kms = kt.cpu().numpy()
     value = flops / (ms * 1e-3) / 1e9
+    input_gb = (x.numel() * x.element_size() + y.numel() * y.element_size()) / 1e9
+    x_elt = x.element_size()
 
     # ---- e2e through the reference-facing C ABI with pinned host buffers (N=1)
     e2e = None
@@ -327,7 +329,7 @@ def run_ours(args):
     pk = peaks()
     hbm = pk.get("hbm_gbs", 6554.2)
     tile = 128 if f32 else 64
-    reorder_bytes = n * (k + m) * x.element_size() + (n + 32 * p) * (-(-(k + m + 1) // tile) * tile) * (8 if f32 else 8)
+    reorder_bytes = n * (k + m) * x_elt + (n + 32 * p) * (-(-(k + m + 1) // tile) * tile) * 8
     epi_bytes = len(masks) * (2 * p * k * (k + m) * 8) + k * (k + m) * 8
     line = {
         "metric": "all_fold_cv_gram_gflops", "value": round(value, 3), "unit": "GFLOP/s", "n_gpus": world,
@@ -337,7 +339,7 @@ def run_ours(args):
         "config": {"workload": f"configs[{cid}] N={n} K={k} M={m} P={p} cfg masks {masks} "
                                f"({workloads.DESCRIPTIONS[cid]})", "global_batch": n,
                    "parallelism": f"folds/{world} ranks",
-                   "l2": f"inputs {x.numel() * x.element_size() / 1e9:.1f} GB > 126 MB L2: no flush needed",
+                   "l2": f"inputs {input_gb:.1f} GB > 126 MB L2: no flush needed",
                    "seed": workloads.SEEDS[cid]},
         "roofline": {"bound": "tensor", "kernel": gram_kernel, "achieved": round(achieved, 3),
                      "peak": peak, "unit": "TFLOP/s", "frac": round(achieved / peak, 4),

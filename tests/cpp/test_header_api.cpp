@@ -291,9 +291,28 @@ void zero_variance_column() {  // 55-66
   y << 1, 2, 3, 4;
   PreprocessConfig cfg;
   cfg.center_x = cfg.scale_x = true;
-  const auto results = run_all_folds(DatasetPair(x, y), {{1, 1, 2, 2}, 2}, cfg);
-  CHECK(results[0].stats.std_x_t(0) == 1.0);
-  CHECK(std::abs(results[0].xtx_t(0, 0)) <= 1e-15);
+  for (const auto& results : {run_all_folds(DatasetPair(x, y), {{1, 1, 2, 2}, 2}, cfg),
+                              baseline_fold_products(DatasetPair(x, y), {{1, 1, 2, 2}, 2}, cfg)}) {
+    CHECK(results[0].stats.std_x_t(0) == 1.0);
+    CHECK(std::abs(results[0].xtx_t(0, 0)) <= 1e-15);
+  }
+}
+
+void device_baseline_micro_and_errors() {  // test_baseline.cpp:23-53, 136-148
+  const auto data = micro_case();
+  const Partitioning micro_part{{1, 1, 2}, 2};
+  auto r0 = baseline_fold_products(data, micro_part, {});
+  CHECK(r0.size() == 2 && r0[1].fold_id == 2);
+  CHECK(near(r0[1].xtx_t(0, 0), 10.0, 1e-12) && near(r0[1].xty_t(0, 0), 14.0, 1e-12));
+  PreprocessConfig cc{true, true, false, false};
+  auto r1 = baseline_fold_products(data, micro_part, cc);
+  CHECK(near(r1[1].xtx_t(0, 0), 2.0, 1e-12) && near(r1[1].xty_t(0, 0), 2.0, 1e-12));
+  CHECK_THROWS_AS(baseline_fold_products(data, micro_part, kAllOn), scalability_error);
+  const auto r = baseline_single_fold(data, {2}, kAllOn, 2);
+  CHECK(near(r.xtx_t(0, 0), 1.0, 1e-12) && near(r.xty_t(0, 0), 1.0, 1e-12));
+  CHECK(near(r.stats.std_x_t(0), std::sqrt(2.0), 1e-15) && near(r.stats.std_y_t(0), std::sqrt(2.0), 1e-15));
+  CHECK_THROWS_AS(baseline_fold_products(data, {{1, 1, 3}, 3}, {}), partition_error);
+  CHECK_THROWS_AS(baseline_fold_products(data, {{1, 2}, 2}, {}), dimension_error);
 }
 
 void errors_like_the_reference() {  // 136-148
@@ -373,6 +392,7 @@ int main(int argc, char** argv) {
       {"thread_count_invariance", thread_count_invariance, true},
       {"hadamard_values", hadamard_values, true},
       {"zero_variance_column", zero_variance_column, true},
+      {"device_baseline_micro_and_errors", device_baseline_micro_and_errors, true},
       {"errors_like_the_reference", errors_like_the_reference, true},
       {"acceptance_c1", acceptance_c1, true},
   };
