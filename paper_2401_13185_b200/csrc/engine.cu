@@ -8,6 +8,7 @@
 // Gram -> K4 fold/total sums -> [cross-rank combine] -> K5 stats + products.
 #include <algorithm>
 #include <climits>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -141,6 +142,19 @@ Status TreeProgram::run(cvg_context* ctx, const int2* tiles, int ntiles, int64_t
     CVG_CK(cudaGetLastError());
   }
   return Status::Ok();
+}
+
+// Rows per segment: a fixed constant per dtype (never a function of the GPU
+// count, so sums stay bit-identical across world sizes).  CVG_CHUNK_ROWS
+// overrides it for tuning experiments (multiple of kRowStep).
+int64_t Plan::chunk_rows() const {
+  static const int64_t env = [] {
+    const char* v = std::getenv("CVG_CHUNK_ROWS");
+    const long long r = v ? std::atoll(v) : 0;
+    return (int64_t)(r > 0 ? round_up(r, kRowStep) : 0);
+  }();
+  if (env > 0) return env;
+  return dtype_ == 1 ? kChunkRowsF32 : kChunkRows;
 }
 
 Status Plan::count_launch(int n) {
@@ -442,8 +456,8 @@ Status Plan::gram(const void* d_x, int64_t ldx, const void* d_y, int64_t ldy, co
     }
   } else {
     // fp64: K1 builds the fold-bucketed, shifted copy Z.  (Gathering X rows
-    // straight into the Gram's shared-memory stages was measured slower: random
-    // 512-byte row chunks over the whole matrix are latency-bound — DESIGN.md §4.)
+    // straight into the Gram's shared-memory stages, or overlapping K1 with K2
+    // inside one persistent launch, were both measured slower — DESIGN.md §8.)
     if (zrows_ > 0) {
       {
         Timed t(ctx_, kReorder);

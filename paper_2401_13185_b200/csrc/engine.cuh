@@ -103,7 +103,7 @@ class Plan {
   Status plan_segments();
   Status count_launch(int n = 1);
   void assign_rank();  // rank mode: fb_/fe_, segment window, fold group
-  int64_t chunk_rows() const { return dtype_ == 1 ? kChunkRowsF32 : kChunkRows; }
+  int64_t chunk_rows() const;
 
   cvg_context* ctx_ = nullptr;
   int dtype_ = 0;
