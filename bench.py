@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--config", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-path", choices=["auto", "capi", "sharded"], default="auto",
+                    help="auto: the C ABI call at N=1, the row-sharded host entry at N>1")
     return ap.parse_args()
 
 
@@ -193,7 +195,7 @@ def run_ours(args):
     plan = P.DevicePlan(n, k, m, p, dtype="f32" if x.dtype == torch.float32 else "f64", ctx=ctx, rank=rank,
                         world=world)
     stream = torch.cuda.current_stream(dev)
-    ctx.set_stream(stream.cuda_stream)
+    ctx.use_torch_stream(stream)
 
     # row 0 of the full data is every rank's shift
     shift = torch.cat([x[0], y[0]]).double().cpu().numpy()
@@ -250,7 +252,8 @@ def run_ours(args):
 
     # ---- e2e through the reference-facing C ABI with pinned host buffers (N=1)
     e2e = None
-    if not args.no_e2e and world == 1:
+    sharded_e2e = args.e2e_path == "sharded" or (args.e2e_path == "auto" and world > 1)
+    if not args.no_e2e and not sharded_e2e:
         hx = torch.empty(x.shape, dtype=x.dtype, pin_memory=True)
         hy = torch.empty(y.shape, dtype=y.dtype, pin_memory=True)
         hl = torch.empty(labels.shape, dtype=torch.int32, pin_memory=True)
@@ -293,6 +296,53 @@ def run_ours(args):
         e2e = {"value": round(flops / (e2e_ms * 1e-3) / 1e9, 3), "unit": "GFLOP/s", "ms_per_step": round(e2e_ms, 3),
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                "path": "cvg_run_all_folds (C ABI) from pinned host buffers, wall clock around the synchronous call"}
+
+    elif not args.no_e2e:
+        # N GPUs from HOST memory: each rank holds its row shard (pinned) and all labels,
+        # copies the shard over its own PCIe link, shards are all-gathered over NVLink,
+        # then the same fold-range run; the owned folds' outputs come back to host.
+        lo, hi = P.shard_rows(n, rank, world)
+        hx = torch.empty((hi - lo, k), dtype=x.dtype, pin_memory=True)
+        hy = torch.empty((hi - lo, m), dtype=y.dtype, pin_memory=True)
+        hl = torch.empty(labels.shape, dtype=torch.int32, pin_memory=True)
+        hx.copy_(x[lo:hi])
+        hy.copy_(y[lo:hi])
+        hl.copy_(labels)
+        elt = x.element_size()
+        del x, y
+        plan = None
+        out = mine = gathered = None
+        torch.cuda.empty_cache()
+        e_plan = P.DevicePlan(n, k, m, p, dtype="f32" if elt == 4 else "f64", ctx=ctx, rank=rank, world=world)
+        host_out = None
+
+        def e2e_step():
+            nonlocal host_out
+            _, host_out = P.run_all_folds_sharded(hx, hy, hl, p, masks, n, plan=e_plan, device=dev,
+                                                  out_host=host_out)
+
+        e2e_step()
+        e_steps = max(2, min(args.steps, 5))
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        for _ in range(e_steps):
+            e2e_step()
+        torch.cuda.synchronize(dev)
+        e2e_ms = (time.perf_counter() - t0) * 1e3 / e_steps
+        if world > 1:
+            t = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_ms = float(t.item())
+        nc = len(masks)
+        h2d = n * k * elt + n * m * elt + world * n * 4
+        d2h = nc * (p * k * k * 8 + p * k * m * 8) + p * (2 * k + 2 * m) * 8
+        e2e = {"value": round(flops / (e2e_ms * 1e-3) / 1e9, 3), "unit": "GFLOP/s", "ms_per_step": round(e2e_ms, 3),
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "path": "plan.run_all_folds_sharded: per-rank pinned host row shard -> own PCIe H2D -> NCCL "
+                       "all-gather of rows -> fold-range run -> owned folds D2H; wall clock, max over ranks; "
+                       "bytes are whole-job totals"}
 
     if rank != 0:
         if world > 1:

@@ -51,7 +51,8 @@ int cvg_version(void);
 /* Binds `device` (CUDA ordinal).  Fails with CVG_E_CUDA if it is not sm_100. */
 int cvg_context_create(int device, cvg_context** out, char* err, size_t errlen);
 void cvg_context_destroy(cvg_context* ctx);
-/* Subsequent work is issued on `stream` (a cudaStream_t; NULL = the context's own). */
+/* Subsequent work is issued on `stream` (a cudaStream_t; NULL = the context's
+ * own non-blocking stream; cudaStreamLegacy = the legacy default stream). */
 int cvg_context_set_stream(cvg_context* ctx, void* stream);
 /* Number of kernels this context has launched (for the bench's gpu_launches). */
 int64_t cvg_context_launch_count(const cvg_context* ctx);

@@ -78,12 +78,20 @@ class Context:
         return int(L.lib().cvg_context_launch_count(self._h))
 
     def set_stream(self, stream_ptr: Optional[int]) -> None:
+        """cudaStream_t handle; None = the context's own stream.  A torch stream
+        handle of 0 is the legacy default stream: pass it as cudaStreamLegacy (1),
+        since NULL would select the context's own (non-blocking) stream."""
         L.lib().cvg_context_set_stream(self._h, stream_ptr)
+
+    def use_torch_stream(self, stream) -> None:
+        """Issue subsequent work on a torch.cuda.Stream (ordered after torch's copies)."""
+        self.set_stream(stream.cuda_stream or CUDA_STREAM_LEGACY)
 
     def close(self) -> None:
         self._fin()
 
 
+CUDA_STREAM_LEGACY = 1  # cudaStreamLegacy
 _contexts: dict = {}
 
 

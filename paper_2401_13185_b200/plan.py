@@ -56,7 +56,7 @@ class DevicePlan:
         self.fold_begin = fold_begin
         self.fold_end = p if fold_end is None else fold_end
         self.dtype_code = L.DTYPE_F32 if dtype in ("f32", "float32", torch.float32) else L.DTYPE_F64
-        self.ctx.set_stream(torch.cuda.current_stream(self.ctx.device).cuda_stream)
+        self.ctx.use_torch_stream(torch.cuda.current_stream(self.ctx.device))
         h = ctypes.c_void_p()
         buf = L.err_buf()
         if rank is not None:
@@ -160,6 +160,73 @@ def run_all_folds_device(x, y, labels, p: int, cfgs, group=None, plan=None, shif
     else:
         out = plan.finish(masks)
     return plan, out
+
+
+def shard_rows(n: int, rank: int, world: int):
+    """Rows [lo, hi) of the row-sharded host ingest: blocks of ceil(n / world)
+    rows in rank order (only the last shard is short)."""
+    s = -(-n // world)
+    return min(n, rank * s), min(n, (rank + 1) * s)
+
+
+def run_all_folds_sharded(x_shard, y_shard, labels, p: int, cfgs, n: int, group=None, plan=None,
+                          plan_factory=None, device=None, out_host=None, gather: Optional[bool] = None):
+    """Multi-GPU entry point from HOST memory (the e2e path at N GPUs).
+
+    This rank holds rows ``shard_rows(n, rank, world)`` of x | y in host memory
+    (pinned for full PCIe speed) and all n labels.  Each rank copies only its
+    shard over its own PCIe link, the shards are all-gathered over NVLink
+    (NCCL; list form on gloo) into the full device-resident x | y, and the run
+    continues exactly as ``run_all_folds_device``: canonical fold range, one
+    partial all-gather, the owned folds' epilogue — so outputs are bit-identical
+    to one GPU.  Returns (plan, outputs) with the owned folds' outputs copied to
+    host tensors (``out_host`` reused when given).  ``gather`` forces (or skips)
+    the row all-gather; default: only when world > 1.
+    """
+    import torch
+    import torch.distributed as dist
+
+    distributed = dist.is_available() and dist.is_initialized()
+    world = dist.get_world_size(group) if distributed else 1
+    rank = dist.get_rank(group) if distributed else 0
+    lo, hi = shard_rows(n, rank, world)
+    if x_shard.shape[0] != hi - lo or y_shard.shape[0] != hi - lo:
+        raise ValueError(f"rank {rank} must hold rows [{lo}, {hi}) of x and y")
+    dev = device if device is not None else (torch.device("cuda", torch.cuda.current_device())
+                                             if torch.cuda.is_available() else torch.device("cpu"))
+    k, m = x_shard.shape[1], y_shard.shape[1]
+    s = -(-n // world)
+    mine_x = torch.zeros((s, k), dtype=x_shard.dtype, device=dev)
+    mine_y = torch.zeros((s, m), dtype=y_shard.dtype, device=dev)
+    mine_x[: hi - lo].copy_(x_shard, non_blocking=True)
+    mine_y[: hi - lo].copy_(y_shard, non_blocking=True)
+    d_labels = labels.to(dev, non_blocking=True)
+    if (world > 1) if gather is None else (gather and distributed):
+        if dist.get_backend(group) == "nccl":
+            full_x = torch.empty((world * s, k), dtype=x_shard.dtype, device=dev)
+            full_y = torch.empty((world * s, m), dtype=y_shard.dtype, device=dev)
+            dist.all_gather_into_tensor(full_x, mine_x, group=group)
+            dist.all_gather_into_tensor(full_y, mine_y, group=group)
+        else:
+            px = [torch.empty_like(mine_x) for _ in range(world)]
+            py = [torch.empty_like(mine_y) for _ in range(world)]
+            dist.all_gather(px, mine_x, group=group)
+            dist.all_gather(py, mine_y, group=group)
+            full_x, full_y = torch.cat(px), torch.cat(py)
+        x, y = full_x[:n], full_y[:n]
+    else:
+        x, y = mine_x[:n], mine_y[:n]
+    plan, out = run_all_folds_device(x, y, d_labels, p, cfgs, group=group, plan=plan, plan_factory=plan_factory)
+    if not isinstance(out, dict) or not all(hasattr(v, "to") for v in out.values()):
+        return plan, out  # stand-in plans (CPU tests) return host arrays already
+    if out_host is None:
+        out_host = {kk: torch.empty(v.shape, dtype=v.dtype, pin_memory=torch.cuda.is_available())
+                    for kk, v in out.items()}
+    for kk, v in out.items():
+        out_host[kk].copy_(v, non_blocking=True)
+    if dev.type == "cuda":
+        torch.cuda.current_stream(dev).synchronize()
+    return plan, out_host
 
 
 def exchange_partials(mine, world: int, group=None):

@@ -167,3 +167,49 @@ def test_world1_matches_long_double_oracle(data):
             d = np.sqrt(np.abs(np.diag(truth[f].xtx_t)))
             err = np.abs(xtx[ci, f] - truth[f].xtx_t) / np.maximum(np.abs(truth[f].xtx_t), np.outer(d, d))
             assert err.max() <= 1e-10
+
+
+def _worker_sharded(rank, world, port, outdir, data):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2401_13185_b200 import plan as P
+
+    x, y, labels, p = data
+    lo, hi = P.shard_rows(len(x), rank, world)
+    pl, out = P.run_all_folds_sharded(torch.from_numpy(x[lo:hi]), torch.from_numpy(y[lo:hi]),
+                                      torch.from_numpy(labels), p, [8, 0], n=len(x), plan_factory=NumpyPlan,
+                                      device=torch.device("cpu"))
+    np.savez(os.path.join(outdir, f"rank{rank}.npz"), fb=pl.fold_begin, fe=pl.fold_end,
+             xtx=np.stack(out["xtx"]), xty=np.stack(out["xty"]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3, 4])
+def test_row_sharded_host_ingest_matches_world1_bitwise(world, data):
+    """run_all_folds_sharded: each rank holds only rows shard_rows(n, r, G) on
+    the host; shards are all-gathered (gloo list form here, NCCL on GPUs) and
+    the fold-range run proceeds as usual: same folds, same bits as one rank
+    (world 3 leaves a short last shard with padding rows)."""
+    single = _run(1, data)[0]
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_worker_sharded, args=(world, _free_port(), d, data), nprocs=world, join=True)
+        parts = [np.load(os.path.join(d, f"rank{r}.npz")) for r in range(world)]
+    covered = []
+    for q in parts:
+        fb, fe = int(q["fb"]), int(q["fe"])
+        covered += list(range(fb, fe))
+        assert np.array_equal(q["xtx"], single[2][:, fb:fe])
+        assert np.array_equal(q["xty"], single[3][:, fb:fe])
+    assert covered == list(range(data[3]))
+
+
+def test_shard_rows_partition():
+    from paper_2401_13185_b200 import plan as P
+
+    for n in (1, 7, 600, 1001):
+        for world in (1, 2, 3, 8):
+            spans = [P.shard_rows(n, r, world) for r in range(world)]
+            assert spans[0][0] == 0 and spans[-1][1] == n
+            assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
