@@ -199,6 +199,9 @@ void cvg_context_destroy(cvg_context* ctx) {
   cudaStreamSynchronize(ctx->stream);
   ctx->clear_recs();
   for (cudaEvent_t e : ctx->event_pool) cudaEventDestroy(e);
+  if (ctx->copy_stream) cudaStreamSynchronize(ctx->copy_stream);
+  for (cudaEvent_t e : ctx->sync_events) cudaEventDestroy(e);
+  if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
   ctx->scratch.reset();
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
   delete ctx;
@@ -317,13 +320,18 @@ int cvg_run_all_folds(cvg_context* ctx, int dtype, const void* x, const void* y,
     TRY(sc.x.ensure(e * n * k));
     TRY(sc.y.ensure(e * n * m));
     TRY(sc.labels.ensure(sizeof(int32_t) * n));
-    TRY(cvg::cuda_status(cudaMemcpyAsync(sc.x.as<void>(), x, e * n * k, cudaMemcpyHostToDevice, st), "H2D x"));
-    TRY(cvg::cuda_status(cudaMemcpyAsync(sc.y.as<void>(), y, e * n * m, cudaMemcpyHostToDevice, st), "H2D y"));
     TRY(cvg::cuda_status(cudaMemcpyAsync(sc.labels.as<void>(), labels, sizeof(int32_t) * n, cudaMemcpyHostToDevice, st),
                          "H2D labels"));
     TRY(sc.plan.create(ctx, dtype, n, k, m, p, 0, p, true));
     TRY(sc.plan.bind_labels(sc.labels.as<int32_t>(), true, scal));
-    TRY(sc.plan.gram(sc.x.as<void>(), k, sc.y.as<void>(), m, nullptr, nullptr));
+    // shift = row 0 of (x | y), read on the host; x and y stream in by column slabs
+    std::vector<double> shift(k + m);
+    for (int64_t c = 0; c < k + m; ++c) {
+      const void* src = c < k ? x : y;
+      const int64_t i = c < k ? c : c - k;
+      shift[c] = dtype == CVG_DTYPE_F32 ? (double)static_cast<const float*>(src)[i] : static_cast<const double*>(src)[i];
+    }
+    TRY(sc.plan.gram_host(x, y, sc.x.as<void>(), sc.y.as<void>(), shift.data()));
     const size_t nxx = (size_t)n_cfg * p * k * k, nxy = (size_t)n_cfg * p * k * m;
     TRY(sc.xtx.ensure(sizeof(double) * nxx));
     TRY(sc.xty.ensure(sizeof(double) * nxy));

@@ -49,8 +49,8 @@ void launch_scatter(const int32_t* labels, int64_t n, int32_t p, int32_t fold_be
 
 // K1: gather + shift + ones column + zero padding (+ finiteness flag).
 void launch_reorder(int dtype, const void* x, int64_t ldx, const void* y, int64_t ldy, int64_t k, int64_t m,
-                    const int64_t* src_row, int64_t zrows, int64_t kp, const double* shift, double* z, int* nonfinite,
-                    cudaStream_t s);
+                    const int64_t* src_row, int64_t zrows, int64_t kp, int64_t c_begin, int64_t c_end,
+                    const double* shift, double* z, int* nonfinite, cudaStream_t s);
 void launch_shift_from_row0(int dtype, const void* x, const void* y, int64_t k, int64_t m, double* shift,
                             cudaStream_t s);
 
@@ -101,8 +101,8 @@ std::vector<int2> gram_tiles(int64_t k, int64_t m, int64_t kp, int edge = kTile)
 // 32-row blocks;
 // then the tcgen05 kind::tf32 Gram (3 products: hi·hi + hi·lo + lo·hi).
 void launch_reorder_split_t(int dtype, const void* x, int64_t ldx, const void* y, int64_t ldy, int64_t k, int64_t m,
-                            const int64_t* src_row, int64_t zrows, int64_t kp, const double* shift, float* zt_hi,
-                            float* zt_lo, int* nonfinite, cudaStream_t s);
+                            const int64_t* src_row, int64_t zrows, int64_t kp, int64_t c_begin, int64_t c_end,
+                            const double* shift, float* zt_hi, float* zt_lo, int* nonfinite, cudaStream_t s);
 bool launch_gram_tf32(const float* zt_hi, const float* zt_lo, int64_t zrows, int64_t kp, const GramTask* segs,
                       int64_t nseg, const int2* tiles128, int ntiles, double* part, int nterms, cudaStream_t s);
 

@@ -25,6 +25,20 @@ cudaEvent_t cvg_context::take_event() {
   return e;
 }
 
+cvg::Status cvg_context::ensure_copy_stream() {
+  if (copy_stream) return cvg::Status::Ok();
+  return cvg::cuda_status(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking), "copy stream");
+}
+
+cudaEvent_t cvg_context::stream_event(size_t i) {
+  while (sync_events.size() <= i) {
+    cudaEvent_t e = nullptr;
+    cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    sync_events.push_back(e);
+  }
+  return sync_events[i];
+}
+
 void cvg_context::begin(int cls) {
   Rec r{cls, take_event(), take_event()};
   cudaEventRecord(r.a, stream);
@@ -438,8 +452,8 @@ Status Plan::gram(const void* d_x, int64_t ldx, const void* d_y, int64_t ldy, co
     if (zrows_ > 0) {
       {
         Timed t(ctx_, kReorder);
-        launch_reorder_split_t(dtype_, d_x, ldx, d_y, ldy, k_, m_, src_row_.as<int64_t>(), zrows_, kp_, shift,
-                               zt_hi_.as<float>(), zt_lo_.as<float>(), flag_.as<int>(), s);
+        launch_reorder_split_t(dtype_, d_x, ldx, d_y, ldy, k_, m_, src_row_.as<int64_t>(), zrows_, kp_, 0, kp_,
+                               shift, zt_hi_.as<float>(), zt_lo_.as<float>(), flag_.as<int>(), s);
       }
       CVG_TRY(count_launch());
     }
@@ -461,7 +475,7 @@ Status Plan::gram(const void* d_x, int64_t ldx, const void* d_y, int64_t ldy, co
     if (zrows_ > 0) {
       {
         Timed t(ctx_, kReorder);
-        launch_reorder(dtype_, d_x, ldx, d_y, ldy, k_, m_, src_row_.as<int64_t>(), zrows_, kp_, shift,
+        launch_reorder(dtype_, d_x, ldx, d_y, ldy, k_, m_, src_row_.as<int64_t>(), zrows_, kp_, 0, kp_, shift,
                        z_.as<double>(), flag_.as<int>(), s);
       }
       CVG_TRY(count_launch());
@@ -475,10 +489,103 @@ Status Plan::gram(const void* d_x, int64_t ldx, const void* d_y, int64_t ldy, co
       CVG_TRY(count_launch());
     }
   }
+  return gram_trees();
+}
+
+Status Plan::gram_trees() {
   CVG_TRY(fold_tree_.run(ctx_, tiles_d_.as<int2>(), (int)tiles_.size(), kp_));
   CVG_TRY(local_tree_.run(ctx_, tiles_d_.as<int2>(), (int)tiles_.size(), kp_));
   grammed_ = true;
   return Status::Ok();
+}
+
+// Host-resident x | y streamed by column slabs (cvg_run_all_folds).  The Gram
+// tile (i, j), i <= j, needs only Z columns of tile columns i and j, so X's
+// columns are copied in slabs of tile columns on a copy stream, and each
+// slab's K1 and the tiles it completes run on the compute stream while the
+// next slab is in flight.  Every tile is the same kernel over the same segments as gram(), so
+// the result is bit-identical; only the schedule changes.
+Status Plan::gram_host(const void* h_x, const void* h_y, void* d_x, void* d_y, const double* host_shift) {
+  if (!bound_) return Status::Err(4, "plan has no bound partitioning");
+  cudaStream_t s = ctx_->stream;
+  CVG_TRY(ctx_->ensure_copy_stream());
+  const size_t e = dtype_ == 1 ? 4 : 8;
+  const int E = dtype_ == 1 ? kTileF32 : kTile;
+  const int nt = (int)(kp_ / E);
+  const std::vector<int2>& tl = dtype_ == 1 ? tiles128_ : tiles_;
+  // tiles ordered by column tile, offsets per column tile
+  std::vector<int2> bycol;
+  std::vector<int> off(nt + 1, 0);
+  for (int j = 0; j < nt; ++j) {
+    off[j] = (int)bycol.size();
+    for (const int2& t : tl)
+      if (t.y == j) bycol.push_back(t);
+  }
+  off[nt] = (int)bycol.size();
+  CVG_TRY(tiles_bycol_d_.ensure(sizeof(int2) * std::max<size_t>(bycol.size(), 1)));
+  CVG_CK(cudaMemcpyAsync(tiles_bycol_d_.as<int2>(), bycol.data(), sizeof(int2) * bycol.size(),
+                         cudaMemcpyHostToDevice, s));
+  double* shift = shift_.as<double>();
+  CVG_CK(cudaMemcpyAsync(shift, host_shift, sizeof(double) * w_, cudaMemcpyHostToDevice, s));
+  CVG_CK(cudaMemsetAsync(flag_.as<void>(), 0, sizeof(int), s));
+  // the copy stream may overwrite d_x / d_y only after earlier work on s is done
+  cudaEvent_t ev0 = ctx_->stream_event(0);
+  CVG_CK(cudaEventRecord(ev0, s));
+  CVG_CK(cudaStreamWaitEvent(ctx_->copy_stream, ev0, 0));
+  // Slabs (in tile columns): [0, nt/2), [nt/2, nt-1), [nt-1, nt).  Tiles touching
+  // the last-arriving column are the only Gram work exposed after the final copy
+  // (nt of the nt(nt+1)/2 upper tiles); wide early slabs keep the 2-D copies at
+  // >= 53 GB/s (measured: 2 KB rows 54, 512 B rows 50, 256 B rows 46 GB/s).
+  std::vector<int> bounds{0};
+  if (nt >= 3) bounds.push_back((nt + 1) / 2);
+  if (nt >= 2 && bounds.back() < nt - 1) bounds.push_back(nt - 1);
+  bounds.push_back(nt);
+  for (size_t slab = 0; slab + 1 < bounds.size(); ++slab) {
+    const int a = bounds[slab], b = bounds[slab + 1];
+    const int64_t z0 = (int64_t)a * E, z1 = (int64_t)b * E;
+    const int64_t x0 = std::min(z0, k_), x1 = std::min(z1, k_);
+    if (x1 - x0 == k_)  // the whole row: one contiguous copy
+      CVG_CK(cudaMemcpyAsync(d_x, h_x, n_ * k_ * e, cudaMemcpyHostToDevice, ctx_->copy_stream));
+    else if (x1 > x0)
+      CVG_CK(cudaMemcpy2DAsync(static_cast<char*>(d_x) + x0 * e, k_ * e, static_cast<const char*>(h_x) + x0 * e,
+                               k_ * e, (x1 - x0) * e, n_, cudaMemcpyHostToDevice, ctx_->copy_stream));
+    // Y (narrow rows: a 2-D copy would be DMA-descriptor bound) goes whole, contiguously,
+    // with the first slab that holds any of its columns.
+    if (z0 <= k_ && k_ < z1)
+      CVG_CK(cudaMemcpyAsync(d_y, h_y, n_ * m_ * e, cudaMemcpyHostToDevice, ctx_->copy_stream));
+    cudaEvent_t ev = ctx_->stream_event(1 + slab);
+    CVG_CK(cudaEventRecord(ev, ctx_->copy_stream));
+    CVG_CK(cudaStreamWaitEvent(s, ev, 0));
+    const int t0 = off[a], t1 = off[b];
+    if (zrows_ > 0) {
+      {
+        Timed t(ctx_, kReorder);
+        if (dtype_ == 1)
+          launch_reorder_split_t(dtype_, d_x, k_, d_y, m_, k_, m_, src_row_.as<int64_t>(), zrows_, kp_, z0, z1, shift,
+                                 zt_hi_.as<float>(), zt_lo_.as<float>(), flag_.as<int>(), s);
+        else
+          launch_reorder(dtype_, d_x, k_, d_y, m_, k_, m_, src_row_.as<int64_t>(), zrows_, kp_, z0, z1, shift,
+                         z_.as<double>(), flag_.as<int>(), s);
+      }
+      CVG_TRY(count_launch());
+    }
+    if (!segs_.empty() && t1 > t0) {
+      bool ok = true;
+      {
+        Timed t(ctx_, kGram);
+        if (dtype_ == 1)
+          ok = launch_gram_tf32(zt_hi_.as<float>(), zt_lo_.as<float>(), zrows_, kp_, segs_d_.as<GramTask>(),
+                                (int64_t)segs_.size(), tiles_bycol_d_.as<int2>() + t0, t1 - t0, part_.as<double>(), 3,
+                                s);
+        else
+          launch_gram_f64(z_.as<double>(), kp_, segs_d_.as<GramTask>(), (int64_t)segs_.size(),
+                          tiles_bycol_d_.as<int2>() + t0, t1 - t0, part_.as<double>(), s);
+      }
+      if (!ok) return Status::Err(5, "cuTensorMapEncodeTiled unavailable or rejected the operand layout");
+      CVG_TRY(count_launch());
+    }
+  }
+  return gram_trees();
 }
 
 Status Plan::finish(const double* d_rank_partials, int32_t n_ranks, const double* total_override,

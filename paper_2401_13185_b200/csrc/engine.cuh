@@ -69,6 +69,10 @@ class Plan {
   // K1 + K2 + K4.  Exactly one of host_shift / dev_shift may be non-null; both null => row 0.
   Status gram(const void* d_x, int64_t ldx, const void* d_y, int64_t ldy, const double* host_shift,
               const double* dev_shift);
+  // Same as gram() for HOST x | y (row-major, ldx = k, ldy = m): column slabs
+  // are copied into d_x / d_y (n x k, n x m) on the context's copy stream while
+  // earlier slabs' K1 + Gram tiles run; bit-identical to gram().
+  Status gram_host(const void* h_x, const void* h_y, void* d_x, void* d_y, const double* host_shift);
   // Cross-rank combine (optional) + K5 for the owned folds into device outputs.
   Status finish(const double* d_rank_partials, int32_t n_ranks, const double* total_override,
                 const uint32_t* cfgs, int32_t ncfg, double* d_xtx, double* d_xty, double* d_mean_x,
@@ -101,6 +105,7 @@ class Plan {
 
  private:
   Status plan_segments();
+  Status gram_trees();
   Status count_launch(int n = 1);
   void assign_rank();  // rank mode: fb_/fe_, segment window, fold group
   int64_t chunk_rows() const;
@@ -124,7 +129,7 @@ class Plan {
   DevBuf zero_g_, zero_nval_, zero_ptr_;
 
   DevBuf tiles_d_, out_tiles_d_, tiles128_d_, zt_hi_, zt_lo_, tile_counts_, fold_counts_, bad_, zbase_d_, src_row_, z_, part_, foldbuf_, local_,
-      total_, shift_, flag_, segs_d_, foldptr_d_, nval_d_, st_mz_, st_sT_, st_sd_, cfg_d_;
+      total_, shift_, flag_, tiles_bycol_d_, segs_d_, foldptr_d_, nval_d_, st_mz_, st_sT_, st_sd_, cfg_d_;
   TreeProgram fold_tree_, local_tree_, rank_tree_;
   std::vector<const double*> fold_ptrs_;
 };
@@ -152,6 +157,11 @@ struct cvg_context {
   std::vector<Rec> recs;
   std::vector<cudaEvent_t> event_pool;
   cudaEvent_t take_event();
+  // host-input streaming (Plan::gram_host): a copy stream and reusable events
+  cudaStream_t copy_stream = nullptr;
+  std::vector<cudaEvent_t> sync_events;
+  cvg::Status ensure_copy_stream();
+  cudaEvent_t stream_event(size_t i);
   void begin(int cls);
   void end();
   void clear_recs();

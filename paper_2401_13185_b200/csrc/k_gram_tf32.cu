@@ -255,8 +255,8 @@ template <typename T>
 __global__ void __launch_bounds__(256) reorder_split_t_kernel(const T* __restrict__ x, int64_t ldx,
                                                               const T* __restrict__ y, int64_t ldy, int64_t k,
                                                               int64_t m, const int64_t* __restrict__ src_row,
-                                                              int64_t zrows, int64_t kp,
-                                                              const double* __restrict__ shift,
+                                                              int64_t zrows, int64_t kp, int64_t c_begin,
+                                                              int64_t c_end, const double* __restrict__ shift,
                                                               float* __restrict__ zt_hi, float* __restrict__ zt_lo,
                                                               int* __restrict__ nonfinite) {
   __shared__ float s_hi[kK1tCols][33], s_lo[kK1tCols][33];
@@ -270,7 +270,7 @@ __global__ void __launch_bounds__(256) reorder_split_t_kernel(const T* __restric
   const int q4 = (t & 31) * 4;  // this thread's 4 columns within the chunk
   const int r_lo = t >> 5;      // rows r_lo + 8j, j = 0..3
   bool bad = false;
-  for (int64_t c0 = 0; c0 < kp; c0 += kK1tCols) {
+  for (int64_t c0 = c_begin; c0 < c_end; c0 += kK1tCols) {
     const int64_t c = c0 + q4;
     float sh[4];
     int kind[4];  // 0 data, 1 ones column, 2 padding
@@ -333,7 +333,7 @@ __global__ void __launch_bounds__(256) reorder_split_t_kernel(const T* __restric
     for (int cc = t >> 3; cc < kK1tCols; cc += 32) {
       const int64_t col = c0 + cc;
       const int r4 = (t & 7) * 4;
-      if (col < kp) {
+      if (col < c_end) {
         const int64_t off = (blk * kp + col) * 32 + r4;  // Zt[block][col][row % 32]
         *reinterpret_cast<float4*>(zt_hi + off) =
             make_float4(s_hi[cc][r4], s_hi[cc][r4 + 1], s_hi[cc][r4 + 2], s_hi[cc][r4 + 3]);
@@ -377,15 +377,15 @@ bool make_map(CUtensorMap* map, const float* base, int64_t zrows, int64_t kp) {
 }  // namespace
 
 void launch_reorder_split_t(int dtype, const void* x, int64_t ldx, const void* y, int64_t ldy, int64_t k, int64_t m,
-                            const int64_t* src_row, int64_t zrows, int64_t kp, const double* shift, float* zt_hi,
-                            float* zt_lo, int* nonfinite, cudaStream_t s) {
+                            const int64_t* src_row, int64_t zrows, int64_t kp, int64_t c_begin, int64_t c_end,
+                            const double* shift, float* zt_hi, float* zt_lo, int* nonfinite, cudaStream_t s) {
   dim3 grid((unsigned)((zrows + 31) / 32));
   if (dtype == 0)
     reorder_split_t_kernel<double><<<grid, 256, 0, s>>>((const double*)x, ldx, (const double*)y, ldy, k, m, src_row,
-                                                        zrows, kp, shift, zt_hi, zt_lo, nonfinite);
+                                                        zrows, kp, c_begin, c_end, shift, zt_hi, zt_lo, nonfinite);
   else
     reorder_split_t_kernel<float><<<grid, 256, 0, s>>>((const float*)x, ldx, (const float*)y, ldy, k, m, src_row,
-                                                       zrows, kp, shift, zt_hi, zt_lo, nonfinite);
+                                                       zrows, kp, c_begin, c_end, shift, zt_hi, zt_lo, nonfinite);
 }
 
 bool launch_gram_tf32(const float* zt_hi, const float* zt_lo, int64_t zrows, int64_t kp, const GramTask* segs,

@@ -23,6 +23,7 @@ template <typename T>
 __global__ void __launch_bounds__(256) reorder_kernel(const T* __restrict__ x, int64_t ldx, const T* __restrict__ y,
                                                       int64_t ldy, int64_t k, int64_t m,
                                                       const int64_t* __restrict__ src_row, int64_t zrows, int64_t kp,
+                                                      int64_t c_begin, int64_t c_end,
                                                       const double* __restrict__ shift, double* __restrict__ z,
                                                       int* __restrict__ nonfinite) {
   const int lane = threadIdx.x & 31;
@@ -33,12 +34,12 @@ __global__ void __launch_bounds__(256) reorder_kernel(const T* __restrict__ x, i
     const int64_t src = src_row[r];
     double* zr = z + r * kp;
     if (src < 0) {
-      for (int64_t c = lane; c < kp; c += 32) zr[c] = 0.0;
+      for (int64_t c = c_begin + lane; c < c_end; c += 32) zr[c] = 0.0;
       continue;
     }
     const T* xr = x + src * ldx;
     const T* yr = y + src * ldy;
-    for (int64_t c0 = 0; c0 < kp; c0 += 128) {
+    for (int64_t c0 = c_begin; c0 < c_end; c0 += 128) {
       double v[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
@@ -53,7 +54,7 @@ __global__ void __launch_bounds__(256) reorder_kernel(const T* __restrict__ x, i
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const int64_t c = c0 + u * 32 + lane;
-        if (c >= kp) break;
+        if (c >= c_end) break;
         double out;
         if (c < w) {
           bad |= !isfinite(v[u]);
@@ -81,18 +82,20 @@ __global__ void shift_row0_kernel(const T* __restrict__ x, const T* __restrict__
 }  // namespace
 
 void launch_reorder(int dtype, const void* x, int64_t ldx, const void* y, int64_t ldy, int64_t k, int64_t m,
-                    const int64_t* src_row, int64_t zrows, int64_t kp, const double* shift, double* z, int* nonfinite,
-                    cudaStream_t s) {
+                    const int64_t* src_row, int64_t zrows, int64_t kp, int64_t c_begin, int64_t c_end,
+                    const double* shift, double* z, int* nonfinite, cudaStream_t s) {
   const int threads = 256;
   int64_t blocks = (zrows * 32 + threads - 1) / threads;
   if (blocks > 148 * 16) blocks = 148 * 16;  // grid-stride: 16 CTAs (128 rows in flight) per SM
   if (blocks < 1) blocks = 1;
   if (dtype == 0)
     reorder_kernel<double><<<(unsigned)blocks, threads, 0, s>>>((const double*)x, ldx, (const double*)y, ldy, k, m,
-                                                                src_row, zrows, kp, shift, z, nonfinite);
+                                                                src_row, zrows, kp, c_begin, c_end, shift, z,
+                                                                nonfinite);
   else
     reorder_kernel<float><<<(unsigned)blocks, threads, 0, s>>>((const float*)x, ldx, (const float*)y, ldy, k, m,
-                                                               src_row, zrows, kp, shift, z, nonfinite);
+                                                               src_row, zrows, kp, c_begin, c_end, shift, z,
+                                                               nonfinite);
 }
 
 void launch_shift_from_row0(int dtype, const void* x, const void* y, int64_t k, int64_t m, double* shift,
