@@ -24,7 +24,10 @@ namespace cvg {
 constexpr int kTile = 64;          // Gram / epilogue tile edge (columns)
 constexpr int kRowStep = 32;       // rows per pipeline stage; fold blocks pad to this
 constexpr int64_t kChunkRows = 32768;     // max rows per fp64 segment (fixed => deterministic split)
-constexpr int64_t kChunkRowsF32 = 32768;  // fp32 segments (the tcgen05 Gram drains fp32 to fp64 every 512 rows)
+// fp32 segments: shorter than fp64 so the 45 tcgen05 tiles of a segment (kp 1152 at c3) re-read
+// less from DRAM (c3 sweep: 32768 -> 44.9 ms, 16384 -> 44.5, 12288 -> 42.9, 8192 -> 44.2: the
+// tree over more partials eats the rest).
+constexpr int64_t kChunkRowsF32 = 12288;
 constexpr int kTileF32 = 128;             // tcgen05 tile edge (M = N = 128)
 constexpr int kTileRowsPerWarp = 1024; // rows per warp in the bucketing passes
 
@@ -59,8 +62,9 @@ struct GramTask {
   int64_t zrow;  // first Z row of the segment
   int64_t rows;  // padded row count (multiple of kRowStep)
 };
+// tiles: n_off off-diagonal tiles first, then the diagonal ones (see the kernel).
 void launch_gram_f64(const double* z, int64_t kp, const GramTask* segs, int64_t nseg, const int2* tiles,
-                     int ntiles, double* part, cudaStream_t s);
+                     int ntiles, int n_off, double* part, cudaStream_t s);
 
 // K4: fixed-order (midpoint-tree) sums of kp x kp matrices over upper tiles,
 // one launch per tree level.  d = a + b; b == null copies a; a == null zeroes d.

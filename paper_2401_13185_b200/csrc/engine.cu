@@ -100,10 +100,17 @@ std::vector<int2> gram_tiles(int64_t k, int64_t m, int64_t kp, int edge) {
   const int tx = (int)((k - 1) / edge);  // last tile holding X columns
   const int to = (int)((k + m) / edge);  // tile holding the ones column
   std::vector<int2> t;
-  for (int i = 0; i < nt; ++i)
-    for (int j = i; j < nt; ++j)
-      if (i <= tx || j == i || j == to) t.push_back(make_int2(i, j));
+  for (int pass = 0; pass < 2; ++pass)  // off-diagonal tiles first, then the diagonal (launch_gram_f64)
+    for (int i = 0; i < nt; ++i)
+      for (int j = i; j < nt; ++j)
+        if ((i <= tx || j == i || j == to) && ((j == i) == (pass == 1))) t.push_back(make_int2(i, j));
   return t;
+}
+
+int off_diagonal_count(const std::vector<int2>& tiles) {
+  int n = 0;
+  for (const int2& t : tiles) n += t.x != t.y;
+  return n;
 }
 
 const double* TreeProgram::emit(const std::vector<const double*>& leaves, int a, int b, int depth, double* root_dst,
@@ -484,7 +491,7 @@ Status Plan::gram(const void* d_x, int64_t ldx, const void* d_y, int64_t ldy, co
       {
         Timed t(ctx_, kGram);
         launch_gram_f64(z_.as<double>(), kp_, segs_d_.as<GramTask>(), (int64_t)segs_.size(), tiles_d_.as<int2>(),
-                        (int)tiles_.size(), part_.as<double>(), s);
+                        (int)tiles_.size(), off_diagonal_count(tiles_), part_.as<double>(), s);
       }
       CVG_TRY(count_launch());
     }
@@ -513,25 +520,6 @@ Status Plan::gram_host(const void* h_x, const void* h_y, void* d_x, void* d_y, c
   const int E = dtype_ == 1 ? kTileF32 : kTile;
   const int nt = (int)(kp_ / E);
   const std::vector<int2>& tl = dtype_ == 1 ? tiles128_ : tiles_;
-  // tiles ordered by column tile, offsets per column tile
-  std::vector<int2> bycol;
-  std::vector<int> off(nt + 1, 0);
-  for (int j = 0; j < nt; ++j) {
-    off[j] = (int)bycol.size();
-    for (const int2& t : tl)
-      if (t.y == j) bycol.push_back(t);
-  }
-  off[nt] = (int)bycol.size();
-  CVG_TRY(tiles_bycol_d_.ensure(sizeof(int2) * std::max<size_t>(bycol.size(), 1)));
-  CVG_CK(cudaMemcpyAsync(tiles_bycol_d_.as<int2>(), bycol.data(), sizeof(int2) * bycol.size(),
-                         cudaMemcpyHostToDevice, s));
-  double* shift = shift_.as<double>();
-  CVG_CK(cudaMemcpyAsync(shift, host_shift, sizeof(double) * w_, cudaMemcpyHostToDevice, s));
-  CVG_CK(cudaMemsetAsync(flag_.as<void>(), 0, sizeof(int), s));
-  // the copy stream may overwrite d_x / d_y only after earlier work on s is done
-  cudaEvent_t ev0 = ctx_->stream_event(0);
-  CVG_CK(cudaEventRecord(ev0, s));
-  CVG_CK(cudaStreamWaitEvent(ctx_->copy_stream, ev0, 0));
   // Slabs (in tile columns): [0, nt/2), [nt/2, nt-1), [nt-1, nt).  Tiles touching
   // the last-arriving column are the only Gram work exposed after the final copy
   // (nt of the nt(nt+1)/2 upper tiles); wide early slabs keep the 2-D copies at
@@ -540,6 +528,29 @@ Status Plan::gram_host(const void* h_x, const void* h_y, void* d_x, void* d_y, c
   if (nt >= 3) bounds.push_back((nt + 1) / 2);
   if (nt >= 2 && bounds.back() < nt - 1) bounds.push_back(nt - 1);
   bounds.push_back(nt);
+  // each slab's tiles (column tile in the slab), off-diagonal first as gram_tiles orders them
+  std::vector<int2> byslab;
+  std::vector<int> off{0}, noff;
+  for (size_t sl = 0; sl + 1 < bounds.size(); ++sl) {
+    int no = 0;
+    for (const int2& t : tl)
+      if (t.y >= bounds[sl] && t.y < bounds[sl + 1]) {
+        byslab.push_back(t);
+        no += t.x != t.y;
+      }
+    off.push_back((int)byslab.size());
+    noff.push_back(no);
+  }
+  CVG_TRY(tiles_bycol_d_.ensure(sizeof(int2) * std::max<size_t>(byslab.size(), 1)));
+  CVG_CK(cudaMemcpyAsync(tiles_bycol_d_.as<int2>(), byslab.data(), sizeof(int2) * byslab.size(),
+                         cudaMemcpyHostToDevice, s));
+  double* shift = shift_.as<double>();
+  CVG_CK(cudaMemcpyAsync(shift, host_shift, sizeof(double) * w_, cudaMemcpyHostToDevice, s));
+  CVG_CK(cudaMemsetAsync(flag_.as<void>(), 0, sizeof(int), s));
+  // the copy stream may overwrite d_x / d_y only after earlier work on s is done
+  cudaEvent_t ev0 = ctx_->stream_event(0);
+  CVG_CK(cudaEventRecord(ev0, s));
+  CVG_CK(cudaStreamWaitEvent(ctx_->copy_stream, ev0, 0));
   for (size_t slab = 0; slab + 1 < bounds.size(); ++slab) {
     const int a = bounds[slab], b = bounds[slab + 1];
     const int64_t z0 = (int64_t)a * E, z1 = (int64_t)b * E;
@@ -556,7 +567,7 @@ Status Plan::gram_host(const void* h_x, const void* h_y, void* d_x, void* d_y, c
     cudaEvent_t ev = ctx_->stream_event(1 + slab);
     CVG_CK(cudaEventRecord(ev, ctx_->copy_stream));
     CVG_CK(cudaStreamWaitEvent(s, ev, 0));
-    const int t0 = off[a], t1 = off[b];
+    const int t0 = off[slab], t1 = off[slab + 1];
     if (zrows_ > 0) {
       {
         Timed t(ctx_, kReorder);
@@ -579,7 +590,7 @@ Status Plan::gram_host(const void* h_x, const void* h_y, void* d_x, void* d_y, c
                                 s);
         else
           launch_gram_f64(z_.as<double>(), kp_, segs_d_.as<GramTask>(), (int64_t)segs_.size(),
-                          tiles_bycol_d_.as<int2>() + t0, t1 - t0, part_.as<double>(), s);
+                          tiles_bycol_d_.as<int2>() + t0, t1 - t0, noff[slab], part_.as<double>(), s);
       }
       if (!ok) return Status::Err(5, "cuTensorMapEncodeTiled unavailable or rejected the operand layout");
       CVG_TRY(count_launch());

@@ -44,12 +44,27 @@ __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
                : "d"(a), "d"(b));
 }
 
+// Grid order: every segment's off-diagonal tiles first (tiles[0, n_off), segment-
+// major so a segment's CTAs share its rows in L2), then every segment's diagonal
+// tiles (tiles[n_off, ntiles)), which do about half the work: the last, partly
+// filled wave is made of the cheap CTAs.
 __global__ void __launch_bounds__(NT, 2)
-    gram_f64_kernel(const double* __restrict__ z, int64_t kp, const GramTask* __restrict__ segs,
-                    const int2* __restrict__ tiles, int ntiles, double* __restrict__ part) {
+    gram_f64_kernel(const double* __restrict__ z, int64_t kp, const GramTask* __restrict__ segs, int64_t nseg,
+                    const int2* __restrict__ tiles, int ntiles, int n_off, double* __restrict__ part) {
   extern __shared__ __align__(128) double smem[];
-  const int seg = blockIdx.x / ntiles;
-  const int2 tile = tiles[blockIdx.x - seg * ntiles];
+  int seg;
+  int2 tile;
+  {
+    const int64_t b = blockIdx.x, head = nseg * (int64_t)n_off;
+    if (b < head) {
+      seg = (int)(b / n_off);
+      tile = tiles[b - (int64_t)seg * n_off];
+    } else {
+      const int nd = ntiles - n_off;
+      seg = (int)((b - head) / nd);
+      tile = tiles[n_off + (b - head - (int64_t)seg * nd)];
+    }
+  }
   const int ti = tile.x, tj = tile.y;
   const bool diag = ti == tj;
   const GramTask task = segs[seg];
@@ -129,7 +144,7 @@ __global__ void __launch_bounds__(NT, 2)
 }  // namespace
 
 void launch_gram_f64(const double* z, int64_t kp, const GramTask* segs, int64_t nseg, const int2* tiles, int ntiles,
-                     double* part, cudaStream_t s) {
+                     int n_off, double* part, cudaStream_t s) {
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(gram_f64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
@@ -137,7 +152,7 @@ void launch_gram_f64(const double* z, int64_t kp, const GramTask* segs, int64_t 
   }
   const int64_t blocks = nseg * (int64_t)ntiles;
   if (blocks <= 0) return;
-  gram_f64_kernel<<<(unsigned)blocks, NT, kSmemBytes, s>>>(z, kp, segs, tiles, ntiles, part);
+  gram_f64_kernel<<<(unsigned)blocks, NT, kSmemBytes, s>>>(z, kp, segs, nseg, tiles, ntiles, n_off, part);
 }
 
 }  // namespace cvg
