@@ -110,7 +110,7 @@ Status small_vector_op(cvg_context* ctx, std::initializer_list<std::pair<const d
 // Gram passes (any shift -> training means; then the exact-mean basis), the
 // direct epilogue per configuration.  Device outputs for this fold:
 // xtx[c] at xtx + c*cstride_xx, xty likewise; stats [k|m] (may be null).
-Status baseline_rows(cvg_context* ctx, int dtype, const void* d_x, const void* d_y, int64_t k, int64_t m,
+Status baseline_rows(cvg_context* ctx, int dtype, const void* d_x, const void* d_y, int64_t n, int64_t k, int64_t m,
                      const std::vector<int64_t>& t_rows, const uint32_t* cfgs, int32_t ncfg, double* d_xtx,
                      int64_t cstride_xx, double* d_xty, int64_t cstride_xy, double* d_mx, double* d_my,
                      double* d_sx, double* d_sy, cvg::DevBuf& mean_buf) {
@@ -118,7 +118,7 @@ Status baseline_rows(cvg_context* ctx, int dtype, const void* d_x, const void* d
   const int64_t nt = (int64_t)t_rows.size();
   Status s = pl.create(ctx, dtype, std::max<int64_t>(nt, 2), k, m, 1, 0, 1, false);
   if (!s.ok()) return s;
-  if (!(s = pl.bind_rows(t_rows.data(), nt)).ok()) return s;
+  if (!(s = pl.bind_rows(t_rows.data(), nt, n)).ok()) return s;
   if (!(s = pl.gram(d_x, k, d_y, m, nullptr, nullptr)).ok()) return s;  // pass 1: means
   if (!(s = mean_buf.ensure(sizeof(double) * (k + m))).ok()) return s;
   if (!(s = pl.direct_means(mean_buf.as<double>())).ok()) return s;
@@ -405,7 +405,7 @@ int cvg_baseline_fold_products(cvg_context* ctx, int dtype, const void* x, const
         if (labels[i] != f + 1) t_rows[f].push_back(i);
     cvg::DevBuf mean_buf;
     for (int32_t f = 0; f < p; ++f) {
-      s = baseline_rows(ctx, dtype, sc.x.as<void>(), sc.y.as<void>(), k, m, t_rows[f], cfg_masks, n_cfg,
+      s = baseline_rows(ctx, dtype, sc.x.as<void>(), sc.y.as<void>(), n, k, m, t_rows[f], cfg_masks, n_cfg,
                         sc.xtx.as<double>() + (size_t)f * k * k, (int64_t)p * k * k,
                         sc.xty.as<double>() + (size_t)f * k * m, (int64_t)p * k * m, sc.mx.as<double>() + f * k,
                         sc.my.as<double>() + f * m, sc.sx.as<double>() + f * k, sc.sy.as<double>() + f * m, mean_buf);
@@ -473,7 +473,7 @@ int cvg_baseline_single_fold(cvg_context* ctx, int dtype, const void* x, const v
       return s;
     double* stv = ost.as<double>();
     const int64_t w = k + m;
-    if (!(s = baseline_rows(ctx, dtype, dx.as<void>(), dy.as<void>(), k, m, t_rows, &cfg, 1, oxx.as<double>(), 0,
+    if (!(s = baseline_rows(ctx, dtype, dx.as<void>(), dy.as<void>(), n, k, m, t_rows, &cfg, 1, oxx.as<double>(), 0,
                             oxy.as<double>(), 0, stv, stv + k, stv + w, stv + w + k, mean_buf))
              .ok())
       return s;

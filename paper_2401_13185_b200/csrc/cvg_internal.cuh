@@ -13,6 +13,8 @@
 // Gram[j][j] the sum of squares: the per-fold statistics ride in the Gram pass.
 #pragma once
 
+#include <cstdio>
+
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -31,6 +33,29 @@ constexpr int64_t kChunkRowsF32 = 12288;
 constexpr int kTileF32 = 128;             // tcgen05 tile edge (M = N = 128)
 constexpr int kTileRowsPerWarp = 1024; // rows per warp in the bucketing passes
 
+// Checked builds (make CHECKED=1 -> _build_checked/, selected with CVG_LIB_VARIANT=checked):
+// device-side bounds assertions on every index the kernels derive (row maps,
+// segment ranges, tile coordinates, scatter positions).  A failed check prints
+// the site and traps, which surfaces as CVG_E_CUDA.  compute-sanitizer is not
+// available on this pool, so this build + the GPU suite is the bounds evidence.
+#ifndef CVG_CHECKED
+#define CVG_CHECKED 0
+#endif
+#if CVG_CHECKED
+#define CVG_DCHECK(cond)                                                                                   \
+  do {                                                                                                     \
+    if (!(cond)) {                                                                                         \
+      printf("CVG_DCHECK failed: %s at %s:%d block %d thread %d\n", #cond, __FILE__, __LINE__, (int)blockIdx.x, \
+             (int)threadIdx.x);                                                                            \
+      __trap();                                                                                            \
+    }                                                                                                      \
+  } while (0)
+#else
+#define CVG_DCHECK(cond) \
+  do {                   \
+  } while (0)
+#endif
+
 struct Status {
   int code = 0;
   std::string msg;
@@ -48,11 +73,11 @@ void launch_tile_scan(int32_t* tile_counts, int64_t ntiles, int32_t p, int64_t* 
 // (a rank owning only part of one fold's segments).
 void launch_scatter(const int32_t* labels, int64_t n, int32_t p, int32_t fold_begin, int32_t fold_end,
                     int32_t* tile_offsets, const int64_t* fold_zbase, int64_t win_lo, int64_t win_hi, int64_t* src_row,
-                    cudaStream_t s);
+                    int64_t zrows, cudaStream_t s);
 
 // K1: gather + shift + ones column + zero padding (+ finiteness flag).
 void launch_reorder(int dtype, const void* x, int64_t ldx, const void* y, int64_t ldy, int64_t k, int64_t m,
-                    const int64_t* src_row, int64_t zrows, int64_t kp, int64_t c_begin, int64_t c_end,
+                    const int64_t* src_row, int64_t zrows, int64_t kp, int64_t c_begin, int64_t c_end, int64_t nsrc,
                     const double* shift, double* z, int* nonfinite, cudaStream_t s);
 void launch_shift_from_row0(int dtype, const void* x, const void* y, int64_t k, int64_t m, double* shift,
                             cudaStream_t s);
@@ -63,8 +88,8 @@ struct GramTask {
   int64_t rows;  // padded row count (multiple of kRowStep)
 };
 // tiles: n_off off-diagonal tiles first, then the diagonal ones (see the kernel).
-void launch_gram_f64(const double* z, int64_t kp, const GramTask* segs, int64_t nseg, const int2* tiles,
-                     int ntiles, int n_off, double* part, cudaStream_t s);
+void launch_gram_f64(const double* z, int64_t kp, int64_t zrows, const GramTask* segs, int64_t nseg,
+                     const int2* tiles, int ntiles, int n_off, double* part, cudaStream_t s);
 
 // K4: fixed-order (midpoint-tree) sums of kp x kp matrices over upper tiles,
 // one launch per tree level.  d = a + b; b == null copies a; a == null zeroes d.

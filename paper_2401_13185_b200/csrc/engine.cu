@@ -284,6 +284,7 @@ void Plan::assign_rank() {
 }
 
 Status Plan::bind_labels(const int32_t* d_labels, bool validate, bool require_scalable) {
+  src_n_ = n_;
   cudaStream_t s = ctx_->stream;
   const int64_t ntiles = (n_ + kTileRowsPerWarp - 1) / kTileRowsPerWarp;
   CVG_TRY(tile_counts_.ensure(sizeof(int32_t) * ntiles * p_));
@@ -330,15 +331,18 @@ Status Plan::bind_labels(const int32_t* d_labels, bool validate, bool require_sc
     const int64_t win_lo = seg_lo_ >= 0 ? seg_lo_ * chunk_rows() : 0;
     const int64_t win_hi = seg_lo_ >= 0 ? win_lo + zrows_ : INT64_MAX;
     launch_scatter(d_labels, n_, p_, fb_, fe_, tile_counts_.as<int32_t>(), zbase_d_.as<int64_t>(), win_lo, win_hi,
-                   src_row_.as<int64_t>(), s);
+                   src_row_.as<int64_t>(), zrows_, s);
   }
   CVG_TRY(count_launch());
   bound_ = true;
   return Status::Ok();
 }
 
-Status Plan::bind_rows(const int64_t* rows, int64_t nrows) {
+Status Plan::bind_rows(const int64_t* rows, int64_t nrows, int64_t n_src) {
   if (p_ != 1 || fb_ != 0 || fe_ != 1) return Status::Err(4, "bind_rows needs a single-fold plan");
+  src_n_ = n_src < 0 ? n_ : n_src;
+  for (int64_t i = 0; i < nrows; ++i)
+    if (rows[i] < 0 || rows[i] >= src_n_) return Status::Err(4, "bind_rows: row index outside the source matrix");
   counts_.assign(1, nrows);
   CVG_TRY(plan_segments());
   std::vector<int64_t> src(std::max<int64_t>(zrows_, 1), -1);
@@ -482,7 +486,7 @@ Status Plan::gram(const void* d_x, int64_t ldx, const void* d_y, int64_t ldy, co
     if (zrows_ > 0) {
       {
         Timed t(ctx_, kReorder);
-        launch_reorder(dtype_, d_x, ldx, d_y, ldy, k_, m_, src_row_.as<int64_t>(), zrows_, kp_, 0, kp_, shift,
+        launch_reorder(dtype_, d_x, ldx, d_y, ldy, k_, m_, src_row_.as<int64_t>(), zrows_, kp_, 0, kp_, src_n_, shift,
                        z_.as<double>(), flag_.as<int>(), s);
       }
       CVG_TRY(count_launch());
@@ -490,7 +494,7 @@ Status Plan::gram(const void* d_x, int64_t ldx, const void* d_y, int64_t ldy, co
     if (!segs_.empty()) {
       {
         Timed t(ctx_, kGram);
-        launch_gram_f64(z_.as<double>(), kp_, segs_d_.as<GramTask>(), (int64_t)segs_.size(), tiles_d_.as<int2>(),
+        launch_gram_f64(z_.as<double>(), kp_, zrows_, segs_d_.as<GramTask>(), (int64_t)segs_.size(), tiles_d_.as<int2>(),
                         (int)tiles_.size(), off_diagonal_count(tiles_), part_.as<double>(), s);
       }
       CVG_TRY(count_launch());
@@ -575,7 +579,7 @@ Status Plan::gram_host(const void* h_x, const void* h_y, void* d_x, void* d_y, c
           launch_reorder_split_t(dtype_, d_x, k_, d_y, m_, k_, m_, src_row_.as<int64_t>(), zrows_, kp_, z0, z1, shift,
                                  zt_hi_.as<float>(), zt_lo_.as<float>(), flag_.as<int>(), s);
         else
-          launch_reorder(dtype_, d_x, k_, d_y, m_, k_, m_, src_row_.as<int64_t>(), zrows_, kp_, z0, z1, shift,
+          launch_reorder(dtype_, d_x, k_, d_y, m_, k_, m_, src_row_.as<int64_t>(), zrows_, kp_, z0, z1, src_n_, shift,
                          z_.as<double>(), flag_.as<int>(), s);
       }
       CVG_TRY(count_launch());
@@ -589,7 +593,7 @@ Status Plan::gram_host(const void* h_x, const void* h_y, void* d_x, void* d_y, c
                                 (int64_t)segs_.size(), tiles_bycol_d_.as<int2>() + t0, t1 - t0, part_.as<double>(), 3,
                                 s);
         else
-          launch_gram_f64(z_.as<double>(), kp_, segs_d_.as<GramTask>(), (int64_t)segs_.size(),
+          launch_gram_f64(z_.as<double>(), kp_, zrows_, segs_d_.as<GramTask>(), (int64_t)segs_.size(),
                           tiles_bycol_d_.as<int2>() + t0, t1 - t0, noff[slab], part_.as<double>(), s);
       }
       if (!ok) return Status::Err(5, "cuTensorMapEncodeTiled unavailable or rejected the operand layout");

@@ -65,7 +65,8 @@ class Plan {
   // Device labels -> fold-bucketed row order (validates like partition.hpp:21-58 when `validate`).
   Status bind_labels(const int32_t* d_labels, bool validate, bool require_scalable);
   // Explicit ascending rows of the single owned fold (fold_products / precompute_global).
-  Status bind_rows(const int64_t* rows, int64_t nrows);
+  // rows index a source X of n_src rows (< 0: the plan's n); checked on the host.
+  Status bind_rows(const int64_t* rows, int64_t nrows, int64_t n_src = -1);
   // K1 + K2 + K4.  Exactly one of host_shift / dev_shift may be non-null; both null => row 0.
   Status gram(const void* d_x, int64_t ldx, const void* d_y, int64_t ldy, const double* host_shift,
               const double* dev_shift);
@@ -120,6 +121,7 @@ class Plan {
   std::vector<int32_t> fold_seg_begin_;
   std::vector<int64_t> fold_zbase_;
   int64_t zrows_ = 0;
+  int64_t src_n_ = 0;  // rows of the x / y the row map indexes (K1 bounds)
   bool bound_ = false, grammed_ = false;
   bool rank_mode_ = false, emits_ = true;
   int32_t rank_ = 0, world_ = 1;

@@ -49,8 +49,8 @@ __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
 // tiles (tiles[n_off, ntiles)), which do about half the work: the last, partly
 // filled wave is made of the cheap CTAs.
 __global__ void __launch_bounds__(NT, 2)
-    gram_f64_kernel(const double* __restrict__ z, int64_t kp, const GramTask* __restrict__ segs, int64_t nseg,
-                    const int2* __restrict__ tiles, int ntiles, int n_off, double* __restrict__ part) {
+    gram_f64_kernel(const double* __restrict__ z, int64_t kp, int64_t zrows, const GramTask* __restrict__ segs,
+                    int64_t nseg, const int2* __restrict__ tiles, int ntiles, int n_off, double* __restrict__ part) {
   extern __shared__ __align__(128) double smem[];
   int seg;
   int2 tile;
@@ -67,7 +67,10 @@ __global__ void __launch_bounds__(NT, 2)
   }
   const int ti = tile.x, tj = tile.y;
   const bool diag = ti == tj;
+  CVG_DCHECK(seg >= 0 && seg < nseg);
   const GramTask task = segs[seg];
+  CVG_DCHECK(task.zrow >= 0 && task.rows % KC == 0 && task.zrow + task.rows <= zrows);
+  CVG_DCHECK(tile.x >= 0 && tile.x <= tile.y && (int64_t)(tile.y + 1) * BT <= kp);
   const double* zb = z + task.zrow * kp;
   const int nsteps = (int)(task.rows / KC);
 
@@ -143,8 +146,8 @@ __global__ void __launch_bounds__(NT, 2)
 
 }  // namespace
 
-void launch_gram_f64(const double* z, int64_t kp, const GramTask* segs, int64_t nseg, const int2* tiles, int ntiles,
-                     int n_off, double* part, cudaStream_t s) {
+void launch_gram_f64(const double* z, int64_t kp, int64_t zrows, const GramTask* segs, int64_t nseg,
+                     const int2* tiles, int ntiles, int n_off, double* part, cudaStream_t s) {
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(gram_f64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
@@ -152,7 +155,7 @@ void launch_gram_f64(const double* z, int64_t kp, const GramTask* segs, int64_t 
   }
   const int64_t blocks = nseg * (int64_t)ntiles;
   if (blocks <= 0) return;
-  gram_f64_kernel<<<(unsigned)blocks, NT, kSmemBytes, s>>>(z, kp, segs, nseg, tiles, ntiles, n_off, part);
+  gram_f64_kernel<<<(unsigned)blocks, NT, kSmemBytes, s>>>(z, kp, zrows, segs, nseg, tiles, ntiles, n_off, part);
 }
 
 }  // namespace cvg

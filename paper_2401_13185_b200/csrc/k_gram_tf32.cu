@@ -130,6 +130,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int2 tile = tiles[blockIdx.x - seg * ntiles];
   const bool diag = tile.x == tile.y;
   const GramTask task = segs[seg];
+  CVG_DCHECK(task.zrow % KS == 0 && task.rows % KS == 0 && task.rows > 0);
+  CVG_DCHECK(tile.x >= 0 && tile.x <= tile.y && (int64_t)(tile.y + 1) * TT <= kp);
   const int nsteps = (int)(task.rows / KS);
   const int nchunks = (nsteps + kDrainSteps - 1) / kDrainSteps;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -265,6 +267,7 @@ __global__ void __launch_bounds__(256) reorder_split_t_kernel(const T* __restric
   const int t = threadIdx.x;
   const int64_t w = k + m;
   if (t < 32) s_src[t] = blk * 32 + t < zrows ? src_row[blk * 32 + t] : -1;
+  CVG_DCHECK(c_begin >= 0 && c_end <= kp && c_begin % kK1tCols == 0);
   __syncthreads();
   const bool vec = (k % 4 == 0) && (ldx % 4 == 0) && sizeof(T) == 4;
   const int q4 = (t & 31) * 4;  // this thread's 4 columns within the chunk

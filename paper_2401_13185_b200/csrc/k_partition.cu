@@ -83,7 +83,7 @@ __global__ void tile_scan_kernel(int32_t* __restrict__ tile_counts, int64_t ntil
 __global__ void scatter_kernel(const int32_t* __restrict__ labels, int64_t n, int32_t p, int32_t fold_begin,
                                int32_t fold_end, int32_t* __restrict__ tile_offsets,
                                const int64_t* __restrict__ fold_zbase, int64_t win_lo, int64_t win_hi,
-                               int64_t* __restrict__ src_row) {
+                               int64_t* __restrict__ src_row, int64_t zrows) {
   const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   const int64_t row0 = warp * kTileRowsPerWarp;
@@ -103,7 +103,11 @@ __global__ void scatter_kernel(const int32_t* __restrict__ labels, int64_t n, in
       before = run[label - 1];
       const int rank = __popc(peers & ((1u << lane) - 1u));
       const int64_t pos = before + rank;  // position within the fold's bucketed rows
-      if (pos >= win_lo && pos < win_hi) src_row[fold_zbase[label - 1 - fold_begin] + pos - win_lo] = row;
+      if (pos >= win_lo && pos < win_hi) {
+        const int64_t dst = fold_zbase[label - 1 - fold_begin] + pos - win_lo;
+        CVG_DCHECK(dst >= 0 && dst < zrows);
+        src_row[dst] = row;
+      }
     }
     __syncwarp();
     if (own && lane == __ffs(peers) - 1) run[label - 1] = before + __popc(peers);
@@ -127,12 +131,12 @@ void launch_tile_scan(int32_t* tile_counts, int64_t ntiles, int32_t p, int64_t* 
 
 void launch_scatter(const int32_t* labels, int64_t n, int32_t p, int32_t fold_begin, int32_t fold_end,
                     int32_t* tile_offsets, const int64_t* fold_zbase, int64_t win_lo, int64_t win_hi, int64_t* src_row,
-                    cudaStream_t s) {
+                    int64_t zrows, cudaStream_t s) {
   const int64_t ntiles = (n + kTileRowsPerWarp - 1) / kTileRowsPerWarp;
   const int threads = 256;
   const int64_t blocks = (ntiles * 32 + threads - 1) / threads;
   scatter_kernel<<<(unsigned)blocks, threads, 0, s>>>(labels, n, p, fold_begin, fold_end, tile_offsets, fold_zbase,
-                                                      win_lo, win_hi, src_row);
+                                                      win_lo, win_hi, src_row, zrows);
 }
 
 }  // namespace cvg

@@ -23,6 +23,8 @@ __global__ void __launch_bounds__(256) pair_sum_kernel(const PairOp* __restrict_
                                                        const int2* __restrict__ tiles) {
   const int2 tile = tiles[blockIdx.x];
   const PairOp op = ops[blockIdx.y];
+  CVG_DCHECK(op.d != nullptr && (op.a != nullptr || op.b == nullptr));
+  CVG_DCHECK(tile.x >= 0 && tile.x <= tile.y && (int64_t)(tile.y + 1) * kTile <= kp);
   const int c2 = (threadIdx.x & 31) * 2;  // column pair within the tile
 #pragma unroll 4
   for (int r = threadIdx.x >> 5; r < kTile; r += 8) {
@@ -44,8 +46,10 @@ __global__ void __launch_bounds__(256) pair_sum_kernel(const PairOp* __restrict_
 
 void launch_pair_sums(const PairOp* ops, int nops, int64_t kp, const int2* tiles, int ntiles, cudaStream_t s) {
   if (nops <= 0 || ntiles <= 0) return;
-  dim3 grid((unsigned)ntiles, (unsigned)nops);
-  pair_sum_kernel<<<grid, 256, 0, s>>>(ops, kp, tiles);
+  for (int o = 0; o < nops; o += 65535) {  // gridDim.y <= 65535 (a level of a leave-one-out tree can hold N ops)
+    dim3 grid((unsigned)ntiles, (unsigned)(nops - o < 65535 ? nops - o : 65535));
+    pair_sum_kernel<<<grid, 256, 0, s>>>(ops + o, kp, tiles);
+  }
 }
 
 }  // namespace cvg

@@ -23,7 +23,7 @@ template <typename T>
 __global__ void __launch_bounds__(256) reorder_kernel(const T* __restrict__ x, int64_t ldx, const T* __restrict__ y,
                                                       int64_t ldy, int64_t k, int64_t m,
                                                       const int64_t* __restrict__ src_row, int64_t zrows, int64_t kp,
-                                                      int64_t c_begin, int64_t c_end,
+                                                      int64_t c_begin, int64_t c_end, int64_t nsrc,
                                                       const double* __restrict__ shift, double* __restrict__ z,
                                                       int* __restrict__ nonfinite) {
   const int lane = threadIdx.x & 31;
@@ -32,6 +32,8 @@ __global__ void __launch_bounds__(256) reorder_kernel(const T* __restrict__ x, i
   bool bad = false;
   for (int64_t r = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; r < zrows; r += warps) {
     const int64_t src = src_row[r];
+    CVG_DCHECK(src < nsrc && src >= -1);
+    CVG_DCHECK(c_begin >= 0 && c_end <= kp && c_begin % 64 == 0);
     double* zr = z + r * kp;
     if (src < 0) {
       for (int64_t c = c_begin + lane; c < c_end; c += 32) zr[c] = 0.0;
@@ -82,7 +84,7 @@ __global__ void shift_row0_kernel(const T* __restrict__ x, const T* __restrict__
 }  // namespace
 
 void launch_reorder(int dtype, const void* x, int64_t ldx, const void* y, int64_t ldy, int64_t k, int64_t m,
-                    const int64_t* src_row, int64_t zrows, int64_t kp, int64_t c_begin, int64_t c_end,
+                    const int64_t* src_row, int64_t zrows, int64_t kp, int64_t c_begin, int64_t c_end, int64_t nsrc,
                     const double* shift, double* z, int* nonfinite, cudaStream_t s) {
   const int threads = 256;
   int64_t blocks = (zrows * 32 + threads - 1) / threads;
@@ -90,11 +92,11 @@ void launch_reorder(int dtype, const void* x, int64_t ldx, const void* y, int64_
   if (blocks < 1) blocks = 1;
   if (dtype == 0)
     reorder_kernel<double><<<(unsigned)blocks, threads, 0, s>>>((const double*)x, ldx, (const double*)y, ldy, k, m,
-                                                                src_row, zrows, kp, c_begin, c_end, shift, z,
+                                                                src_row, zrows, kp, c_begin, c_end, nsrc, shift, z,
                                                                 nonfinite);
   else
     reorder_kernel<float><<<(unsigned)blocks, threads, 0, s>>>((const float*)x, ldx, (const float*)y, ldy, k, m,
-                                                               src_row, zrows, kp, c_begin, c_end, shift, z,
+                                                               src_row, zrows, kp, c_begin, c_end, nsrc, shift, z,
                                                                nonfinite);
 }
 
