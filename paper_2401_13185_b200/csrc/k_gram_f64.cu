@@ -12,7 +12,8 @@
 // Tensor path: sm_100 has no fp64 tcgen05 kind; `mma.sync.m8n8k4.f64` lowers to
 // SASS DMMA.8x8x4, measured at 37.1 TFLOP/s on this B200 (profiles/r01_fp64_peaks.txt).
 // CTA = 64x64 output tile, 8 warps (2 x 4), warp tile 32x16 = 4x2 DMMA tiles.
-// Operands: 32-row x 64-col slabs staged by cp.async (16 B) into a 3-stage ring;
+// Operands: 32-row x 64-col slabs staged by cp.async (16 B) into a 3-stage ring
+// synchronised by mbarriers (see gram_f64_kernel);
 // the smem row pitch of 68 doubles makes the DMMA fragment loads conflict-free
 // (lanes (g, t) read [t][g]: bank = 2(68t + g) mod 32 covers all 32 banks).
 #include "cvg_internal.cuh"
@@ -32,11 +33,6 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
 }
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
-}
 
 __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -44,14 +40,34 @@ __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
                : "d"(a), "d"(b));
 }
 
+// Pipeline: per-stage mbarriers instead of a CTA barrier per step.  Every
+// thread's cp.asyncs for a stage arrive on full[stage] when they land
+// (cp.async.mbarrier.arrive.noinc), each warp arrives on empty[stage] after its
+// DMMAs, and a stage is refilled only once all 8 warps have left it, so warps
+// drift up to one stage apart instead of re-aligning at every 32-row step
+// (measured against __syncthreads per step: c1 Gram 9.13 -> 8.99 ms, c2 13.35
+// -> 12.99, c4 36.77 -> 36.40; 6 stages of 16 rows were slower than 3 of 32).
+__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n.reg .pred P1;\nWAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra DONE_%=;\nbra WAIT_%=;\nDONE_%=:\n}\n" ::"r"(smem_addr(bar)),
+      "r"(parity)
+      : "memory");
+}
+
 // Grid order: every segment's off-diagonal tiles first (tiles[0, n_off), segment-
 // major so a segment's CTAs share its rows in L2), then every segment's diagonal
 // tiles (tiles[n_off, ntiles)), which do about half the work: the last, partly
 // filled wave is made of the cheap CTAs.
+template <int KCm, int STm>
 __global__ void __launch_bounds__(NT, 2)
     gram_f64_kernel(const double* __restrict__ z, int64_t kp, int64_t zrows, const GramTask* __restrict__ segs,
                     int64_t nseg, const int2* __restrict__ tiles, int ntiles, int n_off, double* __restrict__ part) {
+  constexpr int kSl = KCm * LDS;  // doubles per operand slab
   extern __shared__ __align__(128) double smem[];
+  __shared__ __align__(8) uint64_t full[STm], empty[STm];
   int seg;
   int2 tile;
   {
@@ -69,29 +85,35 @@ __global__ void __launch_bounds__(NT, 2)
   const bool diag = ti == tj;
   CVG_DCHECK(seg >= 0 && seg < nseg);
   const GramTask task = segs[seg];
-  CVG_DCHECK(task.zrow >= 0 && task.rows % KC == 0 && task.zrow + task.rows <= zrows);
+  CVG_DCHECK(task.zrow >= 0 && task.rows % KCm == 0 && task.zrow + task.rows <= zrows);
   CVG_DCHECK(tile.x >= 0 && tile.x <= tile.y && (int64_t)(tile.y + 1) * BT <= kp);
   const double* zb = z + task.zrow * kp;
-  const int nsteps = (int)(task.rows / KC);
-
+  const int nsteps = (int)(task.rows / KCm);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t4 = lane & 3;
   const int wi = (warp >> 2) * 32, wj = (warp & 3) * 16;
-  // In diagonal tiles the warps whose 32x16 block lies strictly below the
-  // diagonal skip the MMA loop (warp-uniform; the epilogue reads j >= i only).
   const bool idle = diag && wi >= wj + 16;
+  if (tid == 0) {
+    for (int s = 0; s < STm; ++s) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_addr(&full[s])), "r"(NT));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_addr(&empty[s])), "r"(NT / 32));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
 
   auto load_stage = [&](int step, int buf) {
-    const double* src = zb + (int64_t)step * KC * kp;
-    double* dA = smem + buf * 2 * kSlab;
-    double* dB = dA + kSlab;
+    const double* src = zb + (int64_t)step * KCm * kp;
+    double* dA = smem + buf * 2 * kSl;
+    double* dB = dA + kSl;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int idx = tid + q * NT;  // 0..1023: 32 rows x 32 16-byte chunks
+    for (int q = 0; q < KCm * 32 / NT; ++q) {  // KCm rows x 32 16-byte chunks
+      const int idx = tid + q * NT;
       const int r = idx >> 5, c = (idx & 31) * 2;
       cp_async16(dA + r * LDS + c, src + (int64_t)r * kp + ti * BT + c);
       if (!diag) cp_async16(dB + r * LDS + c, src + (int64_t)r * kp + tj * BT + c);
     }
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_addr(&full[buf])) : "memory");
   };
 
   double acc[4][2][2];
@@ -99,39 +121,39 @@ __global__ void __launch_bounds__(NT, 2)
   for (int a = 0; a < 4; ++a)
 #pragma unroll
     for (int b = 0; b < 2; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
-
 #pragma unroll
-  for (int s = 0; s < STAGES - 1; ++s) {
+  for (int s = 0; s < STm - 1; ++s)
     if (s < nsteps) load_stage(s, s);
-    cp_async_commit();
-  }
   for (int step = 0; step < nsteps; ++step) {
-    cp_async_wait<STAGES - 2>();
-    __syncthreads();
-    {
-      const int nxt = step + STAGES - 1;
-      if (nxt < nsteps) load_stage(nxt, nxt % STAGES);
-      cp_async_commit();
+    const int buf = step % STm;
+    mbar_wait_parity(&full[buf], (uint32_t)(step / STm) & 1u);
+    if (!idle) {
+      const double* sA = smem + buf * 2 * kSl;
+      const double* sB = diag ? sA : sA + kSl;
+#pragma unroll
+      for (int kk = 0; kk < KCm; kk += 4) {
+        const double* pa = sA + (kk + t4) * LDS + wi + g;
+        const double* pb = sB + (kk + t4) * LDS + wj + g;
+        double a[4], b[2];
+#pragma unroll
+        for (int mi = 0; mi < 4; ++mi) a[mi] = pa[mi * 8];
+#pragma unroll
+        for (int ni = 0; ni < 2; ++ni) b[ni] = pb[ni * 8];
+#pragma unroll
+        for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+          for (int ni = 0; ni < 2; ++ni) dmma(acc[mi][ni], a[mi], b[ni]);
+      }
     }
-    if (idle) continue;
-    const double* sA = smem + (step % STAGES) * 2 * kSlab;
-    const double* sB = diag ? sA : sA + kSlab;
-#pragma unroll
-    for (int kk = 0; kk < KC; kk += 4) {
-      const double* pa = sA + (kk + t4) * LDS + wi + g;
-      const double* pb = sB + (kk + t4) * LDS + wj + g;
-      double a[4], b[2];
-#pragma unroll
-      for (int mi = 0; mi < 4; ++mi) a[mi] = pa[mi * 8];
-#pragma unroll
-      for (int ni = 0; ni < 2; ++ni) b[ni] = pb[ni * 8];
-#pragma unroll
-      for (int mi = 0; mi < 4; ++mi)
-#pragma unroll
-        for (int ni = 0; ni < 2; ++ni) dmma(acc[mi][ni], a[mi], b[ni]);
+    __syncwarp();
+    if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_addr(&empty[buf])) : "memory");
+    const int nxt = step + STm - 1;
+    if (nxt < nsteps) {
+      const int nb = nxt % STm;  // last held step nxt - STm = step - 1
+      if (nxt >= STm) mbar_wait_parity(&empty[nb], (uint32_t)((nxt - STm) / STm) & 1u);
+      load_stage(nxt, nb);
     }
   }
-  cp_async_wait<0>();
 
   double* out = part + (int64_t)seg * kp * kp;
 #pragma unroll
@@ -150,12 +172,13 @@ void launch_gram_f64(const double* z, int64_t kp, int64_t zrows, const GramTask*
                      const int2* tiles, int ntiles, int n_off, double* part, cudaStream_t s) {
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(gram_f64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+    cudaFuncSetAttribute(gram_f64_kernel<KC, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
     attr_set = true;
   }
   const int64_t blocks = nseg * (int64_t)ntiles;
   if (blocks <= 0) return;
-  gram_f64_kernel<<<(unsigned)blocks, NT, kSmemBytes, s>>>(z, kp, zrows, segs, nseg, tiles, ntiles, n_off, part);
+  gram_f64_kernel<KC, STAGES><<<(unsigned)blocks, NT, kSmemBytes, s>>>(z, kp, zrows, segs, nseg, tiles, ntiles,
+                                                                      n_off, part);
 }
 
 }  // namespace cvg
