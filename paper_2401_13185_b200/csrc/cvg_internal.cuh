@@ -87,9 +87,8 @@ struct GramTask {
   int64_t zrow;  // first Z row of the segment
   int64_t rows;  // padded row count (multiple of kRowStep)
 };
-// tiles: n_off off-diagonal tiles first, then the diagonal ones (see the kernel).
 void launch_gram_f64(const double* z, int64_t kp, int64_t zrows, const GramTask* segs, int64_t nseg,
-                     const int2* tiles, int ntiles, int n_off, double* part, cudaStream_t s);
+                     const int2* tiles, int ntiles, double* part, cudaStream_t s);
 
 // K4: fixed-order (midpoint-tree) sums of kp x kp matrices over upper tiles,
 // one launch per tree level.  d = a + b; b == null copies a; a == null zeroes d.

@@ -100,18 +100,13 @@ std::vector<int2> gram_tiles(int64_t k, int64_t m, int64_t kp, int edge) {
   const int tx = (int)((k - 1) / edge);  // last tile holding X columns
   const int to = (int)((k + m) / edge);  // tile holding the ones column
   std::vector<int2> t;
-  for (int pass = 0; pass < 2; ++pass)  // off-diagonal tiles first, then the diagonal (launch_gram_f64)
-    for (int i = 0; i < nt; ++i)
-      for (int j = i; j < nt; ++j)
-        if ((i <= tx || j == i || j == to) && ((j == i) == (pass == 1))) t.push_back(make_int2(i, j));
+  for (int i = 0; i < nt; ++i)
+    for (int j = i; j < nt; ++j)
+      if (i <= tx || j == i || j == to) t.push_back(make_int2(i, j));
   return t;
 }
 
-int off_diagonal_count(const std::vector<int2>& tiles) {
-  int n = 0;
-  for (const int2& t : tiles) n += t.x != t.y;
-  return n;
-}
+
 
 const double* TreeProgram::emit(const std::vector<const double*>& leaves, int a, int b, int depth, double* root_dst,
                                 std::vector<std::vector<PairOp>>& by_depth, int64_t kp) {
@@ -495,7 +490,7 @@ Status Plan::gram(const void* d_x, int64_t ldx, const void* d_y, int64_t ldy, co
       {
         Timed t(ctx_, kGram);
         launch_gram_f64(z_.as<double>(), kp_, zrows_, segs_d_.as<GramTask>(), (int64_t)segs_.size(), tiles_d_.as<int2>(),
-                        (int)tiles_.size(), off_diagonal_count(tiles_), part_.as<double>(), s);
+                        (int)tiles_.size(), part_.as<double>(), s);
       }
       CVG_TRY(count_launch());
     }
@@ -532,18 +527,13 @@ Status Plan::gram_host(const void* h_x, const void* h_y, void* d_x, void* d_y, c
   if (nt >= 3) bounds.push_back((nt + 1) / 2);
   if (nt >= 2 && bounds.back() < nt - 1) bounds.push_back(nt - 1);
   bounds.push_back(nt);
-  // each slab's tiles (column tile in the slab), off-diagonal first as gram_tiles orders them
+  // each slab's tiles (column tile in the slab)
   std::vector<int2> byslab;
-  std::vector<int> off{0}, noff;
+  std::vector<int> off{0};
   for (size_t sl = 0; sl + 1 < bounds.size(); ++sl) {
-    int no = 0;
     for (const int2& t : tl)
-      if (t.y >= bounds[sl] && t.y < bounds[sl + 1]) {
-        byslab.push_back(t);
-        no += t.x != t.y;
-      }
+      if (t.y >= bounds[sl] && t.y < bounds[sl + 1]) byslab.push_back(t);
     off.push_back((int)byslab.size());
-    noff.push_back(no);
   }
   CVG_TRY(tiles_bycol_d_.ensure(sizeof(int2) * std::max<size_t>(byslab.size(), 1)));
   CVG_CK(cudaMemcpyAsync(tiles_bycol_d_.as<int2>(), byslab.data(), sizeof(int2) * byslab.size(),
@@ -594,7 +584,7 @@ Status Plan::gram_host(const void* h_x, const void* h_y, void* d_x, void* d_y, c
                                 s);
         else
           launch_gram_f64(z_.as<double>(), kp_, zrows_, segs_d_.as<GramTask>(), (int64_t)segs_.size(),
-                          tiles_bycol_d_.as<int2>() + t0, t1 - t0, noff[slab], part_.as<double>(), s);
+                          tiles_bycol_d_.as<int2>() + t0, t1 - t0, part_.as<double>(), s);
       }
       if (!ok) return Status::Err(5, "cuTensorMapEncodeTiled unavailable or rejected the operand layout");
       CVG_TRY(count_launch());

@@ -57,30 +57,19 @@ __device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, uint32_t parity)
       : "memory");
 }
 
-// Grid order: every segment's off-diagonal tiles first (tiles[0, n_off), segment-
-// major so a segment's CTAs share its rows in L2), then every segment's diagonal
-// tiles (tiles[n_off, ntiles)), which do about half the work: the last, partly
-// filled wave is made of the cheap CTAs.
+// Grid order: segment-major, tile fastest, so the CTAs of one segment run
+// together and share its rows in L2 (ncu, c1: 4.9 GB DRAM for 4.1 GB of Z).
+// (Running every diagonal tile after all off-diagonal ones, to end on cheap
+// CTAs, saved nothing and re-read every segment: 8.8 GB.)
 template <int KCm, int STm>
 __global__ void __launch_bounds__(NT, 2)
     gram_f64_kernel(const double* __restrict__ z, int64_t kp, int64_t zrows, const GramTask* __restrict__ segs,
-                    int64_t nseg, const int2* __restrict__ tiles, int ntiles, int n_off, double* __restrict__ part) {
+                    int64_t nseg, const int2* __restrict__ tiles, int ntiles, double* __restrict__ part) {
   constexpr int kSl = KCm * LDS;  // doubles per operand slab
   extern __shared__ __align__(128) double smem[];
   __shared__ __align__(8) uint64_t full[STm], empty[STm];
-  int seg;
-  int2 tile;
-  {
-    const int64_t b = blockIdx.x, head = nseg * (int64_t)n_off;
-    if (b < head) {
-      seg = (int)(b / n_off);
-      tile = tiles[b - (int64_t)seg * n_off];
-    } else {
-      const int nd = ntiles - n_off;
-      seg = (int)((b - head) / nd);
-      tile = tiles[n_off + (b - head - (int64_t)seg * nd)];
-    }
-  }
+  const int seg = (int)(blockIdx.x / ntiles);
+  const int2 tile = tiles[blockIdx.x - (int64_t)seg * ntiles];
   const int ti = tile.x, tj = tile.y;
   const bool diag = ti == tj;
   CVG_DCHECK(seg >= 0 && seg < nseg);
@@ -169,7 +158,7 @@ __global__ void __launch_bounds__(NT, 2)
 }  // namespace
 
 void launch_gram_f64(const double* z, int64_t kp, int64_t zrows, const GramTask* segs, int64_t nseg,
-                     const int2* tiles, int ntiles, int n_off, double* part, cudaStream_t s) {
+                     const int2* tiles, int ntiles, double* part, cudaStream_t s) {
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(gram_f64_kernel<KC, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
@@ -178,7 +167,7 @@ void launch_gram_f64(const double* z, int64_t kp, int64_t zrows, const GramTask*
   const int64_t blocks = nseg * (int64_t)ntiles;
   if (blocks <= 0) return;
   gram_f64_kernel<KC, STAGES><<<(unsigned)blocks, NT, kSmemBytes, s>>>(z, kp, zrows, segs, nseg, tiles, ntiles,
-                                                                      n_off, part);
+                                                                      part);
 }
 
 }  // namespace cvg

@@ -1,0 +1,15 @@
+# Round measurement: every BASELINE config through bench.py, the reference arm, the
+# launch list (ncu, cold/serialised) and one ncu --set full capture of the c1 Gram.
+# Usage (from the repo root, on the GPU box):  bash tools/gpu_measure.sh r01
+R=${1:-r01}
+set -e; make -s -C paper_2401_13185_b200 >/dev/null; set +e
+python bench.py --steps 10 --warmup 3 > gpurun_out/bench_${R}_default.log 2>&1; echo "bench default rc=$?"
+for c in 0 2 3 4; do
+  python bench.py --config $c --steps 5 --warmup 3 > gpurun_out/bench_${R}_c$c.log 2>&1; echo "bench c$c rc=$?"
+done
+python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_${R}_ref.log 2>&1; echo "ref rc=$?"
+python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e > gpurun_out/plain.log 2>&1 && \
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_${R}.csv \
+  python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e > gpurun_out/ncu_launch.log 2>&1; echo "ncu launches rc=$?"
+ncu --set full --clock-control none --import-source on -k regex:"gram_f64" -c 1 -o gpurun_out/prof_gram_${R} \
+  python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e > gpurun_out/ncu_gram.log 2>&1; echo "ncu gram rc=$?"
