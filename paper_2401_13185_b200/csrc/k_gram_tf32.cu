@@ -246,10 +246,8 @@ __device__ __forceinline__ float tf32_rn(float v) {
 
 // K1T: bucket, shift, TF32-split, transpose into Zt[block][col][32] (HBM-bound).
 // One CTA per 32 bucketed rows, 128-column chunks through a padded shared-memory
-// transpose.  Each thread owns 4 columns (shifts in registers for the chunk) and
-// issues its 4 row loads (float4, 512 B per warp) before using any; each
-// column's 32 rows leave as 128 B, a warp covering 4 adjacent columns = 512
-// contiguous bytes.  The split is pure fp32: fl(x - c) is within 2^-24 of z and
+// transpose; each column's 32 rows leave as 128 B, a warp covering 4 adjacent
+// columns = 512 contiguous bytes.  The split is pure fp32: fl(x - c) is within 2^-24 of z and
 // hi / lo are exact (an fp64 convert chain made this pass compute-bound, ~2.6 TB/s).
 constexpr int kK1tCols = 128;
 
@@ -269,68 +267,58 @@ __global__ void __launch_bounds__(256) reorder_split_t_kernel(const T* __restric
   if (t < 32) s_src[t] = blk * 32 + t < zrows ? src_row[blk * 32 + t] : -1;
   CVG_DCHECK(c_begin >= 0 && c_end <= kp && c_begin % kK1tCols == 0);
   __syncthreads();
-  const bool vec = (k % 4 == 0) && (ldx % 4 == 0) && sizeof(T) == 4;
-  const int q4 = (t & 31) * 4;  // this thread's 4 columns within the chunk
-  const int r_lo = t >> 5;      // rows r_lo + 8j, j = 0..3
+  // Lane l owns columns c0 + l + 32e (e = 0..3) of rows r_lo + 8j: every load
+  // instruction is one coalesced 128-byte row segment, and the transposed
+  // shared-memory writes hit 32 distinct banks (bank = l + row).  The next
+  // chunk's loads are issued before this chunk's stores drain.
+  const int lane = t & 31;
+  const int r_lo = t >> 5;  // rows r_lo + 8j, j = 0..3
   bool bad = false;
-  for (int64_t c0 = c_begin; c0 < c_end; c0 += kK1tCols) {
-    const int64_t c = c0 + q4;
-    float sh[4];
-    int kind[4];  // 0 data, 1 ones column, 2 padding
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const int64_t ce = c + e;
-      sh[e] = ce < w ? (float)shift[ce] : 0.f;
-      kind[e] = ce < w ? 0 : (ce == w ? 1 : 2);
-    }
-    const bool fast = vec && c + 3 < k;
-    float v[4][4];
+  auto load_chunk = [&](int64_t c0, float (&v)[4][4]) {
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const int64_t src = s_src[r_lo + 8 * j];
-      if (fast) {
-        float4 f = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (src >= 0) f = *reinterpret_cast<const float4*>(reinterpret_cast<const float*>(x) + src * ldx + c);
-        v[j][0] = f.x;
-        v[j][1] = f.y;
-        v[j][2] = f.z;
-        v[j][3] = f.w;
-      } else {
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const int64_t ce = c + e;
-          float val = 0.f;
-          if (src >= 0) {
-            if (ce < k)
-              val = (float)x[src * ldx + ce];
-            else if (ce < w)
-              val = (float)y[src * ldy + (ce - k)];
-          }
-          v[j][e] = val;
-        }
-      }
-    }
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int rr = r_lo + 8 * j;
-      const bool live = s_src[rr] >= 0;
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
+        const int64_t ce = c0 + lane + 32 * e;
+        float val = 0.f;
+        if (src >= 0) {
+          if (ce < k)
+            val = (float)__ldg(x + src * ldx + ce);
+          else if (ce < w)
+            val = (float)__ldg(y + src * ldy + (ce - k));
+        }
+        v[j][e] = val;
+      }
+    }
+  };
+  float v[4][4];
+  load_chunk(c_begin, v);
+  for (int64_t c0 = c_begin; c0 < c_end; c0 += kK1tCols) {
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int64_t ce = c0 + lane + 32 * e;
+      const float sh = ce < w ? (float)__ldg(shift + ce) : 0.f;
+      const int kind = ce < w ? 0 : (ce == w ? 1 : 2);  // data, ones column, padding
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int rr = r_lo + 8 * j;
         float z = 0.f;
-        if (live) {
-          if (kind[e] == 0) {
+        if (s_src[rr] >= 0) {
+          if (kind == 0) {
             bad |= !isfinite(v[j][e]);
-            z = v[j][e] - sh[e];
-          } else if (kind[e] == 1) {
+            z = v[j][e] - sh;
+          } else if (kind == 1) {
             z = 1.f;  // ones column: column sums ride in the Gram
           }
         }
         const float hi = tf32_rn(z);
-        s_hi[q4 + e][rr] = hi;
-        s_lo[q4 + e][rr] = tf32_rn(z - hi);
+        s_hi[lane + 32 * e][rr] = hi;
+        s_lo[lane + 32 * e][rr] = tf32_rn(z - hi);
       }
     }
     __syncthreads();
+    if (c0 + kK1tCols < c_end) load_chunk(c0 + kK1tCols, v);  // in flight while the stores below drain
     // write: 8 threads per column (16 B each), 32 columns per pass
 #pragma unroll
     for (int cc = t >> 3; cc < kK1tCols; cc += 32) {
