@@ -341,8 +341,8 @@ def run_ours(args):
         e2e = {"value": round(flops / (e2e_ms * 1e-3) / 1e9, 3), "unit": "GFLOP/s", "ms_per_step": round(e2e_ms, 3),
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                "path": "plan.run_all_folds_sharded: per-rank pinned host row shard -> own PCIe H2D -> NCCL "
-                       "all-gather of rows -> fold-range run -> owned folds D2H; wall clock, max over ranks; "
-                       "bytes are whole-job totals"}
+                       "all-to-all of rows to their fold's owner (all-gather when P < N) -> fold-range run -> "
+                       "owned folds D2H; wall clock, max over ranks; bytes are whole-job totals"}
 
     if rank != 0:
         if world > 1:

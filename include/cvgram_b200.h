@@ -115,6 +115,14 @@ int cvg_plan_bind_labels(cvg_plan* plan, const int32_t* d_labels, int require_sc
  * shift: host pointer to k+m values, or NULL for row 0 of (x | y). */
 int cvg_plan_gram(cvg_plan* plan, const void* d_x, int64_t ldx, const void* d_y, int64_t ldy, const double* shift,
                   char* err, size_t errlen);
+/* cvg_plan_gram over COMPACTED inputs (multi-GPU row exchange): d_x / d_y hold
+ * n_compact rows, and original row i (of the n the labels describe) is compact
+ * row d_row_map[i] (device int64[n]; -1 = not present).  Every row of the
+ * plan's owned folds / segments must be present.  `shift` (k+m host values) is
+ * required: row 0 of the full data need not be present.  Same results, bit for
+ * bit, as cvg_plan_gram over the full x / y. */
+int cvg_plan_gram_mapped(cvg_plan* plan, const void* d_x, int64_t ldx, const void* d_y, int64_t ldy,
+                         const int64_t* d_row_map, int64_t n_compact, const double* shift, char* err, size_t errlen);
 /* This plan's contribution to the cross-rank fold sum (its node of the fold
  * tree): *count doubles, copied into device buffer d_dst when it is non-NULL. */
 int cvg_plan_partial(cvg_plan* plan, double* d_dst, int64_t* count);

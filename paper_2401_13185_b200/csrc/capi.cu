@@ -550,6 +550,16 @@ int cvg_plan_gram(cvg_plan* plan, const void* d_x, int64_t ldx, const void* d_y,
   });
 }
 
+int cvg_plan_gram_mapped(cvg_plan* plan, const void* d_x, int64_t ldx, const void* d_y, int64_t ldy,
+                         const int64_t* d_row_map, int64_t n_compact, const double* shift, char* err, size_t errlen) {
+  return guarded(err, errlen, [&]() -> Status {
+    if (!plan || !d_row_map) return Status::Err(CVG_E_INVALID_ARG, "null plan or row map");
+    if (!shift) return Status::Err(CVG_E_INVALID_ARG, "cvg_plan_gram_mapped needs an explicit shift");
+    if (n_compact < 0) return Status::Err(CVG_E_INVALID_ARG, "negative compact row count");
+    return plan->plan.gram(d_x, ldx, d_y, ldy, shift, nullptr, d_row_map, n_compact);
+  });
+}
+
 int cvg_plan_partial(cvg_plan* plan, double* d_dst, int64_t* count) {
   if (!plan || !count) return CVG_E_INVALID_ARG;
   *count = plan->plan.partial_count();

@@ -75,6 +75,9 @@ void launch_scatter(const int32_t* labels, int64_t n, int32_t p, int32_t fold_be
                     int32_t* tile_offsets, const int64_t* fold_zbase, int64_t win_lo, int64_t win_hi, int64_t* src_row,
                     int64_t zrows, cudaStream_t s);
 
+// out[r] = map[src_row[r]] (-1 for padding rows); *bad = 1 if a bound row is unmapped.
+void launch_remap_rows(const int64_t* src_row, int64_t zrows, const int64_t* map, int64_t n_map, int64_t n_compact,
+                       int64_t* out, int* bad, cudaStream_t s);
 // K1: gather + shift + ones column + zero padding (+ finiteness flag).
 void launch_reorder(int dtype, const void* x, int64_t ldx, const void* y, int64_t ldy, int64_t k, int64_t m,
                     const int64_t* src_row, int64_t zrows, int64_t kp, int64_t c_begin, int64_t c_end, int64_t nsrc,

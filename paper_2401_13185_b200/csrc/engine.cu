@@ -438,9 +438,26 @@ Status Plan::plan_segments() {
 }
 
 Status Plan::gram(const void* d_x, int64_t ldx, const void* d_y, int64_t ldy, const double* host_shift,
-                  const double* dev_shift) {
+                  const double* dev_shift, const int64_t* d_row_map, int64_t n_compact) {
   if (!bound_) return Status::Err(4, "plan has no bound partitioning");
   cudaStream_t s = ctx_->stream;
+  const int64_t* rows = src_row_.as<int64_t>();
+  int64_t nsrc = src_n_;
+  if (d_row_map) {
+    // compacted inputs: K1 reads compact row map[src_row[r]]; row 0 may be absent, so the shift is explicit
+    if (!host_shift && !dev_shift) return Status::Err(4, "a row-mapped gram needs an explicit shift");
+    CVG_TRY(src_map_.ensure(sizeof(int64_t) * std::max<int64_t>(zrows_, 1)));
+    CVG_CK(cudaMemsetAsync(flag_.as<void>(), 0, sizeof(int), s));
+    launch_remap_rows(src_row_.as<int64_t>(), zrows_, d_row_map, n_, n_compact, src_map_.as<int64_t>(),
+                      flag_.as<int>(), s);
+    CVG_TRY(count_launch());
+    int bad = 0;
+    CVG_CK(cudaMemcpyAsync(&bad, flag_.as<int>(), sizeof bad, cudaMemcpyDeviceToHost, s));
+    CVG_CK(cudaStreamSynchronize(s));
+    if (bad) return Status::Err(4, "row map does not cover every row of the owned folds");
+    rows = src_map_.as<int64_t>();
+    nsrc = n_compact;
+  }
   double* shift = shift_.as<double>();
   if (dev_shift) {
     CVG_CK(cudaMemcpyAsync(shift, dev_shift, sizeof(double) * w_, cudaMemcpyDeviceToDevice, s));
@@ -458,8 +475,8 @@ Status Plan::gram(const void* d_x, int64_t ldx, const void* d_y, int64_t ldy, co
     if (zrows_ > 0) {
       {
         Timed t(ctx_, kReorder);
-        launch_reorder_split_t(dtype_, d_x, ldx, d_y, ldy, k_, m_, src_row_.as<int64_t>(), zrows_, kp_, 0, kp_,
-                               shift, zt_hi_.as<float>(), zt_lo_.as<float>(), flag_.as<int>(), s);
+        launch_reorder_split_t(dtype_, d_x, ldx, d_y, ldy, k_, m_, rows, zrows_, kp_, 0, kp_, shift,
+                               zt_hi_.as<float>(), zt_lo_.as<float>(), flag_.as<int>(), s);
       }
       CVG_TRY(count_launch());
     }
@@ -481,7 +498,7 @@ Status Plan::gram(const void* d_x, int64_t ldx, const void* d_y, int64_t ldy, co
     if (zrows_ > 0) {
       {
         Timed t(ctx_, kReorder);
-        launch_reorder(dtype_, d_x, ldx, d_y, ldy, k_, m_, src_row_.as<int64_t>(), zrows_, kp_, 0, kp_, src_n_, shift,
+        launch_reorder(dtype_, d_x, ldx, d_y, ldy, k_, m_, rows, zrows_, kp_, 0, kp_, nsrc, shift,
                        z_.as<double>(), flag_.as<int>(), s);
       }
       CVG_TRY(count_launch());

@@ -68,8 +68,10 @@ class Plan {
   // rows index a source X of n_src rows (< 0: the plan's n); checked on the host.
   Status bind_rows(const int64_t* rows, int64_t nrows, int64_t n_src = -1);
   // K1 + K2 + K4.  Exactly one of host_shift / dev_shift may be non-null; both null => row 0.
+  // d_row_map (optional, n int64): x / y hold only the rows the map covers,
+  // original row i at compact row d_row_map[i] (< n_compact); -1 = absent.
   Status gram(const void* d_x, int64_t ldx, const void* d_y, int64_t ldy, const double* host_shift,
-              const double* dev_shift);
+              const double* dev_shift, const int64_t* d_row_map = nullptr, int64_t n_compact = 0);
   // Same as gram() for HOST x | y (row-major, ldx = k, ldy = m): column slabs
   // are copied into d_x / d_y (n x k, n x m) on the context's copy stream while
   // earlier slabs' K1 + Gram tiles run; bit-identical to gram().
@@ -131,7 +133,7 @@ class Plan {
   DevBuf zero_g_, zero_nval_, zero_ptr_;
 
   DevBuf tiles_d_, out_tiles_d_, tiles128_d_, zt_hi_, zt_lo_, tile_counts_, fold_counts_, bad_, zbase_d_, src_row_, z_, part_, foldbuf_, local_,
-      total_, shift_, flag_, tiles_bycol_d_, segs_d_, foldptr_d_, nval_d_, st_mz_, st_sT_, st_sd_, cfg_d_;
+      total_, shift_, flag_, tiles_bycol_d_, src_map_, segs_d_, foldptr_d_, nval_d_, st_mz_, st_sT_, st_sd_, cfg_d_;
   TreeProgram fold_tree_, local_tree_, rank_tree_;
   std::vector<const double*> fold_ptrs_;
 };

@@ -115,7 +115,31 @@ __global__ void scatter_kernel(const int32_t* __restrict__ labels, int64_t n, in
   }
 }
 
+// Row map for compacted inputs (multi-GPU row exchange): Z row r reads compact
+// row map[src_row[r]]; a bound row the map does not cover sets *bad.
+__global__ void remap_rows_kernel(const int64_t* __restrict__ src_row, int64_t zrows, const int64_t* __restrict__ map,
+                                  int64_t n_map, int64_t n_compact, int64_t* __restrict__ out, int* __restrict__ bad) {
+  const int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (r >= zrows) return;
+  const int64_t src = src_row[r];
+  int64_t v = -1;
+  if (src >= 0) {
+    v = src < n_map ? map[src] : -1;
+    if (v < 0 || v >= n_compact) {
+      atomicExch(bad, 1);
+      v = -1;
+    }
+  }
+  out[r] = v;
+}
+
 }  // namespace
+
+void launch_remap_rows(const int64_t* src_row, int64_t zrows, const int64_t* map, int64_t n_map, int64_t n_compact,
+                       int64_t* out, int* bad, cudaStream_t s) {
+  if (zrows <= 0) return;
+  remap_rows_kernel<<<(unsigned)((zrows + 255) / 256), 256, 0, s>>>(src_row, zrows, map, n_map, n_compact, out, bad);
+}
 
 void launch_tile_histogram(const int32_t* labels, int64_t n, int32_t p, int32_t* tile_counts,
                            unsigned long long* bad, cudaStream_t s) {

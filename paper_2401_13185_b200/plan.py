@@ -84,9 +84,17 @@ class DevicePlan:
         L.lib().cvg_plan_assignment(self._h, ctypes.addressof(b), ctypes.addressof(e))
         self.fold_begin, self.fold_end = b.value, e.value
 
-    def gram(self, x, y, shift: Optional[np.ndarray] = None) -> None:
+    def gram(self, x, y, shift: Optional[np.ndarray] = None, row_map=None) -> None:
+        """row_map (int64 CUDA tensor, n entries): x / y are compacted, original
+        row i at row_map[i] (-1 = absent); shift is then required."""
         buf = L.err_buf()
         sh = None if shift is None else np.ascontiguousarray(shift, np.float64)
+        if row_map is not None:
+            if sh is None:
+                raise ValueError("a row-mapped gram needs an explicit shift")
+            _check(L.lib().cvg_plan_gram_mapped(self._h, _dptr(x), x.stride(0), _dptr(y), y.stride(0),
+                                                _dptr(row_map), x.shape[0], sh.ctypes.data, buf, len(buf)), buf)
+            return
         _check(L.lib().cvg_plan_gram(self._h, _dptr(x), x.stride(0), _dptr(y), y.stride(0),
                                      None if sh is None else sh.ctypes.data, buf, len(buf)), buf)
 
@@ -169,23 +177,44 @@ def shard_rows(n: int, rank: int, world: int):
     return min(n, rank * s), min(n, (rank + 1) * s)
 
 
+def fold_owners(p: int, world: int):
+    """Rank owning each fold (0-based) when every rank owns whole folds (p >= world), else None."""
+    if p < world:
+        return None
+    own = np.empty(p, np.int64)
+    for r in range(world):
+        b, e = fold_range(p, r, world)
+        own[b:e] = r
+    return own
+
+
 def run_all_folds_sharded(x_shard, y_shard, labels, p: int, cfgs, n: int, group=None, plan=None,
-                          plan_factory=None, device=None, out_host=None, gather: Optional[bool] = None):
+                          plan_factory=None, device=None, out_host=None, gather: Optional[bool] = None,
+                          exchange: str = "auto"):
     """Multi-GPU entry point from HOST memory (the e2e path at N GPUs).
 
     This rank holds rows ``shard_rows(n, rank, world)`` of x | y in host memory
     (pinned for full PCIe speed) and all n labels.  Each rank copies only its
-    shard over its own PCIe link, the shards are all-gathered over NVLink
-    (NCCL; list form on gloo) into the full device-resident x | y, and the run
-    continues exactly as ``run_all_folds_device``: canonical fold range, one
-    partial all-gather, the owned folds' epilogue — so outputs are bit-identical
-    to one GPU.  Returns (plan, outputs) with the owned folds' outputs copied to
-    host tensors (``out_host`` reused when given).  ``gather`` forces (or skips)
-    the row all-gather; default: only when world > 1.
+    shard over its own PCIe link; the rows then move over NVLink:
+
+    * ``alltoall`` (default when every rank owns whole folds, p >= world): each
+      row goes only to the rank that owns its fold (one all_to_all per matrix,
+      rows stably bucketed by owner, so each owner receives its folds' rows in
+      original order); the plan reads the compacted rows through a row map
+      (cvg_plan_gram_mapped).  Row 0 (the shift) is broadcast from rank 0.
+    * ``allgather`` (p < world, shared folds): every rank receives every row.
+
+    Either way the canonical fold-range run follows (one partial all-gather,
+    the owned folds' epilogue), bit-identical to one GPU.  Returns (plan,
+    outputs) with the owned folds' outputs copied to host tensors (``out_host``
+    reused when given).  ``gather`` forces (or skips) the row exchange;
+    default: only when world > 1.
     """
     import torch
     import torch.distributed as dist
 
+    cfgs = [_cfg(c) for c in cfgs]
+    masks = [c.mask for c in cfgs]
     distributed = dist.is_available() and dist.is_initialized()
     world = dist.get_world_size(group) if distributed else 1
     rank = dist.get_rank(group) if distributed else 0
@@ -196,27 +225,70 @@ def run_all_folds_sharded(x_shard, y_shard, labels, p: int, cfgs, n: int, group=
                                              if torch.cuda.is_available() else torch.device("cpu"))
     k, m = x_shard.shape[1], y_shard.shape[1]
     s = -(-n // world)
-    mine_x = torch.zeros((s, k), dtype=x_shard.dtype, device=dev)
-    mine_y = torch.zeros((s, m), dtype=y_shard.dtype, device=dev)
-    mine_x[: hi - lo].copy_(x_shard, non_blocking=True)
-    mine_y[: hi - lo].copy_(y_shard, non_blocking=True)
     d_labels = labels.to(dev, non_blocking=True)
-    if (world > 1) if gather is None else (gather and distributed):
-        if dist.get_backend(group) == "nccl":
-            full_x = torch.empty((world * s, k), dtype=x_shard.dtype, device=dev)
-            full_y = torch.empty((world * s, m), dtype=y_shard.dtype, device=dev)
-            dist.all_gather_into_tensor(full_x, mine_x, group=group)
-            dist.all_gather_into_tensor(full_y, mine_y, group=group)
-        else:
-            px = [torch.empty_like(mine_x) for _ in range(world)]
-            py = [torch.empty_like(mine_y) for _ in range(world)]
-            dist.all_gather(px, mine_x, group=group)
-            dist.all_gather(py, mine_y, group=group)
-            full_x, full_y = torch.cat(px), torch.cat(py)
-        x, y = full_x[:n], full_y[:n]
+    do_exchange = (world > 1) if gather is None else (gather and distributed)
+    owners = fold_owners(p, world) if do_exchange else None
+    if exchange == "auto":
+        exchange = "alltoall" if owners is not None else "allgather"
+    if do_exchange and exchange == "alltoall" and owners is not None:
+        mine_x = x_shard.to(dev, non_blocking=True)
+        mine_y = y_shard.to(dev, non_blocking=True)
+        lut = torch.from_numpy(owners).to(dev)
+        lab0 = (d_labels.long() - 1).clamp(0, p - 1)  # out-of-range labels: the plan's bind reports them
+        dest = lut[lab0[lo:hi]]
+        dest_sorted, perm = torch.sort(dest, stable=True)
+        send_counts = torch.bincount(dest_sorted, minlength=world)
+        recv_counts = torch.empty_like(send_counts)
+        dist.all_to_all_single(recv_counts, send_counts, group=group)
+        sc, rc = send_counts.tolist(), recv_counts.tolist()
+        x = torch.empty((sum(rc), k), dtype=x_shard.dtype, device=dev)
+        y = torch.empty((sum(rc), m), dtype=y_shard.dtype, device=dev)
+        dist.all_to_all_single(x, mine_x.index_select(0, perm), output_split_sizes=rc, input_split_sizes=sc,
+                               group=group)
+        dist.all_to_all_single(y, mine_y.index_select(0, perm), output_split_sizes=rc, input_split_sizes=sc,
+                               group=group)
+        owned = lut[lab0] == rank
+        row_map = torch.where(owned, torch.cumsum(owned.long(), 0) - 1, torch.full_like(lab0, -1))
+        sh = torch.empty(k + m, dtype=torch.float64, device=dev)
+        if rank == 0:
+            sh.copy_(torch.cat([mine_x[0].double(), mine_y[0].double()]))
+        dist.broadcast(sh, src=0, group=group)
+        shift = sh.cpu().numpy()
+        if plan is None:
+            if plan_factory is not None:
+                fb, fe = fold_range(p, rank, world)
+                plan = plan_factory(n, k, m, p, fb, fe)
+            else:
+                plan = DevicePlan(n, k, m, p, dtype="f32" if x.dtype == torch.float32 else "f64", rank=rank,
+                                  world=world)
+        plan.bind_labels(d_labels, require_scalable=any(c.any_scale() for c in cfgs))
+        if (plan.fold_begin, plan.fold_end) != fold_range(p, rank, world):
+            raise RuntimeError("rank plan does not own its canonical fold range")
+        plan.gram(x, y, shift, row_map=row_map)
+        mine = torch.empty(plan.partial_count, dtype=torch.float64, device=dev)
+        plan.partial_into(mine)
+        out = plan.finish(masks, exchange_partials(mine, world, group), world)
     else:
-        x, y = mine_x[:n], mine_y[:n]
-    plan, out = run_all_folds_device(x, y, d_labels, p, cfgs, group=group, plan=plan, plan_factory=plan_factory)
+        mine_x = torch.zeros((s, k), dtype=x_shard.dtype, device=dev)
+        mine_y = torch.zeros((s, m), dtype=y_shard.dtype, device=dev)
+        mine_x[: hi - lo].copy_(x_shard, non_blocking=True)
+        mine_y[: hi - lo].copy_(y_shard, non_blocking=True)
+        if do_exchange:
+            if dist.get_backend(group) == "nccl":
+                full_x = torch.empty((world * s, k), dtype=x_shard.dtype, device=dev)
+                full_y = torch.empty((world * s, m), dtype=y_shard.dtype, device=dev)
+                dist.all_gather_into_tensor(full_x, mine_x, group=group)
+                dist.all_gather_into_tensor(full_y, mine_y, group=group)
+            else:
+                px = [torch.empty_like(mine_x) for _ in range(world)]
+                py = [torch.empty_like(mine_y) for _ in range(world)]
+                dist.all_gather(px, mine_x, group=group)
+                dist.all_gather(py, mine_y, group=group)
+                full_x, full_y = torch.cat(px), torch.cat(py)
+            x, y = full_x[:n], full_y[:n]
+        else:
+            x, y = mine_x[:n], mine_y[:n]
+        plan, out = run_all_folds_device(x, y, d_labels, p, cfgs, group=group, plan=plan, plan_factory=plan_factory)
     if not isinstance(out, dict) or not all(hasattr(v, "to") for v in out.values()):
         return plan, out  # stand-in plans (CPU tests) return host arrays already
     if out_host is None:

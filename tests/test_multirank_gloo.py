@@ -40,8 +40,14 @@ class NumpyPlan:
     def bind_labels(self, labels, require_scalable):
         self.labels = labels.numpy()
 
-    def gram(self, x, y, shift):
+    def gram(self, x, y, shift, row_map=None):
         z = np.concatenate([x.numpy(), y.numpy()], axis=1)
+        if row_map is not None:  # compacted rows: rebuild the full row space (absent rows stay 0)
+            rm = row_map.numpy()
+            full = np.zeros((self.n, z.shape[1]))
+            full[rm >= 0] = z[rm[rm >= 0]]
+            assert np.all(rm[np.isin(self.labels, np.arange(self.fold_begin + 1, self.fold_end + 1))] >= 0)
+            z = full
         self.shift = z[0].copy() if shift is None else np.asarray(shift)
         z = z - self.shift
         z1 = np.concatenate([z, np.ones((z.shape[0], 1))], axis=1)
@@ -179,7 +185,7 @@ def _worker_sharded(rank, world, port, outdir, data):
     lo, hi = P.shard_rows(len(x), rank, world)
     pl, out = P.run_all_folds_sharded(torch.from_numpy(x[lo:hi]), torch.from_numpy(y[lo:hi]),
                                       torch.from_numpy(labels), p, [8, 0], n=len(x), plan_factory=NumpyPlan,
-                                      device=torch.device("cpu"))
+                                      device=torch.device("cpu"), exchange=os.environ.get("CVG_TEST_EXCHANGE", "auto"))
     np.savez(os.path.join(outdir, f"rank{rank}.npz"), fb=pl.fold_begin, fe=pl.fold_end,
              xtx=np.stack(out["xtx"]), xty=np.stack(out["xty"]))
     dist.barrier()
@@ -187,11 +193,13 @@ def _worker_sharded(rank, world, port, outdir, data):
 
 
 @pytest.mark.parametrize("world", [2, 3, 4])
-def test_row_sharded_host_ingest_matches_world1_bitwise(world, data):
+@pytest.mark.parametrize("exchange", ["alltoall", "allgather"])
+def test_row_sharded_host_ingest_matches_world1_bitwise(world, exchange, data, monkeypatch):
     """run_all_folds_sharded: each rank holds only rows shard_rows(n, r, G) on
-    the host; shards are all-gathered (gloo list form here, NCCL on GPUs) and
-    the fold-range run proceeds as usual: same folds, same bits as one rank
-    (world 3 leaves a short last shard with padding rows)."""
+    the host.  alltoall: rows go only to their fold's owner and the plan reads
+    them through a row map; allgather: every rank gets every row.  Either way:
+    same folds, same bits as one rank (world 3 leaves a short last shard)."""
+    monkeypatch.setenv("CVG_TEST_EXCHANGE", exchange)
     single = _run(1, data)[0]
     with tempfile.TemporaryDirectory() as d:
         mp.spawn(_worker_sharded, args=(world, _free_port(), d, data), nprocs=world, join=True)
