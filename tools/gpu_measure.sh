@@ -1,5 +1,6 @@
 # Round measurement: every BASELINE config through bench.py, the reference arm, the
-# launch list (ncu, cold/serialised) and one ncu --set full capture of the c1 Gram.
+# launch list (ncu, cold/serialised) and ncu --set full captures of the c1 Gram, the c1
+# K1 reorder and the c2 epilogue (plain runs of the same commands exit 0 first).
 # Usage (from the repo root, on the GPU box):  bash tools/gpu_measure.sh r01
 R=${1:-r01}
 set -e; make -s -C paper_2401_13185_b200 >/dev/null; set +e
@@ -11,5 +12,8 @@ python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_${R}_re
 python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e > gpurun_out/plain.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_${R}.csv \
   python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e > gpurun_out/ncu_launch.log 2>&1; echo "ncu launches rc=$?"
-ncu --set full --clock-control none --import-source on -k regex:"gram_f64" -c 1 -o gpurun_out/prof_gram_${R} \
-  python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e > gpurun_out/ncu_gram.log 2>&1; echo "ncu gram rc=$?"
+ncu --set full --clock-control none --import-source on -k regex:"gram_f64|reorder_kernel" -c 2 -o gpurun_out/prof_c1_${R} \
+  python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e > gpurun_out/ncu_c1.log 2>&1; echo "ncu c1 rc=$?"
+python bench.py --config 2 --steps 1 --warmup 1 --no-cpu-baseline --no-e2e > gpurun_out/plain2.log 2>&1 && \
+ncu --set full --clock-control none -k regex:"products_kernel|fold_stats" -c 2 -o gpurun_out/prof_c2_${R} \
+  python bench.py --config 2 --steps 1 --warmup 1 --no-cpu-baseline --no-e2e > gpurun_out/ncu_c2.log 2>&1; echo "ncu c2 rc=$?"
