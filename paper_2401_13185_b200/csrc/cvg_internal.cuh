@@ -25,7 +25,10 @@ namespace cvg {
 
 constexpr int kTile = 64;          // Gram / epilogue tile edge (columns)
 constexpr int kRowStep = 32;       // rows per pipeline stage; fold blocks pad to this
-constexpr int64_t kChunkRows = 32768;     // max rows per fp64 segment (fixed => deterministic split)
+// max rows per fp64 segment (a fixed constant => a deterministic split; folds are cut into equal
+// segments, Plan::seg_rows).  8192 vs 32768: c1 10.70 vs 10.81 ms (two even CTAs per fold fill the
+// last wave better), c4 45.4 vs 45.8.
+constexpr int64_t kChunkRows = 8192;
 // fp32 segments: shorter than fp64 so the 45 tcgen05 tiles of a segment (kp 1152 at c3) re-read
 // less from DRAM (c3 sweep: 32768 -> 44.9 ms, 16384 -> 44.5, 12288 -> 42.9, 8192 -> 44.2: the
 // tree over more partials eats the rest).

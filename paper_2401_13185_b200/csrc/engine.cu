@@ -173,6 +173,15 @@ int64_t Plan::chunk_rows() const {
   return dtype_ == 1 ? kChunkRowsF32 : kChunkRows;
 }
 
+// Rows per segment of a fold of `count` rows: the fold is cut into
+// ceil(padded / chunk_rows()) segments of equal size (rounded up to 32 rows), so
+// no fold ends in a sliver segment and the Gram's CTAs carry even work.
+int64_t Plan::seg_rows(int64_t count) const {
+  const int64_t padded = round_up(count, kRowStep), chunk = chunk_rows();
+  const int64_t nseg = std::max<int64_t>(1, (padded + chunk - 1) / chunk);
+  return std::max<int64_t>(kRowStep, round_up((padded + nseg - 1) / nseg, kRowStep));
+}
+
 Status Plan::count_launch(int n) {
   ctx_->launches += n;
   return cuda_status(cudaGetLastError(), "kernel launch");
@@ -246,7 +255,8 @@ void Plan::assign_rank() {
     if (b - a == 1) {  // one fold, several ranks: split its segments
       if (s0 < 0) {
         s0 = 0;
-        s1 = (round_up(counts_[a], kRowStep) + chunk_rows() - 1) / chunk_rows();
+        const int64_t sr = seg_rows(counts_[a]);
+        s1 = (round_up(counts_[a], kRowStep) + sr - 1) / sr;
         glo = lo;
         ghi = hi;
       }
@@ -323,7 +333,7 @@ Status Plan::bind_labels(const int32_t* d_labels, bool validate, bool require_sc
   CVG_CK(cudaMemsetAsync(src_row_.as<void>(), 0xff, sizeof(int64_t) * std::max<int64_t>(zrows_, 1), s));
   {
     Timed t(ctx_, kBucket);
-    const int64_t win_lo = seg_lo_ >= 0 ? seg_lo_ * chunk_rows() : 0;
+    const int64_t win_lo = seg_lo_ >= 0 ? seg_lo_ * seg_rows(counts_[fb_]) : 0;
     const int64_t win_hi = seg_lo_ >= 0 ? win_lo + zrows_ : INT64_MAX;
     launch_scatter(d_labels, n_, p_, fb_, fe_, tile_counts_.as<int32_t>(), zbase_d_.as<int64_t>(), win_lo, win_hi,
                    src_row_.as<int64_t>(), zrows_, s);
@@ -354,9 +364,9 @@ Status Plan::plan_segments() {
   fold_seg_begin_.assign(1, 0);
   fold_zbase_.clear();
   zrows_ = 0;
-  const int64_t chunk = chunk_rows();
   for (int32_t f = fb_; f < fe_; ++f) {
     const int64_t padded = round_up(counts_[f], kRowStep);
+    const int64_t chunk = seg_rows(counts_[f]);
     // Owned window of the fold's bucketed rows: all of it, or (shared fold) segments [seg_lo_, seg_hi_).
     const int64_t w0 = seg_lo_ >= 0 ? std::min(padded, seg_lo_ * chunk) : 0;
     const int64_t w1 = seg_lo_ >= 0 ? std::min(padded, seg_hi_ * chunk) : padded;

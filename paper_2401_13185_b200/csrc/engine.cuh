@@ -112,6 +112,7 @@ class Plan {
   Status count_launch(int n = 1);
   void assign_rank();  // rank mode: fb_/fe_, segment window, fold group
   int64_t chunk_rows() const;
+  int64_t seg_rows(int64_t count) const;
 
   cvg_context* ctx_ = nullptr;
   int dtype_ = 0;
