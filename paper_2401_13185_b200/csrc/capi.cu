@@ -538,6 +538,8 @@ void cvg_plan_destroy(cvg_plan* plan) {
 int cvg_plan_bind_labels(cvg_plan* plan, const int32_t* d_labels, int require_scalable, char* err, size_t errlen) {
   return guarded(err, errlen, [&]() -> Status {
     if (!plan) return Status::Err(CVG_E_INVALID_ARG, "null plan");
+    Status dev = cvg::cuda_status(cudaSetDevice(plan->plan.ctx()->device), "cudaSetDevice");
+    if (!dev.ok()) return dev;
     return plan->plan.bind_labels(d_labels, true, require_scalable != 0);
   });
 }
@@ -546,6 +548,8 @@ int cvg_plan_gram(cvg_plan* plan, const void* d_x, int64_t ldx, const void* d_y,
                   char* err, size_t errlen) {
   return guarded(err, errlen, [&]() -> Status {
     if (!plan) return Status::Err(CVG_E_INVALID_ARG, "null plan");
+    Status dev = cvg::cuda_status(cudaSetDevice(plan->plan.ctx()->device), "cudaSetDevice");
+    if (!dev.ok()) return dev;
     return plan->plan.gram(d_x, ldx, d_y, ldy, shift, nullptr);
   });
 }
@@ -554,6 +558,8 @@ int cvg_plan_gram_mapped(cvg_plan* plan, const void* d_x, int64_t ldx, const voi
                          const int64_t* d_row_map, int64_t n_compact, const double* shift, char* err, size_t errlen) {
   return guarded(err, errlen, [&]() -> Status {
     if (!plan || !d_row_map) return Status::Err(CVG_E_INVALID_ARG, "null plan or row map");
+    Status dev = cvg::cuda_status(cudaSetDevice(plan->plan.ctx()->device), "cudaSetDevice");
+    if (!dev.ok()) return dev;
     if (!shift) return Status::Err(CVG_E_INVALID_ARG, "cvg_plan_gram_mapped needs an explicit shift");
     if (n_compact < 0) return Status::Err(CVG_E_INVALID_ARG, "negative compact row count");
     return plan->plan.gram(d_x, ldx, d_y, ldy, shift, nullptr, d_row_map, n_compact);
@@ -564,6 +570,7 @@ int cvg_plan_partial(cvg_plan* plan, double* d_dst, int64_t* count) {
   if (!plan || !count) return CVG_E_INVALID_ARG;
   *count = plan->plan.partial_count();
   if (!d_dst) return CVG_OK;
+  if (cudaSetDevice(plan->plan.ctx()->device) != cudaSuccess) return CVG_E_CUDA;
   const cudaError_t e = cudaMemcpyAsync(d_dst, plan->plan.local(), sizeof(double) * (*count),
                                         cudaMemcpyDeviceToDevice, plan->plan.ctx()->stream);
   return e == cudaSuccess ? CVG_OK : CVG_E_CUDA;
@@ -574,6 +581,8 @@ int cvg_plan_finish(cvg_plan* plan, const double* d_rank_partials, int32_t n_ran
                     double* d_std_x, double* d_std_y, char* err, size_t errlen) {
   return guarded(err, errlen, [&]() -> Status {
     if (!plan) return Status::Err(CVG_E_INVALID_ARG, "null plan");
+    Status dev = cvg::cuda_status(cudaSetDevice(plan->plan.ctx()->device), "cudaSetDevice");
+    if (!dev.ok()) return dev;
     for (int32_t c = 0; c < n_cfg; ++c)
       if (cfg_masks[c] > 15u) return Status::Err(CVG_E_INVALID_ARG, "configuration mask outside 0..15");
     return plan->plan.finish(d_rank_partials, n_ranks, nullptr, cfg_masks, n_cfg, d_xtx, d_xty, d_mean_x, d_mean_y,
@@ -638,6 +647,7 @@ int cvg_global_export(cvg_global* g, uint32_t cfg, double* xtx, double* xty, dou
                       size_t errlen) {
   return guarded(err, errlen, [&]() -> Status {
     if (!g) return Status::Err(CVG_E_INVALID_ARG, "null global");
+    if (cudaSetDevice(g->ctx->device) != cudaSuccess) return Status::Err(CVG_E_CUDA, "cudaSetDevice failed");
     const int64_t k = g->k, m = g->m, w = k + m;
     cudaStream_t st = g->ctx->stream;
     Status s;
@@ -670,6 +680,7 @@ int cvg_global_fold_products(cvg_global* g, const int64_t* v_rows, int64_t n_val
                              int64_t* n_train, char* err, size_t errlen) {
   return guarded(err, errlen, [&]() -> Status {
     if (!g) return Status::Err(CVG_E_INVALID_ARG, "null global");
+    if (cudaSetDevice(g->ctx->device) != cudaSuccess) return Status::Err(CVG_E_CUDA, "cudaSetDevice failed");
     if (cfg > 15u) return Status::Err(CVG_E_INVALID_ARG, "configuration mask outside 0..15");
     const int64_t n = g->n, k = g->k, m = g->m;
     // fast.hpp:78-82

@@ -159,11 +159,8 @@ __global__ void __launch_bounds__(NT, 2)
 
 void launch_gram_f64(const double* z, int64_t kp, int64_t zrows, const GramTask* segs, int64_t nseg,
                      const int2* tiles, int ntiles, double* part, cudaStream_t s) {
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(gram_f64_kernel<KC, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
-    attr_set = true;
-  }
+  // per device (a process may drive several GPUs), so set it on every launch: a host-side call
+  cudaFuncSetAttribute(gram_f64_kernel<KC, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
   const int64_t blocks = nseg * (int64_t)ntiles;
   if (blocks <= 0) return;
   gram_f64_kernel<KC, STAGES><<<(unsigned)blocks, NT, kSmemBytes, s>>>(z, kp, zrows, segs, nseg, tiles, ntiles,
