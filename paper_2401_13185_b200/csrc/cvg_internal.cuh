@@ -98,9 +98,12 @@ void launch_gram_f64(const double* z, int64_t kp, int64_t zrows, const GramTask*
 
 // K4: fixed-order (midpoint-tree) sums of kp x kp matrices over upper tiles,
 // one launch per tree level.  d = a + b; b == null copies a; a == null zeroes d.
+// One node of a midpoint tree whose children are leaves or leaf pairs, fused:
+//   L = in[1] ? in[0] + in[1] : in[0];  R = in[3] ? in[2] + in[3] : in[2];
+//   d = in[2] ? L + R : L   (all null: d = 0)
+// -- the same additions, in the same order, as the unfused binary tree.
 struct PairOp {
-  const double* a;
-  const double* b;
+  const double* in[4];
   double* d;
 };
 void launch_pair_sums(const PairOp* ops, int nops, int64_t kp, const int2* tiles, int ntiles, cudaStream_t s);

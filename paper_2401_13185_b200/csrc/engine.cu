@@ -113,16 +113,26 @@ const double* TreeProgram::emit(const std::vector<const double*>& leaves, int a,
   if ((int)by_depth.size() <= depth) by_depth.resize(depth + 1);
   if (b - a <= 1 && !root_dst) return leaves[a];  // interior leaf: read in place
   double* out = root_dst ? root_dst : scratch_.as<double>() + (next_slot_++) * kp * kp;
-  if (b - a == 0) {
-    by_depth[depth].push_back(PairOp{nullptr, nullptr, out});
-  } else if (b - a == 1) {
-    by_depth[depth].push_back(PairOp{leaves[a], nullptr, out});
-  } else {
+  PairOp op{{nullptr, nullptr, nullptr, nullptr}, out};
+  if (b - a == 1) {
+    op.in[0] = leaves[a];
+  } else if (b - a >= 2) {
+    // S(a,b) = S(a,mid) + S(mid,b); a child of <= 2 leaves is folded into this op
     const int mid = a + (b - a) / 2;
-    const double* l = emit(leaves, a, mid, depth + 1, nullptr, by_depth, kp);
-    const double* r = emit(leaves, mid, b, depth + 1, nullptr, by_depth, kp);
-    by_depth[depth].push_back(PairOp{l, r, out});
+    auto child = [&](int lo, int hi, int slot) {
+      if (hi - lo == 1) {
+        op.in[slot] = leaves[lo];
+      } else if (hi - lo == 2) {
+        op.in[slot] = leaves[lo];  // S(lo, lo+2) = leaf lo + leaf lo+1
+        op.in[slot + 1] = leaves[lo + 1];
+      } else {
+        op.in[slot] = emit(leaves, lo, hi, depth + 1, nullptr, by_depth, kp);
+      }
+    };
+    child(a, mid, 0);
+    child(mid, b, 2);
   }
+  by_depth[depth].push_back(op);
   return out;
 }
 

@@ -10,10 +10,12 @@
 // tree's top levels.  This keeps the reference's bitwise thread-count
 // invariance (threading.hpp:8-10, test_fast.cpp:217-229).  No float atomics.
 //
-// The host flattens the trees into levels of independent pairwise adds
-// (TreeProgram, engine.cu); each level is one launch over (tile, op) with
-// 16-byte loads, so a level streams at HBM speed instead of walking the tree
-// per element.  Only the tiles the Gram wrote are touched.
+// The host flattens the trees into levels of independent ops (TreeProgram,
+// engine.cu); a node whose children are leaves or leaf pairs is ONE op,
+// ((a + b) + (c + d)) evaluated in registers -- the same additions in the same
+// order, so two tree levels cost one pass (intermediate nodes are not written
+// and re-read).  Each level is one launch over (tile, op) with 16-byte loads,
+// streaming at HBM speed.  Only the tiles the Gram wrote are touched.
 #include "cvg_internal.cuh"
 
 namespace cvg {
@@ -23,19 +25,29 @@ __global__ void __launch_bounds__(256) pair_sum_kernel(const PairOp* __restrict_
                                                        const int2* __restrict__ tiles) {
   const int2 tile = tiles[blockIdx.x];
   const PairOp op = ops[blockIdx.y];
-  CVG_DCHECK(op.d != nullptr && (op.a != nullptr || op.b == nullptr));
+  CVG_DCHECK(op.d != nullptr && (op.in[0] != nullptr || op.in[2] == nullptr));
   CVG_DCHECK(tile.x >= 0 && tile.x <= tile.y && (int64_t)(tile.y + 1) * kTile <= kp);
   const int c2 = (threadIdx.x & 31) * 2;  // column pair within the tile
 #pragma unroll 4
   for (int r = threadIdx.x >> 5; r < kTile; r += 8) {
     const int64_t off = ((int64_t)tile.x * kTile + r) * kp + (int64_t)tile.y * kTile + c2;
     double2 v = make_double2(0.0, 0.0);
-    if (op.a) {
-      v = *reinterpret_cast<const double2*>(op.a + off);
-      if (op.b) {
-        const double2 w = *reinterpret_cast<const double2*>(op.b + off);
-        v.x = __dadd_rn(v.x, w.x);
-        v.y = __dadd_rn(v.y, w.y);
+    if (op.in[0]) {
+      v = *reinterpret_cast<const double2*>(op.in[0] + off);
+      if (op.in[1]) {
+        const double2 u = *reinterpret_cast<const double2*>(op.in[1] + off);
+        v.x = __dadd_rn(v.x, u.x);
+        v.y = __dadd_rn(v.y, u.y);
+      }
+      if (op.in[2]) {
+        double2 r = *reinterpret_cast<const double2*>(op.in[2] + off);
+        if (op.in[3]) {
+          const double2 u = *reinterpret_cast<const double2*>(op.in[3] + off);
+          r.x = __dadd_rn(r.x, u.x);
+          r.y = __dadd_rn(r.y, u.y);
+        }
+        v.x = __dadd_rn(v.x, r.x);
+        v.y = __dadd_rn(v.y, r.y);
       }
     }
     *reinterpret_cast<double2*>(op.d + off) = v;
