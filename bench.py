@@ -104,6 +104,15 @@ class ClockSampler:
                 self.proc.wait(timeout=5)
             except Exception:
                 self.proc.kill()
+        self.after = False
+        if not self.lines:  # run shorter than nvidia-smi's start-up: one sample right after it
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=30)
+                self.lines = [ln.strip() for ln in out.stdout.splitlines() if ln.strip()]
+                self.after = bool(self.lines)
+            except Exception:
+                pass
 
     def summary(self):
         sm, mx, reasons = [], 0.0, set()
@@ -120,8 +129,11 @@ class ClockSampler:
             for nm, v in zip(names, parts[3:7]):
                 if v.lower().startswith("active"):
                     reasons.add(nm)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        out = {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+               "reasons": sorted(reasons), "samples": len(sm)}
+        if getattr(self, "after", False):
+            out["note"] = "timed region shorter than the sampler's start-up: sampled right after it"
+        return out
 
 
 # ------------------------------------------------------------- reference arm
