@@ -123,6 +123,15 @@ int cvg_plan_gram(cvg_plan* plan, const void* d_x, int64_t ldx, const void* d_y,
  * bit, as cvg_plan_gram over the full x / y. */
 int cvg_plan_gram_mapped(cvg_plan* plan, const void* d_x, int64_t ldx, const void* d_y, int64_t ldy,
                          const int64_t* d_row_map, int64_t n_compact, const double* shift, char* err, size_t errlen);
+/* cvg_plan_finish for the emitted folds [fold_lo, fold_hi) only (0-based fold ids
+ * inside [fold_begin, fold_end)); outputs are packed for that range
+ * ([n_cfg][fold_hi - fold_lo][k][k] ...), so P x K x K outputs can be streamed
+ * through bounded buffers (leave-one-out at scale).  Same values as the
+ * corresponding slice of cvg_plan_finish. */
+int cvg_plan_finish_range(cvg_plan* plan, const double* d_rank_partials, int32_t n_ranks, const uint32_t* cfg_masks,
+                          int32_t n_cfg, int32_t fold_lo, int32_t fold_hi, double* d_xtx, double* d_xty,
+                          double* d_mean_x, double* d_mean_y, double* d_std_x, double* d_std_y, char* err,
+                          size_t errlen);
 /* This plan's contribution to the cross-rank fold sum (its node of the fold
  * tree): *count doubles, copied into device buffer d_dst when it is non-NULL. */
 int cvg_plan_partial(cvg_plan* plan, double* d_dst, int64_t* count);

@@ -590,6 +590,24 @@ int cvg_plan_finish(cvg_plan* plan, const double* d_rank_partials, int32_t n_ran
   });
 }
 
+int cvg_plan_finish_range(cvg_plan* plan, const double* d_rank_partials, int32_t n_ranks, const uint32_t* cfg_masks,
+                          int32_t n_cfg, int32_t fold_lo, int32_t fold_hi, double* d_xtx, double* d_xty,
+                          double* d_mean_x, double* d_mean_y, double* d_std_x, double* d_std_y, char* err,
+                          size_t errlen) {
+  return guarded(err, errlen, [&]() -> Status {
+    if (!plan) return Status::Err(CVG_E_INVALID_ARG, "null plan");
+    Status dev = cvg::cuda_status(cudaSetDevice(plan->plan.ctx()->device), "cudaSetDevice");
+    if (!dev.ok()) return dev;
+    for (int32_t c = 0; c < n_cfg; ++c)
+      if (cfg_masks[c] > 15u) return Status::Err(CVG_E_INVALID_ARG, "configuration mask outside 0..15");
+    const int32_t fb = plan->plan.fold_begin(), fe = plan->plan.fold_end();
+    if (fold_lo < fb || fold_hi > fe || fold_lo > fold_hi)
+      return Status::Err(CVG_E_INVALID_ARG, "fold range outside the plan's emitted folds");
+    return plan->plan.finish(d_rank_partials, n_ranks, nullptr, cfg_masks, n_cfg, d_xtx, d_xty, d_mean_x, d_mean_y,
+                             d_std_x, d_std_y, fold_lo - fb, fold_hi - fb);
+  });
+}
+
 int cvg_plan_fold_counts(const cvg_plan* plan, int64_t* counts) {
   if (!plan || !counts) return CVG_E_INVALID_ARG;
   const auto& c = plan->plan.counts();

@@ -114,12 +114,21 @@ struct FoldStatsDev {
   double* sT;   // [nfold][w] training column sums (shifted)
   double* sd;   // [nfold][w] training std (zero -> 1)
 };
+// Small-fold mode (every fold <= kSmallFoldRows rows, e.g. leave-one-out): no per-fold Gram partials; a fold's
+// Gram entries are formed in the epilogue from its rows of Z (z: zrows x kp, rows zbase[f] .. + n_val[f]).
+constexpr int kSmallFoldRows = 32;
+struct SmallFolds {
+  const double* z = nullptr;       // null: fold Grams come from foldG
+  const int64_t* zbase = nullptr;  // first Z row of each fold
+};
 void launch_fold_stats(const double* total, const double* const* foldG, const int64_t* n_val, int nfold, int64_t n,
                        int64_t k, int64_t m, int64_t kp, const double* shift, FoldStatsDev st, double* mean_x,
-                       double* mean_y, double* std_x, double* std_y, int* nonfinite, cudaStream_t s);
+                       double* mean_y, double* std_x, double* std_y, int* nonfinite, cudaStream_t s,
+                       SmallFolds sf = SmallFolds());
 void launch_products(const double* total, const double* const* foldG, const int64_t* n_val, int nfold, int64_t n,
                      int64_t k, int64_t m, int64_t kp, const double* shift, FoldStatsDev st, const int2* tiles,
-                     int ntiles, const uint32_t* cfgs, int ncfg, double* xtx, double* xty, cudaStream_t s);
+                     int ntiles, const uint32_t* cfgs, int ncfg, double* xtx, double* xty, cudaStream_t s,
+                     SmallFolds sf = SmallFolds());
 void launch_unshift_global(const double* total, int64_t n, int64_t k, int64_t m, int64_t kp, const double* shift,
                            double* xtx, double* xty, double* sum, double* sumsq, double* mean, cudaStream_t s);
 void launch_training_mean(const double* g, const double* v, int64_t len, int64_t n, int64_t nv, double* out,

@@ -339,6 +339,12 @@ Status Plan::bind_labels(const int32_t* d_labels, bool validate, bool require_sc
                                     std::to_string(n_ - counts_[f]) + " rows; scaling needs at least 2");
   }
   if (rank_mode_) assign_rank();
+  small_ = false;
+  if (dtype_ == 0 && !rank_mode_ && fb_ == 0 && fe_ == p_ && small_folds_enabled()) {
+    int64_t mx = 0;
+    for (int32_t f = 0; f < p_; ++f) mx = std::max(mx, counts_[f]);
+    small_ = mx <= kSmallFoldRows;
+  }
   CVG_TRY(plan_segments());
   CVG_CK(cudaMemsetAsync(src_row_.as<void>(), 0xff, sizeof(int64_t) * std::max<int64_t>(zrows_, 1), s));
   {
@@ -353,8 +359,18 @@ Status Plan::bind_labels(const int32_t* d_labels, bool validate, bool require_sc
   return Status::Ok();
 }
 
+// CVG_SMALL_FOLDS=0 keeps per-fold Gram partials even when every fold is tiny (A/B tests).
+bool Plan::small_folds_enabled() {
+  static const bool on = [] {
+    const char* v = std::getenv("CVG_SMALL_FOLDS");
+    return !(v && v[0] == '0');
+  }();
+  return on;
+}
+
 Status Plan::bind_rows(const int64_t* rows, int64_t nrows, int64_t n_src) {
   if (p_ != 1 || fb_ != 0 || fe_ != 1) return Status::Err(4, "bind_rows needs a single-fold plan");
+  small_ = false;
   src_n_ = n_src < 0 ? n_ : n_src;
   for (int64_t i = 0; i < nrows; ++i)
     if (rows[i] < 0 || rows[i] >= src_n_) return Status::Err(4, "bind_rows: row index outside the source matrix");
@@ -374,7 +390,22 @@ Status Plan::plan_segments() {
   fold_seg_begin_.assign(1, 0);
   fold_zbase_.clear();
   zrows_ = 0;
-  for (int32_t f = fb_; f < fe_; ++f) {
+  if (small_) {
+    // Small-fold mode: folds packed back to back (no per-fold padding); segments are
+    // equal fixed-size row chunks of Z regardless of fold boundaries (they only feed
+    // the whole-data Gram); each fold's own Gram is formed in the epilogue.
+    int64_t rows = 0;
+    for (int32_t f = fb_; f < fe_; ++f) {
+      fold_zbase_.push_back(rows);
+      rows += counts_[f];
+      fold_seg_begin_.push_back(0);
+    }
+    zrows_ = round_up(std::max<int64_t>(rows, 1), kRowStep);
+    const int64_t chunk = seg_rows(zrows_);
+    for (int64_t off = 0; off < zrows_; off += chunk)
+      segs_.push_back(GramTask{off, std::min<int64_t>(chunk, zrows_ - off)});
+  }
+  for (int32_t f = fb_; f < fe_ && !small_; ++f) {
     const int64_t padded = round_up(counts_[f], kRowStep);
     const int64_t chunk = seg_rows(counts_[f]);
     // Owned window of the fold's bucketed rows: all of it, or (shared fold) segments [seg_lo_, seg_hi_).
@@ -408,6 +439,19 @@ Status Plan::plan_segments() {
   if (!segs_.empty())
     CVG_CK(cudaMemcpyAsync(segs_d_.as<GramTask>(), segs_.data(), sizeof(GramTask) * segs_.size(),
                            cudaMemcpyHostToDevice, s));
+  if (small_) {  // no per-fold Grams: the plan's node is the tree over all chunks
+    TreeGroup g{{}, local_.as<double>()};
+    for (size_t sgi = 0; sgi < segs_.size(); ++sgi) g.leaves.push_back(part_.as<double>() + (int64_t)sgi * kp_ * kp_);
+    CVG_TRY(fold_tree_.build({}, kp_, s));
+    CVG_TRY(local_tree_.build({g}, kp_, s));
+    fold_ptrs_.assign(nown, nullptr);
+    CVG_TRY(foldptr_d_.ensure(sizeof(void*) * std::max(nown, 1)));
+    if (nown > 0)
+      CVG_CK(cudaMemcpyAsync(foldptr_d_.as<void>(), fold_ptrs_.data(), sizeof(void*) * nown,
+                             cudaMemcpyHostToDevice, s));
+    CVG_CK(cudaStreamSynchronize(s));
+    return Status::Ok();
+  }
   // Fold Gram pointers: the segment partial itself for single-segment folds,
   // otherwise a fixed-order sum of its segments into foldbuf (K4, phase 1).
   int nmulti = 0;
@@ -632,7 +676,7 @@ Status Plan::gram_host(const void* h_x, const void* h_y, void* d_x, void* d_y, c
 
 Status Plan::finish(const double* d_rank_partials, int32_t n_ranks, const double* total_override,
                     const uint32_t* cfgs, int32_t ncfg, double* d_xtx, double* d_xty, double* d_mean_x,
-                    double* d_mean_y, double* d_std_x, double* d_std_y) {
+                    double* d_mean_y, double* d_std_x, double* d_std_y, int32_t range_lo, int32_t range_hi) {
   if (!grammed_) return Status::Err(4, "finish called before gram");
   cudaStream_t s = ctx_->stream;
   const double* total = nullptr;
@@ -659,7 +703,12 @@ Status Plan::finish(const double* d_rank_partials, int32_t n_ranks, const double
     CVG_TRY(group_tree_.build({g}, kp_, s));
     CVG_TRY(group_tree_.run(ctx_, tiles_d_.as<int2>(), (int)tiles_.size(), kp_));
   }
-  const int nown = this->nown();
+  // Emitted folds [lo, hi) of the owned ones (default: all); outputs are packed for that range, so a
+  // caller can stream huge P (e.g. leave-one-out) through bounded buffers.
+  const int32_t lo = range_lo < 0 ? 0 : range_lo;
+  const int32_t hi = range_hi < 0 ? this->nown() : range_hi;
+  if (lo > hi || hi > this->nown()) return Status::Err(4, "fold range outside the plan's emitted folds");
+  const int nown = hi - lo;
   if (nown == 0) {
     CVG_CK(cudaStreamSynchronize(s));
     return Status::Ok();
@@ -668,10 +717,14 @@ Status Plan::finish(const double* d_rank_partials, int32_t n_ranks, const double
   CVG_TRY(st_sT_.ensure(sizeof(double) * nown * w_));
   CVG_TRY(st_sd_.ensure(sizeof(double) * nown * w_));
   FoldStatsDev st{st_mz_.as<double>(), st_sT_.as<double>(), st_sd_.as<double>()};
+  const double* const* fptr = foldptr_d_.as<const double*>() + lo;
+  const int64_t* nval = nval_d_.as<int64_t>() + lo;
+  SmallFolds sf = small_folds();
+  if (sf.zbase) sf.zbase += lo;
   {
     Timed t(ctx_, kStats);
-    launch_fold_stats(total, foldptr_d_.as<const double*>(), nval_d_.as<int64_t>(), nown, n_, k_, m_, kp_,
-                      shift_.as<double>(), st, d_mean_x, d_mean_y, d_std_x, d_std_y, flag_.as<int>(), s);
+    launch_fold_stats(total, fptr, nval, nown, n_, k_, m_, kp_, shift_.as<double>(), st, d_mean_x, d_mean_y, d_std_x,
+                      d_std_y, flag_.as<int>(), s, sf);
   }
   CVG_TRY(count_launch());
   if (ncfg > 0) {
@@ -679,9 +732,8 @@ Status Plan::finish(const double* d_rank_partials, int32_t n_ranks, const double
     CVG_CK(cudaMemcpyAsync(cfg_d_.as<void>(), cfgs, sizeof(uint32_t) * ncfg, cudaMemcpyHostToDevice, s));
     {
       Timed t(ctx_, kProducts);
-      launch_products(total, foldptr_d_.as<const double*>(), nval_d_.as<int64_t>(), nown, n_, k_, m_, kp_,
-                      shift_.as<double>(), st, out_tiles_d_.as<int2>(), (int)out_tiles_.size(),
-                      cfg_d_.as<uint32_t>(), ncfg, d_xtx, d_xty, s);
+      launch_products(total, fptr, nval, nown, n_, k_, m_, kp_, shift_.as<double>(), st, out_tiles_d_.as<int2>(),
+                      (int)out_tiles_.size(), cfg_d_.as<uint32_t>(), ncfg, d_xtx, d_xty, s, sf);
     }
     CVG_TRY(count_launch());
   }

@@ -77,9 +77,10 @@ class Plan {
   // earlier slabs' K1 + Gram tiles run; bit-identical to gram().
   Status gram_host(const void* h_x, const void* h_y, void* d_x, void* d_y, const double* host_shift);
   // Cross-rank combine (optional) + K5 for the owned folds into device outputs.
+  // [range_lo, range_hi): emitted-fold subrange (default all), outputs packed for it.
   Status finish(const double* d_rank_partials, int32_t n_ranks, const double* total_override,
                 const uint32_t* cfgs, int32_t ncfg, double* d_xtx, double* d_xty, double* d_mean_x,
-                double* d_mean_y, double* d_std_x, double* d_std_y);
+                double* d_mean_y, double* d_std_x, double* d_std_y, int32_t range_lo = -1, int32_t range_hi = -1);
 
   // Baseline (direct) epilogue for a bind_rows plan: the bound rows ARE the
   // training set (no downdate): total = their Gram, fold Gram = 0, n_val = 0.
@@ -109,6 +110,15 @@ class Plan {
  private:
   Status plan_segments();
   Status gram_trees();
+  static bool small_folds_enabled();
+  SmallFolds small_folds() const {
+    SmallFolds sf;
+    if (small_) {
+      sf.z = z_.as<double>();
+      sf.zbase = zbase_d_.as<int64_t>();
+    }
+    return sf;
+  }
   Status count_launch(int n = 1);
   void assign_rank();  // rank mode: fb_/fe_, segment window, fold group
   int64_t chunk_rows() const;
@@ -125,6 +135,7 @@ class Plan {
   std::vector<int64_t> fold_zbase_;
   int64_t zrows_ = 0;
   int64_t src_n_ = 0;  // rows of the x / y the row map indexes (K1 bounds)
+  bool small_ = false;  // small-fold mode (every fold <= kSmallFoldRows rows; see plan_segments)
   bool bound_ = false, grammed_ = false;
   bool rank_mode_ = false, emits_ = true;
   int32_t rank_ = 0, world_ = 1;

@@ -125,6 +125,40 @@ class DevicePlan:
                                        buf, len(buf)), buf)
         return out
 
+    def finish_range(self, cfg_masks: Sequence[int], fold_lo: int, fold_hi: int, rank_partials=None,
+                     n_ranks: int = 1, out=None):
+        """finish() for emitted folds [fold_lo, fold_hi) only; outputs packed for the range."""
+        import torch
+
+        dev = torch.device("cuda", self.ctx.device)
+        masks = np.ascontiguousarray(cfg_masks, np.uint32)
+        nc, nf, k, m = masks.size, fold_hi - fold_lo, self.k, self.m
+        if out is None or out["xtx"].shape[1] != nf or out["xtx"].shape[0] != nc:
+            f64 = torch.float64
+            out = {"xtx": torch.empty((nc, nf, k, k), dtype=f64, device=dev),
+                   "xty": torch.empty((nc, nf, k, m), dtype=f64, device=dev),
+                   "mean_x": torch.empty((nf, k), dtype=f64, device=dev),
+                   "mean_y": torch.empty((nf, m), dtype=f64, device=dev),
+                   "std_x": torch.empty((nf, k), dtype=f64, device=dev),
+                   "std_y": torch.empty((nf, m), dtype=f64, device=dev)}
+        view = out
+        buf = L.err_buf()
+        _check(L.lib().cvg_plan_finish_range(self._h, _dptr(rank_partials), n_ranks, masks.ctypes.data, nc, fold_lo,
+                                             fold_hi, _dptr(view["xtx"]), _dptr(view["xty"]),
+                                             _dptr(view["mean_x"]), _dptr(view["mean_y"]), _dptr(view["std_x"]),
+                                             _dptr(view["std_y"]), buf, len(buf)), buf)
+        return view
+
+    def iter_folds(self, cfg_masks: Sequence[int], batch: int, rank_partials=None, n_ranks: int = 1):
+        """Stream the emitted folds in batches of `batch` (lazy per-fold generation:
+        leave-one-out-scale P without P x K x K of outputs in memory).  Yields
+        (fold_lo, fold_hi, outputs) with device tensors reused between batches."""
+        out = None
+        for lo in range(self.fold_begin, self.fold_end, batch):
+            hi = min(lo + batch, self.fold_end)
+            out = self.finish_range(cfg_masks, lo, hi, rank_partials, n_ranks, out)  # reallocated only if shorter
+            yield lo, hi, out
+
     def fold_counts(self) -> np.ndarray:
         c = np.empty(self.p, np.int64)
         L.lib().cvg_plan_fold_counts(self._h, c.ctypes.data)
