@@ -6,6 +6,10 @@
 // (partition.hpp:61-68) + parallel_for over fold_products (fast.hpp:73-130,
 // threading.hpp:12-26).  Here: bucket (device) -> K1 reorder/shift -> K2 fold
 // Gram -> K4 fold/total sums -> [cross-rank combine] -> K5 stats + products.
+// Variants: host inputs streamed by column slabs on a copy stream (gram_host),
+// compacted rows through a row map (multi-GPU all-to-all ingest), small-fold
+// mode (every fold <= 32 rows: no per-fold partials, fold Grams formed in K5),
+// and K5 over an emitted-fold subrange (streaming leave-one-out-scale P).
 #include <algorithm>
 #include <climits>
 #include <cstdlib>
