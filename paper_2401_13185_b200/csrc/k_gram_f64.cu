@@ -11,7 +11,9 @@
 //
 // Tensor path: sm_100 has no fp64 tcgen05 kind; `mma.sync.m8n8k4.f64` lowers to
 // SASS DMMA.8x8x4, measured at 37.1 TFLOP/s on this B200 (profiles/r01_fp64_peaks.txt).
-// CTA = 64x64 output tile, 8 warps (2 x 4), warp tile 32x16 = 4x2 DMMA tiles.
+// CTA = 64x64 output tile, 8 warps (2 x 4), warp tile 32x16 = 4x2 DMMA tiles;
+// a diagonal tile instead deals its 36 upper 8x8 blocks round-robin to the 8
+// warps (no DMMA below the diagonal: c1 Gram 8.81 -> 8.31 ms, c4 36.4 -> 32.8).
 // Operands: 32-row x 64-col slabs staged by cp.async (16 B) into a 3-stage ring
 // synchronised by mbarriers (see gram_f64_kernel);
 // the smem row pitch of 68 doubles makes the DMMA fragment loads conflict-free
@@ -57,6 +59,12 @@ __device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, uint32_t parity)
       : "memory");
 }
 
+// Diagonal tiles: the 36 upper 8x8 blocks (bi <= bj) of the 64x64 tile, dealt round-robin to the 8 warps
+// (5 or 4 each) so no DMMA is spent below the diagonal.  Packed as bi * 8 + bj.
+__constant__ unsigned char kDiagBlocks[40] = {
+    0,  1,  2,  3,  4,  5,  6,  7,  9,  10, 11, 12, 13, 14, 15, 18, 19, 20, 21, 22,
+    23, 27, 28, 29, 30, 31, 36, 37, 38, 39, 45, 46, 47, 54, 55, 63, 0,  0,  0,  0};
+
 // Grid order: segment-major, tile fastest, so the CTAs of one segment run
 // together and share its rows in L2 (ncu, c1: 4.9 GB DRAM for 4.1 GB of Z).
 // (Running every diagonal tile after all off-diagonal ones, to end on cheap
@@ -81,7 +89,15 @@ __global__ void __launch_bounds__(NT, 2)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t4 = lane & 3;
   const int wi = (warp >> 2) * 32, wj = (warp & 3) * 16;
-  const bool idle = diag && wi >= wj + 16;
+  // diagonal tiles: this warp's upper blocks b = warp, warp + 8, ... (< 36)
+  const int nblk = diag ? (warp < 4 ? 5 : 4) : 0;
+  int boff_a[5], boff_b[5];
+#pragma unroll
+  for (int u = 0; u < 5; ++u) {
+    const int code = kDiagBlocks[u < nblk ? warp + 8 * u : 0];
+    boff_a[u] = (code >> 3) * 8 + g;
+    boff_b[u] = (code & 7) * 8 + g;
+  }
   if (tid == 0) {
     for (int s = 0; s < STm; ++s) {
       asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_addr(&full[s])), "r"(NT));
@@ -116,9 +132,18 @@ __global__ void __launch_bounds__(NT, 2)
   for (int step = 0; step < nsteps; ++step) {
     const int buf = step % STm;
     mbar_wait_parity(&full[buf], (uint32_t)(step / STm) & 1u);
-    if (!idle) {
+    if (diag) {
       const double* sA = smem + buf * 2 * kSl;
-      const double* sB = diag ? sA : sA + kSl;
+#pragma unroll
+      for (int kk = 0; kk < KCm; kk += 4) {
+        const double* pr = sA + (kk + t4) * LDS;
+#pragma unroll
+        for (int u = 0; u < 5; ++u)
+          if (u < nblk) dmma(acc[u >> 1][u & 1], pr[boff_a[u]], pr[boff_b[u]]);
+      }
+    } else {
+      const double* sA = smem + buf * 2 * kSl;
+      const double* sB = sA + kSl;
 #pragma unroll
       for (int kk = 0; kk < KCm; kk += 4) {
         const double* pa = sA + (kk + t4) * LDS + wi + g;
@@ -145,6 +170,23 @@ __global__ void __launch_bounds__(NT, 2)
   }
 
   double* out = part + (int64_t)seg * kp * kp;
+  if (diag) {
+#pragma unroll
+    for (int u = 0; u < 5; ++u)
+      if (u < nblk) {
+        const int64_t row = (int64_t)ti * BT + boff_a[u];
+        const int64_t col = (int64_t)tj * BT + (boff_b[u] - g) + 2 * t4;
+        *reinterpret_cast<double2*>(out + row * kp + col) = make_double2(acc[u >> 1][u & 1][0], acc[u >> 1][u & 1][1]);
+      }
+    // strictly-lower blocks are never read downstream; zero them so every partial is fully defined
+    for (int lb = warp; lb < 64; lb += 8) {
+      const int bi = lb >> 3, bj = lb & 7;
+      if (bi <= bj) continue;
+      const int64_t row = (int64_t)ti * BT + bi * 8 + g, col = (int64_t)tj * BT + bj * 8 + 2 * t4;
+      *reinterpret_cast<double2*>(out + row * kp + col) = make_double2(0.0, 0.0);
+    }
+    return;
+  }
 #pragma unroll
   for (int mi = 0; mi < 4; ++mi)
 #pragma unroll

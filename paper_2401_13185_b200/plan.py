@@ -358,7 +358,10 @@ def gram_tiles(k: int, m: int, edge: int = 64):
 
 def executed_gram_flops(n: int, k: int, m: int, p: int, f32: bool = False) -> float:
     """Tensor-core flops the Gram kernel issues for n rows (fold padding ignored):
-    64x64 DMMA tiles for fp64; 128x128 tcgen05 tiles x 3 TF32 products for fp32."""
+    fp64: 64x64 DMMA tiles, diagonal tiles only their 36 upper 8x8 blocks;
+    fp32: 128x128 tcgen05 tiles x 3 TF32 products."""
     if f32:
         return 3 * 2.0 * len(gram_tiles(k, m, 128)) * 128 * 128 * n
-    return 2.0 * len(gram_tiles(k, m)) * 64 * 64 * n
+    tiles = gram_tiles(k, m)
+    n_diag = sum(1 for i, j in tiles if i == j)
+    return 2.0 * ((len(tiles) - n_diag) * 64 * 64 + n_diag * 36 * 64) * n
