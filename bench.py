@@ -431,8 +431,9 @@ def run_ours(args):
                      "algorithmic_flops_per_launch": gram_flops_per_launch,
                      "executed_tflops": round(executed, 3),
                      "executed_frac": round(executed / peak, 4),
-                     "note": "algorithmic flops = 2NK(K+M) (BASELINE metric); the kernel computes only the "
-                             "upper 64x64 tiles, so executed < algorithmic"},
+                     "note": "algorithmic flops = 2NK(K+M) (BASELINE metric); the fp64 kernel computes only the "
+                             "upper 64x64 tiles (diagonal tiles: their upper 8x8 blocks), the fp32 kernel the upper "
+                             "128x128 tiles x 3 TF32 products: executed_tflops counts what the tensor cores issue"},
         "kernels_ms_per_step": per_kernel,
         "hbm_rooflines": {
             "reorder": {"bytes": reorder_bytes, "achieved_gbs": round(reorder_bytes / (kms[1] / args.steps * 1e-3) / 1e9, 1)
