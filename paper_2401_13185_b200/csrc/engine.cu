@@ -78,6 +78,39 @@ Status cuda_status(cudaError_t e, const char* what) {
     if (!_s.ok()) return _s;   \
   } while (0)
 
+PinnedStage::~PinnedStage() {
+  if (pending_) cudaEventSynchronize(ev_);
+  if (ev_) cudaEventDestroy(ev_);
+  if (p_) cudaFreeHost(p_);
+}
+
+Status PinnedStage::upload(std::initializer_list<Part> parts, cudaStream_t s) {
+  size_t need = 0;
+  for (const Part& q : parts) need += (q.bytes + 15) & ~size_t(15);
+  if (pending_) {  // the previous upload must have left the buffer
+    CVG_CK(cudaEventSynchronize(ev_));
+    pending_ = false;
+  }
+  if (need > bytes_) {
+    if (p_) cudaFreeHost(p_);
+    p_ = nullptr;
+    bytes_ = 0;
+    CVG_CK(cudaHostAlloc(&p_, std::max<size_t>(need, 4096), cudaHostAllocDefault));
+    bytes_ = std::max<size_t>(need, 4096);
+  }
+  if (!ev_) CVG_CK(cudaEventCreateWithFlags(&ev_, cudaEventDisableTiming));
+  char* h = static_cast<char*>(p_);
+  for (const Part& q : parts) {
+    if (!q.bytes) continue;
+    std::memcpy(h, q.src, q.bytes);
+    CVG_CK(cudaMemcpyAsync(q.dst, h, q.bytes, cudaMemcpyHostToDevice, s));
+    h += (q.bytes + 15) & ~size_t(15);
+  }
+  CVG_CK(cudaEventRecord(ev_, s));
+  pending_ = true;
+  return Status::Ok();
+}
+
 Status DevBuf::ensure(size_t bytes) {
   if (bytes <= bytes_) return Status::Ok();
   release();
@@ -156,8 +189,7 @@ Status TreeProgram::build(const std::vector<TreeGroup>& groups, int64_t kp, cuda
   }
   CVG_TRY(ops_d_.ensure(sizeof(PairOp) * std::max<size_t>(flat_.size(), 1)));
   if (!flat_.empty())
-    CVG_CK(cudaMemcpyAsync(ops_d_.as<PairOp>(), flat_.data(), sizeof(PairOp) * flat_.size(), cudaMemcpyHostToDevice,
-                           s));
+    CVG_TRY(stage_.upload({{flat_.data(), sizeof(PairOp) * flat_.size(), ops_d_.as<void>()}}, s));
   return Status::Ok();
 }
 
@@ -434,15 +466,10 @@ Status Plan::plan_segments() {
   CVG_TRY(part_.ensure(sizeof(double) * std::max<size_t>(segs_.size(), 1) * kp_ * kp_));
   CVG_TRY(segs_d_.ensure(sizeof(GramTask) * std::max<size_t>(segs_.size(), 1)));
   CVG_TRY(nval_d_.ensure(sizeof(int64_t) * std::max(nown, 1)));
-  if (nown > 0) {
-    CVG_CK(cudaMemcpyAsync(zbase_d_.as<int64_t>(), fold_zbase_.data(), sizeof(int64_t) * nown,
-                           cudaMemcpyHostToDevice, s));
-    CVG_CK(cudaMemcpyAsync(nval_d_.as<int64_t>(), counts_.data() + fb_, sizeof(int64_t) * nown,
-                           cudaMemcpyHostToDevice, s));
-  }
-  if (!segs_.empty())
-    CVG_CK(cudaMemcpyAsync(segs_d_.as<GramTask>(), segs_.data(), sizeof(GramTask) * segs_.size(),
-                           cudaMemcpyHostToDevice, s));
+  CVG_TRY(seg_stage_.upload({{fold_zbase_.data(), sizeof(int64_t) * nown, zbase_d_.as<void>()},
+                             {counts_.data() + fb_, sizeof(int64_t) * nown, nval_d_.as<void>()},
+                             {segs_.data(), sizeof(GramTask) * segs_.size(), segs_d_.as<void>()}},
+                            s));
   if (small_) {  // no per-fold Grams: the plan's node is the tree over all chunks
     TreeGroup g{{}, local_.as<double>()};
     for (size_t sgi = 0; sgi < segs_.size(); ++sgi) g.leaves.push_back(part_.as<double>() + (int64_t)sgi * kp_ * kp_);
@@ -450,10 +477,7 @@ Status Plan::plan_segments() {
     CVG_TRY(local_tree_.build({g}, kp_, s));
     fold_ptrs_.assign(nown, nullptr);
     CVG_TRY(foldptr_d_.ensure(sizeof(void*) * std::max(nown, 1)));
-    if (nown > 0)
-      CVG_CK(cudaMemcpyAsync(foldptr_d_.as<void>(), fold_ptrs_.data(), sizeof(void*) * nown,
-                             cudaMemcpyHostToDevice, s));
-    CVG_CK(cudaStreamSynchronize(s));
+    CVG_TRY(ptr_stage_.upload({{fold_ptrs_.data(), sizeof(void*) * nown, foldptr_d_.as<void>()}}, s));
     return Status::Ok();
   }
   // Fold Gram pointers: the segment partial itself for single-segment folds,
@@ -474,8 +498,7 @@ Status Plan::plan_segments() {
     CVG_TRY(fold_tree_.build(phase1, kp_, s));
     CVG_TRY(local_tree_.build({}, kp_, s));
     CVG_TRY(foldptr_d_.ensure(sizeof(void*)));
-    CVG_CK(cudaMemcpyAsync(foldptr_d_.as<void>(), fold_ptrs_.data(), sizeof(void*), cudaMemcpyHostToDevice, s));
-    CVG_CK(cudaStreamSynchronize(s));
+    CVG_TRY(ptr_stage_.upload({{fold_ptrs_.data(), sizeof(void*), foldptr_d_.as<void>()}}, s));
     return Status::Ok();
   }
   int slot = 0;
@@ -497,11 +520,7 @@ Status Plan::plan_segments() {
                                           local_.as<double>()}};
   CVG_TRY(local_tree_.build(phase2, kp_, s));
   CVG_TRY(foldptr_d_.ensure(sizeof(void*) * std::max(nown, 1)));
-  if (nown > 0)
-    CVG_CK(cudaMemcpyAsync(foldptr_d_.as<void>(), fold_ptrs_.data(), sizeof(void*) * nown, cudaMemcpyHostToDevice,
-                           s));
-  // Host vectors above are pageable temporaries: make the copies complete.
-  CVG_CK(cudaStreamSynchronize(s));
+  CVG_TRY(ptr_stage_.upload({{fold_ptrs_.data(), sizeof(void*) * nown, foldptr_d_.as<void>()}}, s));
   return Status::Ok();
 }
 
@@ -530,8 +549,7 @@ Status Plan::gram(const void* d_x, int64_t ldx, const void* d_y, int64_t ldy, co
   if (dev_shift) {
     CVG_CK(cudaMemcpyAsync(shift, dev_shift, sizeof(double) * w_, cudaMemcpyDeviceToDevice, s));
   } else if (host_shift) {
-    CVG_CK(cudaMemcpyAsync(shift, host_shift, sizeof(double) * w_, cudaMemcpyHostToDevice, s));
-    CVG_CK(cudaStreamSynchronize(s));
+    CVG_TRY(shift_stage_.upload({{host_shift, sizeof(double) * w_, shift}}, s));
   } else {
     Timed t(ctx_, kReorder);
     launch_shift_from_row0(dtype_, d_x, d_y, k_, m_, shift, s);
@@ -621,10 +639,9 @@ Status Plan::gram_host(const void* h_x, const void* h_y, void* d_x, void* d_y, c
     off.push_back((int)byslab.size());
   }
   CVG_TRY(tiles_bycol_d_.ensure(sizeof(int2) * std::max<size_t>(byslab.size(), 1)));
-  CVG_CK(cudaMemcpyAsync(tiles_bycol_d_.as<int2>(), byslab.data(), sizeof(int2) * byslab.size(),
-                         cudaMemcpyHostToDevice, s));
+  CVG_TRY(col_stage_.upload({{byslab.data(), sizeof(int2) * byslab.size(), tiles_bycol_d_.as<void>()}}, s));
   double* shift = shift_.as<double>();
-  CVG_CK(cudaMemcpyAsync(shift, host_shift, sizeof(double) * w_, cudaMemcpyHostToDevice, s));
+  CVG_TRY(shift_stage_.upload({{host_shift, sizeof(double) * w_, shift}}, s));
   CVG_CK(cudaMemsetAsync(flag_.as<void>(), 0, sizeof(int), s));
   // the copy stream may overwrite d_x / d_y only after earlier work on s is done
   cudaEvent_t ev0 = ctx_->stream_event(0);
@@ -733,7 +750,7 @@ Status Plan::finish(const double* d_rank_partials, int32_t n_ranks, const double
   CVG_TRY(count_launch());
   if (ncfg > 0) {
     CVG_TRY(cfg_d_.ensure(sizeof(uint32_t) * ncfg));
-    CVG_CK(cudaMemcpyAsync(cfg_d_.as<void>(), cfgs, sizeof(uint32_t) * ncfg, cudaMemcpyHostToDevice, s));
+    CVG_TRY(cfg_stage_.upload({{cfgs, sizeof(uint32_t) * ncfg, cfg_d_.as<void>()}}, s));
     {
       Timed t(ctx_, kProducts);
       launch_products(total, fptr, nval, nown, n_, k_, m_, kp_, shift_.as<double>(), st, out_tiles_d_.as<int2>(),

@@ -1,6 +1,7 @@
 // Host orchestration of the cvgram B200 engine: context, plan, global cache.
 #pragma once
 
+#include <initializer_list>
 #include <memory>
 #include <string>
 #include <vector>
@@ -31,6 +32,32 @@ class DevBuf {
 
 Status cuda_status(cudaError_t e, const char* what);
 
+// Pinned staging for small host->device uploads on the hot path (segment
+// tables, tree programs, the shift, configuration masks): copies from pinned
+// memory are truly asynchronous, where a pageable cudaMemcpyAsync synchronises
+// the stream.  Before the buffer is rewritten, the previous upload from it is
+// waited for (an event), so back-to-back calls stay correct.
+class PinnedStage {
+ public:
+  PinnedStage() = default;
+  PinnedStage(const PinnedStage&) = delete;
+  PinnedStage& operator=(const PinnedStage&) = delete;
+  ~PinnedStage();
+  // Uploads `parts` (host pointer, bytes, device destination) through the buffer on stream s.
+  struct Part {
+    const void* src;
+    size_t bytes;
+    void* dst;
+  };
+  Status upload(std::initializer_list<Part> parts, cudaStream_t s);
+
+ private:
+  void* p_ = nullptr;
+  size_t bytes_ = 0;
+  cudaEvent_t ev_ = nullptr;
+  bool pending_ = false;
+};
+
 // A set of midpoint-tree sums flattened into levels of independent pairwise
 // adds (K4).  Group g: dst = S(leaves[0..n)); n == 1 copies, n == 0 zeroes.
 struct TreeGroup {
@@ -49,6 +76,7 @@ class TreeProgram {
   std::vector<int> level_off_;
   std::vector<PairOp> flat_;
   DevBuf scratch_, ops_d_;
+  PinnedStage stage_;
   int64_t next_slot_ = 0;
 };
 
@@ -147,6 +175,7 @@ class Plan {
   DevBuf tiles_d_, out_tiles_d_, tiles128_d_, zt_hi_, zt_lo_, tile_counts_, fold_counts_, bad_, zbase_d_, src_row_, z_, part_, foldbuf_, local_,
       total_, shift_, flag_, tiles_bycol_d_, src_map_, segs_d_, foldptr_d_, nval_d_, st_mz_, st_sT_, st_sd_, cfg_d_;
   TreeProgram fold_tree_, local_tree_, rank_tree_;
+  PinnedStage seg_stage_, ptr_stage_, shift_stage_, cfg_stage_, col_stage_;
   std::vector<const double*> fold_ptrs_;
 };
 
