@@ -151,6 +151,10 @@ void launch_reorder_split_t(int dtype, const void* x, int64_t ldx, const void* y
                             const double* shift, float* zt_hi, float* zt_lo, int* nonfinite, cudaStream_t s);
 bool launch_gram_tf32(const float* zt_hi, const float* zt_lo, int64_t zrows, int64_t kp, const GramTask* segs,
                       int64_t nseg, const int2* tiles128, int ntiles, double* part, int nterms, cudaStream_t s);
+// The same on CTA pairs (cta_group::2, cluster of 2): pairs[i] = {a, j, write0, write1}
+// covers row blocks 2a, 2a+1 (128 wide) x column block j; writeN: that CTA's tile is needed.
+bool launch_gram_tf32_2sm(const float* zt_hi, const float* zt_lo, int64_t zrows, int64_t kp, const GramTask* segs,
+                          int64_t nseg, const int4* pairs, int npairs, double* part, cudaStream_t s);
 
 inline int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
 inline int64_t padded_cols(int64_t k, int64_t m, int dtype = 0) {

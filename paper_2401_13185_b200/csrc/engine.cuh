@@ -157,6 +157,8 @@ class Plan {
   int64_t n_ = 0, k_ = 0, m_ = 0, w_ = 0, kp_ = 0;
   int32_t p_ = 0, fb_ = 0, fe_ = 0;
   std::vector<int2> tiles_, out_tiles_, tiles128_;
+  std::vector<int4> pairs128_;  // CTA-pair tiles for the cta_group::2 fp32 Gram
+  DevBuf pairs128_d_;
   std::vector<int64_t> counts_;  // per fold (all p) validation sizes
   std::vector<GramTask> segs_;
   std::vector<int32_t> fold_seg_begin_;
