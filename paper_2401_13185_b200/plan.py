@@ -11,8 +11,15 @@ one collective per run, as the north star prescribes.  The all-gather + fixed
 tree combine (instead of a rank-count-dependent all-reduce order) keeps
 results bit-identical for 1, 2, 4 and 8 GPUs.
 
+From host memory (``run_all_folds_sharded``) each rank copies only its row
+shard over PCIe and the rows cross NVLink once: an all-to-all to their fold's
+owner (the rank plan then reads compacted rows through a row map,
+cvg_plan_gram_mapped), or an all-gather when folds are shared (P < G).
+``DevicePlan.iter_folds`` streams the emitted folds in batches
+(cvg_plan_finish_range) for leave-one-out-scale P.
+
 PyTorch is plumbing here: device buffers, the current stream, and
-torch.distributed for the collective.  No torch types cross the C ABI.
+torch.distributed for the collectives.  No torch types cross the C ABI.
 """
 from __future__ import annotations
 
