@@ -4,6 +4,7 @@
 // validation products; the per-fold downdate, centering and scaling run in the
 // device epilogue.  Same signatures, validation order and exceptions.
 
+#include <type_traits>
 #include <vector>
 
 #include "cvgram/core.hpp"
@@ -132,6 +133,64 @@ inline std::vector<std::vector<FoldResult>> run_all_folds_configs(const DatasetP
     }
   }
   return out;
+}
+
+/// Lazy per-fold generation (cvg_run_all_folds_stream) for leave-one-out-scale P:
+/// fn(config_index, FoldResult&&) is called for every configuration and fold, folds
+/// ascending, while only `batch` folds of outputs exist at a time.  fn may return
+/// bool (true stops the run) or void.  Same values as run_all_folds_configs.
+template <class F>
+inline void for_each_fold(const DatasetPair& data, const Partitioning& part, const std::vector<PreprocessConfig>& cfgs,
+                          F&& fn, int batch = 1024) {
+  const Index n = data.n_rows(), k = data.n_features(), m = data.n_responses();
+  std::vector<int32_t> labels(part.labels.begin(), part.labels.end());
+  std::vector<uint32_t> masks;
+  for (const auto& c : cfgs) masks.push_back(c.mask());
+  struct State {
+    F* fn;
+    const std::vector<PreprocessConfig>* cfgs;
+    Index k, m;
+  } state{&fn, &cfgs, k, m};
+  auto tramp = [](int32_t lo, int32_t hi, const double* xtx, const double* xty, const double* mx, const double* my,
+                  const double* sx, const double* sy, const int64_t* nt, const int64_t* nv, void* user) -> int {
+    State& st = *static_cast<State*>(user);
+    const Index nb = hi - lo, kk = st.k, mm = st.m;
+    const size_t nc = st.cfgs->size();
+    auto vec = [](const double* src, Index len) {
+      Vector v(len);
+      std::copy(src, src + len, v.data());
+      return v;
+    };
+    for (Index f = 0; f < nb; ++f)
+      for (size_t c = 0; c < nc; ++c) {
+        const PreprocessConfig& cfg = (*st.cfgs)[c];
+        FoldResult r;
+        r.fold_id = static_cast<int>(lo + f) + 1;
+        r.xtx_t = Matrix(kk, kk);
+        r.xty_t = Matrix(kk, mm);
+        std::copy_n(xtx + (c * nb + f) * kk * kk, kk * kk, r.xtx_t.data());
+        std::copy_n(xty + (c * nb + f) * kk * mm, kk * mm, r.xty_t.data());
+        r.stats.n_train = nt[f];
+        r.stats.n_val = nv[f];
+        if (cfg.any()) {
+          r.stats.mean_x_t = vec(mx + f * kk, kk);
+          r.stats.mean_y_t = vec(my + f * mm, mm);
+        }
+        if (cfg.scale_x) r.stats.std_x_t = vec(sx + f * kk, kk);
+        if (cfg.scale_y) r.stats.std_y_t = vec(sy + f * mm, mm);
+        if constexpr (std::is_same_v<decltype((*st.fn)(0, std::move(r))), bool>) {
+          if ((*st.fn)(static_cast<int>(c), std::move(r))) return 1;
+        } else {
+          (*st.fn)(static_cast<int>(c), std::move(r));
+        }
+      }
+    return 0;
+  };
+  char err[512] = {0};
+  detail::check(cvg_run_all_folds_stream(detail::Context::get(), CVG_DTYPE_F64, data.x().data(), data.y().data(), n, k,
+                                         m, labels.data(), part.n_rows(), part.p, masks.data(),
+                                         static_cast<int32_t>(masks.size()), batch, +tramp, &state, err, sizeof err),
+                err);
 }
 
 /// One global pass, then every fold; ascending fold_id (fast.hpp:133-152).

@@ -91,6 +91,22 @@ int cvg_run_all_folds(cvg_context* ctx, int dtype, const void* x, const void* y,
                       double* xtx, double* xty, double* mean_x, double* mean_y, double* std_x, double* std_y,
                       int64_t* n_train, int64_t* n_val, char* err, size_t errlen);
 
+/* run_all_folds streamed in fold batches (a lazy per-fold generator for
+ * leave-one-out-scale P, where the P*K*(K+M) outputs cannot all exist at once).
+ * `fn` is called once per batch of folds [fold_lo, fold_hi) (0-based, ascending)
+ * with host buffers valid only during the call:
+ *   xtx [n_cfg][nb][k][k], xty [n_cfg][nb][k][m]  (nb = fold_hi - fold_lo)
+ *   mean_x, std_x [nb][k], mean_y, std_y [nb][m]  (training statistics, every entry filled)
+ *   n_train, n_val [nb]
+ * A nonzero return from `fn` stops the run early (CVG_OK is still returned).
+ * Same values, bit for bit, as cvg_run_all_folds. */
+typedef int (*cvg_fold_batch_fn)(int32_t fold_lo, int32_t fold_hi, const double* xtx, const double* xty,
+                                 const double* mean_x, const double* mean_y, const double* std_x, const double* std_y,
+                                 const int64_t* n_train, const int64_t* n_val, void* user);
+int cvg_run_all_folds_stream(cvg_context* ctx, int dtype, const void* x, const void* y, int64_t n, int64_t k, int64_t m,
+                             const int32_t* labels, int64_t n_labels, int32_t p, const uint32_t* cfg_masks,
+                             int32_t n_cfg, int32_t batch, cvg_fold_batch_fn fn, void* user, char* err, size_t errlen);
+
 /* ------------------------------- device-resident staged API (bench, multi-GPU) */
 /* A plan owns folds [fold_begin, fold_end) of a p-fold partitioning of n rows. */
 int cvg_plan_create(cvg_context* ctx, int dtype, int64_t n, int64_t k, int64_t m, int32_t p, int32_t fold_begin,

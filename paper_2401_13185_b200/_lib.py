@@ -45,6 +45,8 @@ SIGNATURES = {
     "cvg_plan_bind_labels": (c_int, [c_vp, c_vp, c_int, c_char_p, c_size_t]),
     "cvg_plan_gram": (c_int, [c_vp, c_vp, c_i64, c_vp, c_i64, c_vp, c_char_p, c_size_t]),
     "cvg_plan_gram_mapped": (c_int, [c_vp, c_vp, c_i64, c_vp, c_i64, c_vp, c_i64, c_vp, c_char_p, c_size_t]),
+    "cvg_run_all_folds_stream": (c_int, [c_vp, c_int, c_vp, c_vp, c_i64, c_i64, c_i64, c_vp, c_i64, c_i32, c_vp, c_i32,
+                                         c_i32, c_vp, c_vp, c_char_p, c_size_t]),
     "cvg_plan_finish_range": (c_int, [c_vp, c_vp, c_i32, c_vp, c_i32, c_i32, c_i32] + [c_vp] * 6 + [c_char_p, c_size_t]),
     "cvg_plan_partial": (c_int, [c_vp, c_vp, ctypes.POINTER(c_i64)]),
     "cvg_plan_finish": (c_int, [c_vp, c_vp, c_i32, c_vp, c_i32] + [c_vp] * 6 + [c_char_p, c_size_t]),

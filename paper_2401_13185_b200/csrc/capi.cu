@@ -363,6 +363,98 @@ int cvg_run_all_folds(cvg_context* ctx, int dtype, const void* x, const void* y,
   });
 }
 
+int cvg_run_all_folds_stream(cvg_context* ctx, int dtype, const void* x, const void* y, int64_t n, int64_t k, int64_t m,
+                             const int32_t* labels, int64_t n_labels, int32_t p, const uint32_t* cfg_masks,
+                             int32_t n_cfg, int32_t batch, cvg_fold_batch_fn fn, void* user, char* err, size_t errlen) {
+  return guarded(err, errlen, [&]() -> Status {
+    if (!ctx) return Status::Err(CVG_E_INVALID_ARG, "null context");
+    if (!fn) return Status::Err(CVG_E_INVALID_ARG, "null fold callback");
+    if (batch < 1) return Status::Err(CVG_E_INVALID_ARG, "batch must be at least 1 fold");
+    if (dtype != CVG_DTYPE_F64 && dtype != CVG_DTYPE_F32) return Status::Err(CVG_E_INVALID_ARG, "unsupported dtype");
+    if (n < 2) return Status::Err(CVG_E_DIMENSION, "need at least 2 samples");
+    if (k < 1 || m < 1) return Status::Err(CVG_E_DIMENSION, "x and y must each have at least one column");
+    if (n_cfg < 1 || !cfg_masks) return Status::Err(CVG_E_INVALID_ARG, "need at least one configuration");
+    for (int32_t c = 0; c < n_cfg; ++c)
+      if (cfg_masks[c] > 15u) return Status::Err(CVG_E_INVALID_ARG, "configuration mask outside 0..15");
+    if (n_labels != n) return Status::Err(CVG_E_DIMENSION, "partitioning length does not match sample count");
+    std::vector<int64_t> counts;
+    Status s = validate_partitioning(labels, n, p, &counts);
+    if (!s.ok()) return s;
+    const bool scal = any_scale(cfg_masks, n_cfg);
+    if (scal && !(s = check_scalable(counts, n)).ok()) return s;
+    if (!(s = cvg::cuda_status(cudaSetDevice(ctx->device), "cudaSetDevice")).ok()) return s;
+    if (!ctx->scratch) ctx->scratch.reset(new cvg::HostScratch());
+    cvg::HostScratch& sc = *ctx->scratch;
+    cudaStream_t st = ctx->stream;
+    const size_t e = elt(dtype);
+    if (!(s = sc.x.ensure(e * n * k)).ok() || !(s = sc.y.ensure(e * n * m)).ok() ||
+        !(s = sc.labels.ensure(sizeof(int32_t) * n)).ok())
+      return s;
+    if (!(s = cvg::cuda_status(cudaMemcpyAsync(sc.labels.as<void>(), labels, sizeof(int32_t) * n,
+                                               cudaMemcpyHostToDevice, st),
+                               "H2D labels"))
+             .ok())
+      return s;
+    if (!(s = sc.plan.create(ctx, dtype, n, k, m, p, 0, p, true)).ok()) return s;
+    if (!(s = sc.plan.bind_labels(sc.labels.as<int32_t>(), true, scal)).ok()) return s;
+    std::vector<double> shift(k + m);
+    for (int64_t c = 0; c < k + m; ++c) {
+      const void* src = c < k ? x : y;
+      const int64_t i = c < k ? c : c - k;
+      shift[c] = dtype == CVG_DTYPE_F32 ? (double)static_cast<const float*>(src)[i] : static_cast<const double*>(src)[i];
+    }
+    if (!(s = sc.plan.gram_host(x, y, sc.x.as<void>(), sc.y.as<void>(), shift.data())).ok()) return s;
+    // one batch of outputs on the device and in pinned host memory, reused
+    const int32_t nb = std::min<int32_t>(batch, p);
+    const size_t nxx = (size_t)n_cfg * nb * k * k, nxy = (size_t)n_cfg * nb * k * m;
+    cvg::DevBuf dxx, dxy, dvec;
+    if (!(s = dxx.ensure(sizeof(double) * nxx)).ok() || !(s = dxy.ensure(sizeof(double) * nxy)).ok() ||
+        !(s = dvec.ensure(sizeof(double) * 2 * nb * (k + m))).ok())
+      return s;
+    struct Pinned {
+      void* p = nullptr;
+      ~Pinned() {
+        if (p) cudaFreeHost(p);
+      }
+    } host;
+    const size_t hbytes = sizeof(double) * (nxx + nxy + 2 * (size_t)nb * (k + m)) + 2 * sizeof(int64_t) * nb;
+    if (!(s = cvg::cuda_status(cudaHostAlloc(&host.p, hbytes, cudaHostAllocDefault), "pinned batch buffer")).ok())
+      return s;
+    double* hxx = static_cast<double*>(host.p);
+    double* hxy = hxx + nxx;
+    double* hmx = hxy + nxy;
+    double* hmy = hmx + (size_t)nb * k;
+    double* hsx = hmy + (size_t)nb * m;
+    double* hsy = hsx + (size_t)nb * k;
+    int64_t* hnt = reinterpret_cast<int64_t*>(hsy + (size_t)nb * m);
+    int64_t* hnv = hnt + nb;
+    double* dmx = dvec.as<double>();
+    double* dmy = dmx + (size_t)nb * k;
+    double* dsx = dmy + (size_t)nb * m;
+    double* dsy = dsx + (size_t)nb * k;
+    for (int32_t lo = 0; lo < p; lo += nb) {
+      const int32_t hi = std::min<int32_t>(p, lo + nb), cnt = hi - lo;
+      if (!(s = sc.plan.finish(nullptr, 1, nullptr, cfg_masks, n_cfg, dxx.as<double>(), dxy.as<double>(), dmx, dmy,
+                               dsx, dsy, lo, hi))
+               .ok())
+        return s;
+      // packed for cnt folds: [n_cfg][cnt][k][k] etc.
+      if (!(s = d2h(hxx, dxx.as<void>(), sizeof(double) * n_cfg * cnt * k * k, st)).ok() ||
+          !(s = d2h(hxy, dxy.as<void>(), sizeof(double) * n_cfg * cnt * k * m, st)).ok() ||
+          !(s = d2h(hmx, dmx, sizeof(double) * cnt * k, st)).ok() || !(s = d2h(hmy, dmy, sizeof(double) * cnt * m, st)).ok() ||
+          !(s = d2h(hsx, dsx, sizeof(double) * cnt * k, st)).ok() || !(s = d2h(hsy, dsy, sizeof(double) * cnt * m, st)).ok())
+        return s;
+      if (!(s = cvg::cuda_status(cudaStreamSynchronize(st), "stream synchronize")).ok()) return s;
+      for (int32_t f = 0; f < cnt; ++f) {
+        hnt[f] = n - counts[lo + f];
+        hnv[f] = counts[lo + f];
+      }
+      if (fn(lo, hi, hxx, hxy, hmx, hmy, hsx, hsy, hnt, hnv, user)) break;
+    }
+    return Status::Ok();
+  });
+}
+
 int cvg_baseline_fold_products(cvg_context* ctx, int dtype, const void* x, const void* y, int64_t n, int64_t k,
                                int64_t m, const int32_t* labels, int64_t n_labels, int32_t p,
                                const uint32_t* cfg_masks, int32_t n_cfg, double* xtx, double* xty, double* mean_x,

@@ -454,6 +454,56 @@ def run_all_folds_configs(data: DatasetPair, part: Partitioning, cfgs, ctx: Opti
     return out
 
 
+_FOLD_BATCH_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_int32, ctypes.c_int32, *([ctypes.c_void_p] * 9))
+
+
+def for_each_fold(data: DatasetPair, part: Partitioning, cfgs, fn, batch: int = 1024,
+                  ctx: Optional[Context] = None) -> None:
+    """Lazy per-fold generation (cvg_run_all_folds_stream): ``fn(config_index, FoldResult)`` is called for every
+    configuration and fold, folds in ascending order, while only ``batch`` folds of outputs exist at a time
+    (leave-one-out-scale P).  ``fn`` returning True stops the run.  Same values as run_all_folds_configs."""
+    cfgs = [_cfg(c) for c in cfgs]
+    ctx = ctx or get_context()
+    n, k, m, p = data.n_rows(), data.n_features(), data.n_responses(), part.p
+    nc = len(cfgs)
+    masks = np.array([c.mask for c in cfgs], np.uint32)
+    stop = [False]
+    error = []
+
+    def on_batch(lo, hi, pxx, pxy, pmx, pmy, psx, psy, pnt, pnv, _user):
+        try:
+            nb = hi - lo
+            arr = lambda ptr, shape, dt=np.float64: np.ctypeslib.as_array(  # noqa: E731
+                ctypes.cast(ptr, ctypes.POINTER(ctypes.c_double if dt == np.float64 else ctypes.c_int64)), shape)
+            xtx, xty = arr(pxx, (nc, nb, k, k)), arr(pxy, (nc, nb, k, m))
+            mx, my, sx, sy = arr(pmx, (nb, k)), arr(pmy, (nb, m)), arr(psx, (nb, k)), arr(psy, (nb, m))
+            nt, nv = arr(pnt, (nb,), np.int64), arr(pnv, (nb,), np.int64)
+            for f in range(nb):
+                for ci, cfg in enumerate(cfgs):
+                    st = FoldStats(n_train=int(nt[f]), n_val=int(nv[f]))
+                    if cfg.any():
+                        st.mean_x_t, st.mean_y_t = mx[f].copy(), my[f].copy()
+                    if cfg.scale_x:
+                        st.std_x_t = sx[f].copy()
+                    if cfg.scale_y:
+                        st.std_y_t = sy[f].copy()
+                    if fn(ci, FoldResult(lo + f + 1, xtx[ci, f].copy(), xty[ci, f].copy(), st)):
+                        stop[0] = True
+                        return 1
+            return 0
+        except BaseException as e:  # surface Python errors after the C call returns
+            error.append(e)
+            return 1
+
+    cb = _FOLD_BATCH_FN(on_batch)
+    buf = L.err_buf()
+    _check(L.lib().cvg_run_all_folds_stream(ctx.handle, data.dtype_code, _ptr(data.x()), _ptr(data.y()), n, k, m,
+                                            _ptr(part.labels), part.labels.size, p, _ptr(masks), nc, int(batch),
+                                            ctypes.cast(cb, ctypes.c_void_p), None, buf, len(buf)), buf)
+    if error:
+        raise error[0]
+
+
 def run_all_folds(data: DatasetPair, part: Partitioning, cfg=None, n_threads: int = 1,
                   ctx: Optional[Context] = None) -> List[FoldResult]:
     """One global pass, then every fold; ascending fold_id (fast.hpp:133-152).

@@ -368,6 +368,31 @@ void acceptance_c1() {  // 62-84
   CHECK(worst <= 1e-8);
 }
 
+// Lazy per-fold generation (beyond the reference API): same bits as run_all_folds_configs, early stop honoured.
+void for_each_fold_streams_the_same_results() {
+  std::mt19937_64 rng(77);
+  const auto data = random_dataset(300, 12, 3, rng);
+  const auto part = random_partitioning(300, 41, rng);
+  const std::vector<PreprocessConfig> cfgs{from_bits(15), from_bits(0), from_bits(12)};
+  const auto all = run_all_folds_configs(data, part, cfgs);
+  int seen = 0;
+  bool same = true;
+  for_each_fold(
+      data, part, cfgs,
+      [&](int c, FoldResult&& r) {
+        const FoldResult& ref = all[c][r.fold_id - 1];
+        same = same && r.xtx_t == ref.xtx_t && r.xty_t == ref.xty_t && r.stats.n_val == ref.stats.n_val &&
+               r.stats.std_x_t == ref.stats.std_x_t && r.stats.mean_y_t == ref.stats.mean_y_t;
+        ++seen;
+      },
+      /*batch=*/7);
+  CHECK(same);
+  CHECK(seen == 3 * 41);
+  int calls = 0;
+  for_each_fold(data, part, cfgs, [&](int, FoldResult&&) { return ++calls == 5; }, 4);
+  CHECK(calls == 5);
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
@@ -395,6 +420,7 @@ int main(int argc, char** argv) {
       {"device_baseline_micro_and_errors", device_baseline_micro_and_errors, true},
       {"errors_like_the_reference", errors_like_the_reference, true},
       {"acceptance_c1", acceptance_c1, true},
+      {"for_each_fold_streams_the_same_results", for_each_fold_streams_the_same_results, true},
   };
   int failed_tests = 0;
   for (const auto& t : tests) {
