@@ -388,11 +388,18 @@ def run_ours(args):
 
     f32 = not x_dtype_is_f64(cid)
     executed = executed_gram_flops(n, k, m, p, f32) / max(world, 1) / (gram_ms * 1e-3) / 1e12
-    if f32:
-        gram_kernel = "gram_tf32_kernel (tcgen05.mma kind::tf32, 3xTF32, TMEM accumulators)"
+    tf32_kind = os.environ.get("CVG_FP32_KIND") == "tf32"
+    if f32 and tf32_kind:
+        gram_kernel = "gram_tf32_kernel (tcgen05.mma kind::tf32, 3xTF32, TMEM accumulators; CVG_FP32_KIND=tf32)"
         peak = TF32_PEAK_TFLOPS
         peak_source = ("measured cuBLAS TF32 GEMM (8192^3, sustained) on this pool's B200 "
                        "(profiles/r01_fp64_peaks.txt); executed counts the 3 TF32 products")
+    elif f32:
+        gram_kernel = ("gram_f16s_kernel (tcgen05.mma kind::f16: power-of-two scaled fp16 hi+lo split, "
+                       "3 products, TMEM accumulators, exact unscale into fp64)")
+        peak = peaks().get("bf16_tflops_sustained", 1374.5)
+        peak_source = ("MEASURED_PEAKS.json bf16_tflops_sustained (cuBLAS bf16 8192^3 back to back; kind::f16 "
+                       "runs fp16 and bf16 at one rate); executed counts the 3 fp16 products")
     else:
         gram_kernel = "gram_f64_kernel (DMMA.8x8x4)"
         peak = FP64_DMMA_PEAK_TFLOPS
@@ -410,7 +417,8 @@ def run_ours(args):
     pk = peaks()
     hbm = pk.get("hbm_gbs", 6554.2)
     tile = 128 if f32 else 64
-    reorder_bytes = n * (k + m) * x_elt + (n + 32 * p) * (-(-(k + m + 1) // tile) * tile) * 8
+    z_elem = 4 if (f32 and not tf32_kind) else 8  # Z: fp64 | fp16 hi + lo | tf32 hi + lo
+    reorder_bytes = n * (k + m) * x_elt + n * (-(-(k + m + 1) // tile) * tile) * z_elem
     epi_bytes = len(masks) * (2 * p * k * (k + m) * 8) + k * (k + m) * 8
     line = {
         "metric": "all_fold_cv_gram_gflops", "value": round(value, 3), "unit": "GFLOP/s", "n_gpus": world,
@@ -433,7 +441,7 @@ def run_ours(args):
                      "executed_frac": round(executed / peak, 4),
                      "note": "algorithmic flops = 2NK(K+M) (BASELINE metric); the fp64 kernel computes only the "
                              "upper 64x64 tiles (diagonal tiles: their upper 8x8 blocks), the fp32 kernel the upper "
-                             "128x128 tiles x 3 TF32 products: executed_tflops counts what the tensor cores issue"},
+                             "128x128 tiles x 3 fp16 products: executed_tflops counts what the tensor cores issue"},
         "kernels_ms_per_step": per_kernel,
         "hbm_rooflines": {
             "reorder": {"bytes": reorder_bytes, "achieved_gbs": round(reorder_bytes / (kms[1] / args.steps * 1e-3) / 1e9, 1)

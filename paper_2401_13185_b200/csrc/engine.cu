@@ -208,7 +208,7 @@ Status TreeProgram::run(cvg_context* ctx, const int2* tiles, int ntiles, int64_t
 
 // Rows per segment: a fixed constant per dtype (never a function of the GPU
 // count, so sums stay bit-identical across world sizes).  CVG_CHUNK_ROWS
-// overrides it for tuning experiments (multiple of kRowStep).
+// overrides it for tuning experiments (rounded to the plan's row step).
 // fp32 Gram on CTA pairs (tcgen05 cta_group::2): CVG_TF32_2SM=1 (A/B against the single-CTA kernel).
 static bool tf32_2sm() {
   static const bool v = [] {
@@ -218,23 +218,54 @@ static bool tf32_2sm() {
   return v;
 }
 
+// fp32 operand kind: the scaled fp16 split on kind::f16 (default) or, with
+// CVG_FP32_KIND=tf32, the 3xTF32 split on kind::tf32 (k_gram_tf32.cu; A/B tests).
+bool Plan::fp32_tf32() {
+  static const bool v = [] {
+    const char* e = std::getenv("CVG_FP32_KIND");
+    return e && std::string(e) == "tf32";
+  }();
+  return v;
+}
+
+// The fp16 path's row group G (one exponent per group and column, one fp32 TMEM
+// chunk) is also the fold padding and segment alignment.  Largest of 256 / 128 /
+// 64 whose padding stays within 1/8 of the 64-row minimum; a function of the
+// global fold sizes only, so every rank plan picks the same G.
+void Plan::choose_row_step() {
+  row_step_ = kRowStep;
+  if (!f16_path()) return;
+  auto padded = [&](int64_t g) {
+    int64_t t = 0;
+    for (int64_t c : counts_) t += round_up(std::max<int64_t>(c, 1), g);
+    return t;
+  };
+  const int64_t base = padded(64);
+  row_step_ = 64;
+  for (int64_t g : {256, 128})
+    if (padded(g) * 8 <= base * 9) {
+      row_step_ = g;
+      break;
+    }
+}
+
 int64_t Plan::chunk_rows() const {
   static const int64_t env = [] {
     const char* v = std::getenv("CVG_CHUNK_ROWS");
     const long long r = v ? std::atoll(v) : 0;
-    return (int64_t)(r > 0 ? round_up(r, kRowStep) : 0);
+    return (int64_t)(r > 0 ? r : 0);
   }();
-  if (env > 0) return env;
-  return dtype_ == 1 ? kChunkRowsF32 : kChunkRows;
+  if (env > 0) return round_up(env, row_step_);
+  return round_up(dtype_ == 1 ? kChunkRowsF32 : kChunkRows, row_step_);
 }
 
 // Rows per segment of a fold of `count` rows: the fold is cut into
-// ceil(padded / chunk_rows()) segments of equal size (rounded up to 32 rows), so
+// ceil(padded / chunk_rows()) segments of equal size (rounded up to the row step), so
 // no fold ends in a sliver segment and the Gram's CTAs carry even work.
 int64_t Plan::seg_rows(int64_t count) const {
-  const int64_t padded = round_up(count, kRowStep), chunk = chunk_rows();
+  const int64_t padded = round_up(count, row_step_), chunk = chunk_rows();
   const int64_t nseg = std::max<int64_t>(1, (padded + chunk - 1) / chunk);
-  return std::max<int64_t>(kRowStep, round_up((padded + nseg - 1) / nseg, kRowStep));
+  return std::max<int64_t>(row_step_, round_up((padded + nseg - 1) / nseg, row_step_));
 }
 
 Status Plan::count_launch(int n) {
@@ -256,6 +287,7 @@ Status Plan::create(cvg_context* ctx, int dtype, int64_t n, int64_t k, int64_t m
   bound_ = grammed_ = false;
   if (dtype != 0 && dtype != 1) return Status::Err(4, "unsupported dtype");
   if (n < 2) return Status::Err(1, "need at least 2 samples");
+  if (n > INT32_MAX) return Status::Err(4, "more than 2^31 - 1 samples per plan is unsupported (int32 row indices)");
   if (k < 1 || m < 1) return Status::Err(1, "x and y must each have at least one column");
   if (validate) {
     if (p < 2) return Status::Err(2, "fold count must be at least 2, got " + std::to_string(p));
@@ -328,7 +360,7 @@ void Plan::assign_rank() {
       if (s0 < 0) {
         s0 = 0;
         const int64_t sr = seg_rows(counts_[a]);
-        s1 = (round_up(counts_[a], kRowStep) + sr - 1) / sr;
+        s1 = (round_up(counts_[a], row_step_) + sr - 1) / sr;
         glo = lo;
         ghi = hi;
       }
@@ -400,6 +432,7 @@ Status Plan::bind_labels(const int32_t* d_labels, bool validate, bool require_sc
           return Status::Err(3, "fold " + std::to_string(f + 1) + " leaves a training partition of " +
                                     std::to_string(n_ - counts_[f]) + " rows; scaling needs at least 2");
   }
+  choose_row_step();
   if (rank_mode_) assign_rank();
   small_ = false;
   if (dtype_ == 0 && !rank_mode_ && fb_ == 0 && fe_ == p_ && small_folds_enabled()) {
@@ -434,9 +467,11 @@ Status Plan::bind_rows(const int64_t* rows, int64_t nrows, int64_t n_src) {
   if (p_ != 1 || fb_ != 0 || fe_ != 1) return Status::Err(4, "bind_rows needs a single-fold plan");
   small_ = false;
   src_n_ = n_src < 0 ? n_ : n_src;
+  if (src_n_ > INT32_MAX) return Status::Err(4, "bind_rows: source matrices beyond 2^31 - 1 rows are unsupported");
   for (int64_t i = 0; i < nrows; ++i)
     if (rows[i] < 0 || rows[i] >= src_n_) return Status::Err(4, "bind_rows: row index outside the source matrix");
   counts_.assign(1, nrows);
+  choose_row_step();
   CVG_TRY(plan_segments());
   std::vector<int64_t> src(std::max<int64_t>(zrows_, 1), -1);
   std::copy(rows, rows + nrows, src.begin());
@@ -468,7 +503,7 @@ Status Plan::plan_segments() {
       segs_.push_back(GramTask{off, std::min<int64_t>(chunk, zrows_ - off)});
   }
   for (int32_t f = fb_; f < fe_ && !small_; ++f) {
-    const int64_t padded = round_up(counts_[f], kRowStep);
+    const int64_t padded = round_up(counts_[f], row_step_);
     const int64_t chunk = seg_rows(counts_[f]);
     // Owned window of the fold's bucketed rows: all of it, or (shared fold) segments [seg_lo_, seg_hi_).
     const int64_t w0 = seg_lo_ >= 0 ? std::min(padded, seg_lo_ * chunk) : 0;
@@ -483,9 +518,11 @@ Status Plan::plan_segments() {
   cudaStream_t s = ctx_->stream;
   CVG_TRY(zbase_d_.ensure(sizeof(int64_t) * std::max(nown, 1)));
   CVG_TRY(src_row_.ensure(sizeof(int64_t) * std::max<int64_t>(zrows_, 1)));
-  if (dtype_ == 1) {  // blocked-transposed TF32 hi / lo operands for the tcgen05 Gram
-    CVG_TRY(zt_hi_.ensure(sizeof(float) * std::max<int64_t>(zrows_, 32) * kp_));
-    CVG_TRY(zt_lo_.ensure(sizeof(float) * std::max<int64_t>(zrows_, 32) * kp_));
+  if (dtype_ == 1) {  // blocked-transposed hi / lo operands for the tcgen05 Gram (fp16 or TF32)
+    const size_t e = f16_path() ? 2 : 4;
+    CVG_TRY(zt_hi_.ensure(e * std::max<int64_t>(zrows_, row_step_) * kp_));
+    CVG_TRY(zt_lo_.ensure(e * std::max<int64_t>(zrows_, row_step_) * kp_));
+    if (f16_path()) CVG_TRY(unscale_.ensure(sizeof(float) * std::max<int64_t>(zrows_ / row_step_, 1) * kp_));
   } else {
     CVG_TRY(z_.ensure(sizeof(double) * std::max<int64_t>(zrows_, 1) * kp_));
   }
@@ -583,12 +620,17 @@ Status Plan::gram(const void* d_x, int64_t ldx, const void* d_y, int64_t ldy, co
   }
   CVG_CK(cudaMemsetAsync(flag_.as<void>(), 0, sizeof(int), s));
   if (dtype_ == 1) {
-    // fp32: K1T (bucket, shift, TF32 split, blocked transpose) then the tcgen05 Gram.
+    // fp32: K1H / K1T (bucket, shift, split, blocked transpose) then the tcgen05 Gram.
     if (zrows_ > 0) {
       {
         Timed t(ctx_, kReorder);
-        launch_reorder_split_t(dtype_, d_x, ldx, d_y, ldy, k_, m_, rows, zrows_, kp_, 0, kp_, shift,
-                               zt_hi_.as<float>(), zt_lo_.as<float>(), flag_.as<int>(), s);
+        if (f16_path())
+          launch_reorder_split_h(dtype_, d_x, ldx, d_y, ldy, k_, m_, rows, zrows_, kp_, 0, kp_, nsrc, shift,
+                                 (int)row_step_, zt_hi_.as<void>(), zt_lo_.as<void>(), unscale_.as<float>(),
+                                 flag_.as<int>(), s);
+        else
+          launch_reorder_split_t(dtype_, d_x, ldx, d_y, ldy, k_, m_, rows, zrows_, kp_, 0, kp_, shift,
+                                 zt_hi_.as<float>(), zt_lo_.as<float>(), flag_.as<int>(), s);
       }
       CVG_TRY(count_launch());
     }
@@ -596,7 +638,11 @@ Status Plan::gram(const void* d_x, int64_t ldx, const void* d_y, int64_t ldy, co
       bool ok;
       {
         Timed t(ctx_, kGram);
-        ok = tf32_2sm()
+        ok = f16_path()
+                 ? launch_gram_f16s(zt_hi_.as<void>(), zt_lo_.as<void>(), unscale_.as<float>(), (int)row_step_,
+                                    zrows_, kp_, segs_d_.as<GramTask>(), (int64_t)segs_.size(),
+                                    tiles128_d_.as<int2>(), (int)tiles128_.size(), part_.as<double>(), s)
+             : tf32_2sm()
                  ? launch_gram_tf32_2sm(zt_hi_.as<float>(), zt_lo_.as<float>(), zrows_, kp_, segs_d_.as<GramTask>(),
                                         (int64_t)segs_.size(), pairs128_d_.as<int4>(), (int)pairs128_.size(),
                                         part_.as<double>(), s)
@@ -697,7 +743,11 @@ Status Plan::gram_host(const void* h_x, const void* h_y, void* d_x, void* d_y, c
     if (zrows_ > 0) {
       {
         Timed t(ctx_, kReorder);
-        if (dtype_ == 1)
+        if (f16_path())
+          launch_reorder_split_h(dtype_, d_x, k_, d_y, m_, k_, m_, src_row_.as<int64_t>(), zrows_, kp_, z0, z1, src_n_,
+                                 shift, (int)row_step_, zt_hi_.as<void>(), zt_lo_.as<void>(), unscale_.as<float>(),
+                                 flag_.as<int>(), s);
+        else if (dtype_ == 1)
           launch_reorder_split_t(dtype_, d_x, k_, d_y, m_, k_, m_, src_row_.as<int64_t>(), zrows_, kp_, z0, z1, shift,
                                  zt_hi_.as<float>(), zt_lo_.as<float>(), flag_.as<int>(), s);
         else
@@ -710,7 +760,11 @@ Status Plan::gram_host(const void* h_x, const void* h_y, void* d_x, void* d_y, c
       bool ok = true;
       {
         Timed t(ctx_, kGram);
-        if (dtype_ == 1)
+        if (f16_path())
+          ok = launch_gram_f16s(zt_hi_.as<void>(), zt_lo_.as<void>(), unscale_.as<float>(), (int)row_step_, zrows_,
+                                kp_, segs_d_.as<GramTask>(), (int64_t)segs_.size(), tiles_bycol_d_.as<int2>() + t0,
+                                t1 - t0, part_.as<double>(), s);
+        else if (dtype_ == 1)
           ok = launch_gram_tf32(zt_hi_.as<float>(), zt_lo_.as<float>(), zrows_, kp_, segs_d_.as<GramTask>(),
                                 (int64_t)segs_.size(), tiles_bycol_d_.as<int2>() + t0, t1 - t0, part_.as<double>(), 3,
                                 s);
@@ -791,6 +845,8 @@ Status Plan::finish(const double* d_rank_partials, int32_t n_ranks, const double
   int flag = 0;
   CVG_CK(cudaMemcpyAsync(&flag, flag_.as<int>(), sizeof flag, cudaMemcpyDeviceToHost, s));
   CVG_CK(cudaStreamSynchronize(s));
+  if (flag & 2)  // K1H range bit (an out-of-range value also surfaces as non-finite Gram entries: bit 0)
+    return Status::Err(1, "fp32 inputs: |x - x[0]| >= 2^79 exceeds the fp32 tensor-core accumulation range");
   if (flag) return Status::Err(1, "x and y entries must be finite");
   return Status::Ok();
 }

@@ -151,6 +151,9 @@ class Plan {
   void assign_rank();  // rank mode: fb_/fe_, segment window, fold group
   int64_t chunk_rows() const;
   int64_t seg_rows(int64_t count) const;
+  bool f16_path() const { return dtype_ == 1 && !fp32_tf32(); }
+  static bool fp32_tf32();
+  void choose_row_step();  // fold padding / segment alignment (fp16 path: its row group G)
 
   cvg_context* ctx_ = nullptr;
   int dtype_ = 0;
@@ -165,6 +168,7 @@ class Plan {
   std::vector<int64_t> fold_zbase_;
   int64_t zrows_ = 0;
   int64_t src_n_ = 0;  // rows of the x / y the row map indexes (K1 bounds)
+  int64_t row_step_ = kRowStep;  // folds pad to, and segments align on, this many rows
   bool small_ = false;  // small-fold mode (every fold <= kSmallFoldRows rows; see plan_segments)
   bool bound_ = false, grammed_ = false;
   bool rank_mode_ = false, emits_ = true;
@@ -174,7 +178,7 @@ class Plan {
   TreeProgram group_tree_;
   DevBuf zero_g_, zero_nval_, zero_ptr_;
 
-  DevBuf tiles_d_, out_tiles_d_, tiles128_d_, zt_hi_, zt_lo_, tile_counts_, fold_counts_, bad_, zbase_d_, src_row_, z_, part_, foldbuf_, local_,
+  DevBuf tiles_d_, out_tiles_d_, tiles128_d_, zt_hi_, zt_lo_, unscale_, tile_counts_, fold_counts_, bad_, zbase_d_, src_row_, z_, part_, foldbuf_, local_,
       total_, shift_, flag_, tiles_bycol_d_, src_map_, segs_d_, foldptr_d_, nval_d_, st_mz_, st_sT_, st_sd_, cfg_d_;
   TreeProgram fold_tree_, local_tree_, rank_tree_;
   PinnedStage seg_stage_, ptr_stage_, shift_stage_, cfg_stage_, col_stage_;

@@ -29,9 +29,12 @@
 #include <cuda.h>
 
 #include "cvg_internal.cuh"
+#include "tc_util.cuh"
 
 namespace cvg {
 namespace {
+
+using namespace tc;
 
 constexpr int TT = 128;                       // tile edge (M = N = 128)
 constexpr int KS = 32;                        // rows per stage = 128 B of fp32
@@ -43,48 +46,6 @@ constexpr int kDrainSteps = 4;                // 128 rows per fp32 accumulation 
 constexpr int kEpiWarps = 8;                  // 4 TMEM lane quarters x 2 column halves
 constexpr int kThreads = 64 + 32 * kEpiWarps;
 
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
-}
-
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred P1;\n"
-      "WAIT:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
-      "@P1 bra DONE;\n"
-      "bra WAIT;\n"
-      "DONE:\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
-               : "memory");
-}
-
-__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
-                                            int c2) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];\n" ::
-          "r"(smem_u32(dst)),
-      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
-      : "memory");
-}
-
-// K-major, 128B-swizzled operand: 8-row atoms of 1024 B (SBO), version 1 (sm_100).
-__device__ __forceinline__ uint64_t kmajor_sw128_desc(const void* tile) {
-  const uint64_t addr = smem_u32(tile);
-  return ((addr >> 4) & 0x3FFFull) | (1ull << 16) | ((1024ull >> 4) << 32) | (1ull << 46) | (2ull << 61);
-}
 
 // kind::tf32, fp32 accumulate, both operands K-major, M = N = 128.
 constexpr uint32_t kIdescTf32 = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(TT >> 3) << 17) |
@@ -100,23 +61,6 @@ __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b
       "l"(a), "l"(b), "r"(kIdescTf32), "r"(accumulate));
 }
 
-__device__ __forceinline__ void mma_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(smem_u32(bar))
-               : "memory");
-}
-
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
-      "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];\n"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
-        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
-        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-      : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-}
-
 __global__ void __launch_bounds__(kThreads, 1)
     gram_tf32_kernel(const __grid_constant__ CUtensorMap map_hi, const __grid_constant__ CUtensorMap map_lo,
                      const GramTask* __restrict__ segs, const int2* __restrict__ tiles, int ntiles, int64_t kp,
@@ -127,9 +71,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   __shared__ uint32_t tmem_base;
 
   const int seg = blockIdx.x / ntiles;
-  const int2 tile = tiles[blockIdx.x - seg * ntiles];
+  const int2 tile0 = tiles[blockIdx.x - seg * ntiles];
+  const int2 tile = make_int2(uniform(tile0.x), uniform(tile0.y));
   const bool diag = tile.x == tile.y;
-  const GramTask task = segs[seg];
+  const GramTask task0 = segs[seg];
+  const GramTask task{uniform(task0.zrow), uniform(task0.rows)};
   CVG_DCHECK(task.zrow % KS == 0 && task.rows % KS == 0 && task.rows > 0);
   CVG_DCHECK(tile.x >= 0 && tile.x <= tile.y && (int64_t)(tile.y + 1) * TT <= kp);
   const int nsteps = (int)(task.rows / KS);
@@ -155,19 +101,19 @@ __global__ void __launch_bounds__(kThreads, 1)
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-  const uint32_t tmem_d = tmem_base;
+  const uint32_t tmem_d = uniform(tmem_base);
 
   auto op = [&](int s, int which) { return smem + s * kStageBytes + which * kOpBytes; };  // 0 Ahi 1 Alo 2 Bhi 3 Blo
 
-  if (warp == 0) {
-    if (lane == 0) {  // ---- TMA producer
-      const uint32_t bytes = (uint32_t)kOpBytes * (nterms == 3 ? 2u : 1u) * (diag ? 1u : 2u);
-      for (int it = 0; it < nsteps; ++it) {
-        const int s = it % NST;
-        const uint32_t ph = (uint32_t)(it / NST) & 1u;
-        mbar_wait(&empty_bar[s], ph ^ 1u);
+  if (warp == 0) {  // ---- TMA producer (whole warp waits; one elected lane issues)
+    const uint32_t bytes = (uint32_t)kOpBytes * (nterms == 3 ? 2u : 1u) * (diag ? 1u : 2u);
+    for (int it = 0; it < nsteps; ++it) {
+      const int s = it % NST;
+      const uint32_t ph = (uint32_t)(it / NST) & 1u;
+      mbar_wait(&empty_bar[s], ph ^ 1u);
+      const int blk = (int)(task.zrow / KS) + it;  // 32-row block index
+      if (elect_one()) {
         mbar_expect_tx(&full_bar[s], bytes);
-        const int blk = (int)(task.zrow / KS) + it;  // 32-row block index
         tma_load_3d(op(s, 0), &map_hi, &full_bar[s], 0, tile.x * TT, blk);
         if (nterms == 3) tma_load_3d(op(s, 1), &map_lo, &full_bar[s], 0, tile.x * TT, blk);
         if (!diag) {
@@ -175,21 +121,22 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (nterms == 3) tma_load_3d(op(s, 3), &map_lo, &full_bar[s], 0, tile.y * TT, blk);
         }
       }
+      __syncwarp();
     }
-  } else if (warp == 1) {
-    if (lane == 0) {  // ---- MMA issuer, accumulator b = chunk & 1
-      for (int it = 0; it < nsteps; ++it) {
-        const int chunk = it / kDrainSteps, b = chunk & 1;
-        const bool first = it % kDrainSteps == 0;
-        if (first && chunk >= 2) mbar_wait(&acc_empty[b], (uint32_t)((chunk >> 1) - 1) & 1u);  // drained
-        const int s = it % NST;
-        const uint32_t ph = (uint32_t)(it / NST) & 1u;
-        mbar_wait(&full_bar[s], ph);
-        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-        const uint32_t acc = tmem_d + (uint32_t)(b * TT);
-        const uint64_t a_hi = kmajor_sw128_desc(op(s, 0)), a_lo = kmajor_sw128_desc(op(s, 1));
-        const uint64_t b_hi = diag ? a_hi : kmajor_sw128_desc(op(s, 2));
-        const uint64_t b_lo = diag ? a_lo : kmajor_sw128_desc(op(s, 3));
+  } else if (warp == 1) {  // ---- MMA issuer (whole warp waits; one elected lane issues), accumulator b = chunk & 1
+    for (int it = 0; it < nsteps; ++it) {
+      const int chunk = it / kDrainSteps, b = chunk & 1;
+      const bool first = it % kDrainSteps == 0;
+      if (first && chunk >= 2) mbar_wait(&acc_empty[b], (uint32_t)((chunk >> 1) - 1) & 1u);  // drained
+      const int s = it % NST;
+      const uint32_t ph = (uint32_t)(it / NST) & 1u;
+      mbar_wait(&full_bar[s], ph);
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+      const uint32_t acc = tmem_d + (uint32_t)(b * TT);
+      const uint64_t a_hi = kmajor_sw128_desc(op(s, 0)), a_lo = kmajor_sw128_desc(op(s, 1));
+      const uint64_t b_hi = diag ? a_hi : kmajor_sw128_desc(op(s, 2));
+      const uint64_t b_lo = diag ? a_lo : kmajor_sw128_desc(op(s, 3));
+      if (elect_one()) {
 #pragma unroll
         for (int k = 0; k < KS / 8; ++k) {  // K = 8 tf32 = 32 B per MMA: +2 in 16-byte descriptor units
           const uint64_t dk = 2ull * k;
@@ -202,6 +149,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         mma_commit(&empty_bar[s]);  // frees the stage once these MMAs have read it
         if (it % kDrainSteps == kDrainSteps - 1 || it == nsteps - 1) mma_commit(&acc_full[b]);
       }
+      __syncwarp();
     }
   } else {  // ---- drain warps: fp32 TMEM chunks -> fp64 registers -> fp64 partial
     const int q = warp & 3;            // TMEM lanes [32q, 32q + 32) (hardware: warp id mod 4)
@@ -222,7 +170,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
       __syncwarp();
-      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(&acc_empty[b])) : "memory");
+      if (lane == 0) mbar_arrive(&acc_empty[b]);
     }
     const int64_t row = (int64_t)tile.x * TT + 32 * q + lane;
     double* out = part + (int64_t)seg * kp * kp + row * kp + (int64_t)tile.y * TT + 64 * h;
@@ -519,35 +467,11 @@ __global__ void __launch_bounds__(256) reorder_split_t_kernel(const T* __restric
     }
     __syncthreads();
   }
-  if (__any_sync(0xffffffffu, bad) && (t & 31) == 0) atomicExch(nonfinite, 1);
-}
-
-typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
-EncodeTiledFn encode_fn() {
-  static EncodeTiledFn fn = nullptr;
-  if (!fn) {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<EncodeTiledFn>(p);
-  }
-  return fn;
+  if (__any_sync(0xffffffffu, bad) && (t & 31) == 0) atomicOr(nonfinite, 1);
 }
 
 bool make_map(CUtensorMap* map, const float* base, int64_t zrows, int64_t kp, int box_cols = TT) {
-  EncodeTiledFn enc = encode_fn();
-  if (!enc) return false;
-  const cuuint64_t dims[3] = {(cuuint64_t)KS, (cuuint64_t)kp, (cuuint64_t)(zrows / KS)};  // Zt[block][col][32]
-  const cuuint64_t strides[2] = {(cuuint64_t)KS * sizeof(float), (cuuint64_t)kp * KS * sizeof(float)};
-  const cuuint32_t box[3] = {KS, (cuuint32_t)box_cols, 1};
-  const cuuint32_t estr[3] = {1, 1, 1};
-  return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims, strides, box, estr,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  return make_blocked_map(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, base, 4, zrows, kp, box_cols);
 }
 
 }  // namespace

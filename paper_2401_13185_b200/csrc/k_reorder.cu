@@ -68,7 +68,7 @@ __global__ void __launch_bounds__(256) reorder_kernel(const T* __restrict__ x, i
       }
     }
   }
-  if (__any_sync(0xffffffffu, bad) && lane == 0) atomicExch(nonfinite, 1);
+  if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(nonfinite, 1);
 }
 
 template <typename T>

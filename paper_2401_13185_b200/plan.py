@@ -366,7 +366,7 @@ def gram_tiles(k: int, m: int, edge: int = 64):
 def executed_gram_flops(n: int, k: int, m: int, p: int, f32: bool = False) -> float:
     """Tensor-core flops the Gram kernel issues for n rows (fold padding ignored):
     fp64: 64x64 DMMA tiles, diagonal tiles only their 36 upper 8x8 blocks;
-    fp32: 128x128 tcgen05 tiles x 3 TF32 products."""
+    fp32: 128x128 tcgen05 tiles x 3 products (fp16 hi/lo split by default, TF32 with CVG_FP32_KIND=tf32)."""
     if f32:
         return 3 * 2.0 * len(gram_tiles(k, m, 128)) * 128 * 128 * n
     tiles = gram_tiles(k, m)
