@@ -209,36 +209,55 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 // K1H: bucket, shift, scale, fp16-split, transpose into Zh[block][col][64] (HBM-bound).
-// One CTA per G bucketed rows; 128-column chunks.  Warp w / lane l hold columns
-// c0 + l + 32e (e < 4) of the row pairs (2w + 32j, 2w + 1 + 32j): every load is a
-// coalesced 128-byte row segment, a column's group max is a 16-warp reduction
-// in shared memory, and each (hi, lo) row pair is one 32-bit shared-memory word
-// (column pitch G/2 + 1 words: the transposed writes hit 32 distinct banks).
+// One CTA per G bucketed rows, two CTAs per SM (one loads while the other
+// computes); 64-column chunks.  Lane (h, cq) = (lane >> 4, lane & 15) holds the 4
+// adjacent columns c0 + 4cq .. + 3 (one 16-byte load per row: a warp reads two
+// 256-byte row segments) of the row pairs rp = 2w + h + 32j of warp w.  A column's
+// group max is a 32-way reduction in shared memory; each (hi, lo) row pair is one
+// 32-bit word of a column-major shared tile whose row-pair index is XOR-swizzled
+// by the column quad (word = col * G/2 + (rp ^ 2(col >> 2))): the transposed
+// writes hit 32 distinct banks and the write-out reads 16-byte blocks
+// conflict-free, so the output leaves as 16-byte stores (a warp: 4 columns x 128 B
+// contiguous).
 constexpr int kK1hThreads = 512;
 constexpr int kK1hWarps = kK1hThreads / 32;
-constexpr int kK1hCols = 128;
+constexpr int kK1hCols = 64;
 
 template <int G>
 constexpr int k1h_smem_bytes() {
-  return 2 * kK1hCols * (G / 2 + 1) * 4 + kK1hWarps * kK1hCols * 4 + kK1hCols * 4 + G * 8;
+  return 2 * kK1hCols * (G / 2) * 4 + 2 * kK1hWarps * kK1hCols * 4 + kK1hCols * 4 + G * 8;
+}
+
+template <typename T>
+__device__ __forceinline__ void load4(const T* p, float (&v)[4]) {
+  if constexpr (sizeof(T) == 4) {
+    const float4 q = __ldg(reinterpret_cast<const float4*>(p));
+    v[0] = q.x, v[1] = q.y, v[2] = q.z, v[3] = q.w;
+  } else {
+    const double2 a = __ldg(reinterpret_cast<const double2*>(p)), b = __ldg(reinterpret_cast<const double2*>(p) + 1);
+    v[0] = (float)a.x, v[1] = (float)a.y, v[2] = (float)b.x, v[3] = (float)b.y;
+  }
 }
 
 template <typename T, int G>
-__global__ void __launch_bounds__(kK1hThreads) reorder_split_h_kernel(
+__global__ void __launch_bounds__(kK1hThreads, 2) reorder_split_h_kernel(
     const T* __restrict__ x, int64_t ldx, const T* __restrict__ y, int64_t ldy, int64_t k, int64_t m,
     const int64_t* __restrict__ src_row, int64_t zrows, int64_t kp, int64_t c_begin, int64_t c_end, int64_t nsrc,
     const double* __restrict__ shift, __half* __restrict__ zh_hi, __half* __restrict__ zh_lo,
     float* __restrict__ unscale, int* __restrict__ nonfinite) {
-  constexpr int S = G / 2 + 1;  // words per column (row pairs + 1 pad)
-  constexpr int NJ = G / 32;    // row pairs per thread per column
+  constexpr int S = G / 2;    // words (row pairs) per column
+  constexpr int NJ = G / 64;  // row pairs per thread
+  constexpr int kSlots = 2 * kK1hWarps;  // row-pair slots per 32 row pairs (= 32)
   extern __shared__ __align__(16) uint8_t k1h_smem[];
   uint32_t* s_hi = reinterpret_cast<uint32_t*>(k1h_smem);
   uint32_t* s_lo = s_hi + kK1hCols * S;
-  float* s_max = reinterpret_cast<float*>(s_lo + kK1hCols * S);  // [warps][cols]
-  float* s_scale = s_max + kK1hWarps * kK1hCols;                  // [cols] 2^e
+  float* s_max = reinterpret_cast<float*>(s_lo + kK1hCols * S);  // [slot][cols]
+  float* s_scale = s_max + kSlots * kK1hCols;                     // [cols] 2^e
   int64_t* s_src = reinterpret_cast<int64_t*>(s_scale + kK1hCols);
   const int64_t grp = blockIdx.x;
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  const int h = lane >> 4, cq = lane & 15;
+  const int slot = 2 * w + h;  // this thread's row pairs: slot + 32j
   const int64_t wd = k + m;
   CVG_DCHECK(c_begin >= 0 && c_end <= kp && c_begin % kK1hCols == 0 && zrows % G == 0);
   for (int i = t; i < G; i += kK1hThreads) {
@@ -248,44 +267,35 @@ __global__ void __launch_bounds__(kK1hThreads) reorder_split_h_kernel(
     s_src[i] = src;
   }
   __syncthreads();
-  // This thread's rows 2w + p + 32j (source row indices), and whether all are real rows.
-  int32_t xr[NJ][2];
   bool all_real = true;
 #pragma unroll
   for (int j = 0; j < NJ; ++j)
 #pragma unroll
-    for (int p = 0; p < 2; ++p) {
-      const int64_t src = s_src[2 * w + p + 32 * j];
-      all_real &= src >= 0;
-      xr[j][p] = (int32_t)(src >= 0 ? src : 0);  // row counts are < 2^31 (cvg_plan validates n)
-    }
+    for (int p = 0; p < 2; ++p) all_real &= s_src[2 * (slot + 32 * j) + p] >= 0;
+  // 16-byte row loads need 16-byte aligned rows
+  const bool vec_ok = (ldx * (int64_t)sizeof(T)) % 16 == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0;
   float nan_acc = 0.f;  // v * 0 is NaN exactly when v is not finite
   bool too_big = false;
   float v[NJ][2][4];
-  // Fast chunks (every column an X column, every row real): no per-element checks.
-  auto fast_chunk = [&](int64_t c0) { return all_real && c0 + kK1hCols <= k; };
+  // Fast chunks (every column an X column, every row real, aligned rows): no per-element checks.
+  auto fast_chunk = [&](int64_t c0) { return all_real && vec_ok && c0 + kK1hCols <= k; };
   auto load_chunk = [&](int64_t c0) {
     if (fast_chunk(c0)) {
 #pragma unroll
       for (int j = 0; j < NJ; ++j)
 #pragma unroll
         for (int p = 0; p < 2; ++p)
-#pragma unroll
-          {
-            const T* rp = x + (int64_t)xr[j][p] * ldx + c0 + lane;
-#pragma unroll
-            for (int e = 0; e < 4; ++e) v[j][p][e] = (float)__ldg(rp + 32 * e);
-          }
+          load4(x + (int64_t)(int32_t)s_src[2 * (slot + 32 * j) + p] * ldx + c0 + 4 * cq, v[j][p]);
       return;
     }
 #pragma unroll
     for (int j = 0; j < NJ; ++j)
 #pragma unroll
       for (int p = 0; p < 2; ++p) {
-        const int64_t src = s_src[2 * w + p + 32 * j];
+        const int64_t src = s_src[2 * (slot + 32 * j) + p];
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-          const int64_t ce = c0 + lane + 32 * e;
+          const int64_t ce = c0 + 4 * cq + e;
           float val = 0.f;
           if (src >= 0) {
             if (ce < k)
@@ -302,39 +312,29 @@ __global__ void __launch_bounds__(kK1hThreads) reorder_split_h_kernel(
   load_chunk(c_begin);
   for (int64_t c0 = c_begin; c0 < c_end; c0 += kK1hCols) {
     // shift; per-column max |z| over this thread's rows
+    const bool fast = fast_chunk(c0);
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      const int64_t ce = c0 + lane + 32 * e;
+      const int64_t ce = c0 + 4 * cq + e;
       const float sh = ce < wd ? (float)__ldg(shift + ce) : 0.f;  // ones / padding columns: no shift
       float mx = 0.f;
-      if (fast_chunk(c0)) {
 #pragma unroll
-        for (int j = 0; j < NJ; ++j)
+      for (int j = 0; j < NJ; ++j)
 #pragma unroll
-          for (int p = 0; p < 2; ++p) {
-            nan_acc = fmaf(v[j][p][e], 0.f, nan_acc);
-            const float z = v[j][p][e] - sh;
-            v[j][p][e] = z;
-            mx = fmaxf(mx, fabsf(z));
-          }
-      } else {
-#pragma unroll
-        for (int j = 0; j < NJ; ++j)
-#pragma unroll
-          for (int p = 0; p < 2; ++p) {
-            nan_acc = fmaf(v[j][p][e], 0.f, nan_acc);
-            const float z = (s_src[2 * w + p + 32 * j] >= 0 && ce < wd) ? v[j][p][e] - sh : v[j][p][e];
-            v[j][p][e] = z;
-            mx = fmaxf(mx, fabsf(z));
-          }
-      }
-      s_max[w * kK1hCols + lane + 32 * e] = mx;
+        for (int p = 0; p < 2; ++p) {
+          nan_acc = fmaf(v[j][p][e], 0.f, nan_acc);
+          const bool shifted = fast || (s_src[2 * (slot + 32 * j) + p] >= 0 && ce < wd);
+          const float z = shifted ? v[j][p][e] - sh : v[j][p][e];
+          v[j][p][e] = z;
+          mx = fmaxf(mx, fabsf(z));
+        }
+      s_max[slot * kK1hCols + 4 * cq + e] = mx;
     }
     __syncthreads();
     if (t < kK1hCols) {
       float mx = 0.f;
 #pragma unroll
-      for (int i = 0; i < kK1hWarps; ++i) mx = fmaxf(mx, s_max[i * kK1hCols + t]);
+      for (int i = 0; i < kSlots; ++i) mx = fmaxf(mx, s_max[i * kK1hCols + t]);
       // e: the group's max |z| scaled into [2^14, 2^15); zero / non-finite columns keep e = 0
       int ex = 0;
       if (mx > 0.f && isfinite(mx)) {
@@ -347,10 +347,11 @@ __global__ void __launch_bounds__(kK1hThreads) reorder_split_h_kernel(
       unscale[grp * kp + c0 + t] = __uint_as_float((uint32_t)(127 - ex) << 23);
     }
     __syncthreads();
-    // scale (exact) and split: hi = fp16_rn(z'), lo = fp16_rn(z' - hi); one word per row pair
+    // scale (exact) and split: hi = fp16_rn(z'), lo = fp16_rn(z' - hi); one word per row pair,
+    // at col * S + (rp ^ 2cq) (col >> 2 == cq)
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      const int col = lane + 32 * e;
+      const int col = 4 * cq + e;
       const float sc = s_scale[col];
 #pragma unroll
       for (int j = 0; j < NJ; ++j) {
@@ -358,21 +359,30 @@ __global__ void __launch_bounds__(kK1hThreads) reorder_split_h_kernel(
         const __half2 hi = __floats2half2_rn(z0, z1);
         const float2 hf = __half22float2(hi);
         const __half2 lo = __floats2half2_rn(z0 - hf.x, z1 - hf.y);
-        s_hi[col * S + w + 16 * j] = *reinterpret_cast<const uint32_t*>(&hi);
-        s_lo[col * S + w + 16 * j] = *reinterpret_cast<const uint32_t*>(&lo);
+        const int word = col * S + ((slot + 32 * j) ^ (2 * cq));
+        s_hi[word] = *reinterpret_cast<const uint32_t*>(&hi);
+        s_lo[word] = *reinterpret_cast<const uint32_t*>(&lo);
       }
     }
     __syncthreads();
     if (c0 + kK1hCols < c_end) load_chunk(c0 + kK1hCols);  // in flight while the stores below drain
-    // write: one warp per (64-row block, column) = 128 B of hi and 128 B of lo
-    uint32_t* ohi = reinterpret_cast<uint32_t*>(zh_hi) + (grp * (G / 64) * kp + c0) * 32 + lane;
-    uint32_t* olo = reinterpret_cast<uint32_t*>(zh_lo) + (grp * (G / 64) * kp + c0) * 32 + lane;
-#pragma unroll 4
-    for (int task = w; task < (G / 64) * kK1hCols; task += kK1hWarps) {
-      const int b = task / kK1hCols, col = task - b * kK1hCols;
-      const int64_t off = ((int64_t)b * kp + col) * 32;  // words
-      ohi[off] = s_hi[col * S + 32 * b + lane];
-      olo[off] = s_lo[col * S + 32 * b + lane];
+    // write: task = (64-row block b, column quad q): lane i -> column 4q + i / 8, words 4(i % 8) .. + 3
+    // of the block (16 B; a warp stores 4 columns x 128 B contiguous) for hi and for lo.
+    const int mq = lane & 7, cl = lane >> 3;
+#pragma unroll 2
+    for (int task = w; task < (G / 64) * (kK1hCols / 4); task += kK1hWarps) {
+      const int b = task / (kK1hCols / 4), q = task - b * (kK1hCols / 4);
+      const int col = 4 * q + cl;
+      // row pairs 32b + 4mq + r (r < 4) are stored at 32b + ((4mq + r) ^ 2q): one 16-B block, words permuted
+      const int word = col * S + 32 * b + 4 * (mq ^ (q >> 1));
+      const uint4 hv = *reinterpret_cast<const uint4*>(s_hi + word);
+      const uint4 lv = *reinterpret_cast<const uint4*>(s_lo + word);
+      const bool sw = q & 1;  // warp-uniform: words r ^ 2
+      const uint4 ho = sw ? make_uint4(hv.z, hv.w, hv.x, hv.y) : hv;
+      const uint4 lo = sw ? make_uint4(lv.z, lv.w, lv.x, lv.y) : lv;
+      const int64_t off = ((grp * (G / 64) + b) * kp + c0 + col) * 32 + 4 * mq;  // words
+      *reinterpret_cast<uint4*>(reinterpret_cast<uint32_t*>(zh_hi) + off) = ho;
+      *reinterpret_cast<uint4*>(reinterpret_cast<uint32_t*>(zh_lo) + off) = lo;
     }
     __syncthreads();
   }
