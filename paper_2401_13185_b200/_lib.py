@@ -11,9 +11,10 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-# CVG_LIB_VARIANT=checked loads the bounds-checked build (make CHECKED=1 -> _build_checked/).
+# CVG_LIB_VARIANT=checked loads the bounds-checked build (make CHECKED=1 -> _build_checked/);
+# any other name loads _build_<name>/ (make OUT=_build_<name> EXTRA=-D...: experiment builds).
 _VARIANT = os.environ.get("CVG_LIB_VARIANT", "")
-LIB_PATH = os.path.join(_HERE, "_build_checked" if _VARIANT == "checked" else "_build", "libcvgram_b200.so")
+LIB_PATH = os.path.join(_HERE, f"_build_{_VARIANT}" if _VARIANT else "_build", "libcvgram_b200.so")
 
 OK, E_DIMENSION, E_PARTITION, E_SCALABILITY, E_INVALID_ARG, E_CUDA, E_OOM = 0, 1, 2, 3, 4, 5, 6
 DTYPE_F64, DTYPE_F32 = 0, 1

@@ -218,6 +218,15 @@ static bool tf32_2sm() {
   return v;
 }
 
+// fp16 Gram on CTA pairs (cta_group::2): CVG_F16_2SM=1.
+static bool f16_2sm() {
+  static const bool v = [] {
+    const char* e = std::getenv("CVG_F16_2SM");
+    return e && e[0] == '1';
+  }();
+  return v;
+}
+
 // fp32 operand kind: the scaled fp16 split on kind::f16 (default) or, with
 // CVG_FP32_KIND=tf32, the 3xTF32 split on kind::tf32 (k_gram_tf32.cu; A/B tests).
 bool Plan::fp32_tf32() {
@@ -638,7 +647,11 @@ Status Plan::gram(const void* d_x, int64_t ldx, const void* d_y, int64_t ldy, co
       bool ok;
       {
         Timed t(ctx_, kGram);
-        ok = f16_path()
+        ok = f16_path() && f16_2sm()
+                 ? launch_gram_f16s_2sm(zt_hi_.as<void>(), zt_lo_.as<void>(), unscale_.as<float>(), (int)row_step_,
+                                        zrows_, kp_, segs_d_.as<GramTask>(), (int64_t)segs_.size(),
+                                        pairs128_d_.as<int4>(), (int)pairs128_.size(), part_.as<double>(), s)
+             : f16_path()
                  ? launch_gram_f16s(zt_hi_.as<void>(), zt_lo_.as<void>(), unscale_.as<float>(), (int)row_step_,
                                     zrows_, kp_, segs_d_.as<GramTask>(), (int64_t)segs_.size(),
                                     tiles128_d_.as<int2>(), (int)tiles128_.size(), part_.as<double>(), s)

@@ -1,5 +1,5 @@
 set -e; make -s -C paper_2401_13185_b200 >/dev/null; set +e
-timeout 600 python -m pytest tests/test_gpu_parity.py -q -m gpu -x -k "accumulation_range or nonfinite" 2>&1 | tail -2
-python bench.py --config 3 --steps 1 --warmup 1 --no-cpu-baseline --no-e2e > gpurun_out/plain3.log 2>&1; echo "plain rc=$?"
-ncu --set full --clock-control none --import-source on -k regex:"reorder_split_h" -c 1 -o gpurun_out/prof_k1h_b \
-  python bench.py --config 3 --steps 1 --warmup 1 --no-cpu-baseline --no-e2e > gpurun_out/ncu_k1h.log 2>&1; echo "ncu rc=$?"
+for v in "" nodrain; do
+  CVG_LIB_VARIANT=$v python bench.py --config 3 --steps 3 --warmup 2 --no-cpu-baseline --no-e2e > gpurun_out/exp_$v.log 2>&1; echo "$v rc=$?"
+  tail -1 gpurun_out/exp_$v.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('[$v]', d['ms_per_step'], d.get('kernels_ms_per_step'))"
+done
