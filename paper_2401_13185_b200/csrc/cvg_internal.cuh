@@ -29,10 +29,14 @@ constexpr int kRowStep = 32;       // rows per pipeline stage; fold blocks pad t
 // segments, Plan::seg_rows).  8192 vs 32768: c1 10.70 vs 10.81 ms (two even CTAs per fold fill the
 // last wave better), c4 45.4 vs 45.8.
 constexpr int64_t kChunkRows = 8192;
-// fp32 segments: shorter than fp64 so the 45 tcgen05 tiles of a segment (kp 1152 at c3) re-read
-// less from DRAM (c3 sweep: 32768 -> 44.9 ms, 16384 -> 44.5, 12288 -> 42.9, 8192 -> 44.2: the
-// tree over more partials eats the rest).
-constexpr int64_t kChunkRowsF32 = 12288;
+// fp32 segments (fp16 hi/lo operands: 4 B per Z element, half of fp64's): c3 sweep of the total step
+// with the kind::f16 Gram: 8192 -> 27.8 ms, 12288 -> 26.7, 16384 -> 26.4, 24576 -> 25.3, 32768 -> 25.1,
+// 49152 -> 25.8, 65536 -> 25.2 (the fold tree shrinks from 1.30 to 0.19 ms; the Gram is flat within noise
+// up to 32768 rows).  A multiple of every fp16 row group (64 / 128 / 256).
+constexpr int64_t kChunkRowsF32 = 32768;
+// 3xTF32 operands (CVG_FP32_KIND=tf32, 8 B per element): 32768 -> 44.9 ms, 16384 -> 44.5, 12288 -> 42.9,
+// 8192 -> 44.2 on c3 (shorter segments re-read less from DRAM; the tree over more partials eats the rest).
+constexpr int64_t kChunkRowsTf32 = 12288;
 constexpr int kTileF32 = 128;             // tcgen05 tile edge (M = N = 128)
 constexpr int kTileRowsPerWarp = 1024; // rows per warp in the bucketing passes
 

@@ -265,7 +265,7 @@ int64_t Plan::chunk_rows() const {
     return (int64_t)(r > 0 ? r : 0);
   }();
   if (env > 0) return round_up(env, row_step_);
-  return round_up(dtype_ == 1 ? kChunkRowsF32 : kChunkRows, row_step_);
+  return round_up(dtype_ == 0 ? kChunkRows : f16_path() ? kChunkRowsF32 : kChunkRowsTf32, row_step_);
 }
 
 // Rows per segment of a fold of `count` rows: the fold is cut into
