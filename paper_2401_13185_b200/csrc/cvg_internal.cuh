@@ -37,6 +37,9 @@ constexpr int64_t kChunkRowsF32 = 32768;
 // 3xTF32 operands (CVG_FP32_KIND=tf32, 8 B per element): 32768 -> 44.9 ms, 16384 -> 44.5, 12288 -> 42.9,
 // 8192 -> 44.2 on c3 (shorter segments re-read less from DRAM; the tree over more partials eats the rest).
 constexpr int64_t kChunkRowsTf32 = 12288;
+// int8-slice fp64 Gram (CVG_FP64_KIND=i8): exact int32 TMEM sums need S * 4096 * rows < 2^31
+// (rows < 74,898 at S = 7); the exponent is per (segment, column).
+constexpr int64_t kChunkRowsI8 = 32768;
 constexpr int kTileF32 = 128;             // tcgen05 tile edge (M = N = 128)
 constexpr int kTileRowsPerWarp = 1024; // rows per warp in the bucketing passes
 
@@ -174,6 +177,21 @@ bool launch_gram_tf32(const float* zt_hi, const float* zt_lo, int64_t zrows, int
 // covers row blocks 2a, 2a+1 (128 wide) x column block j; writeN: that CTA's tile is needed.
 bool launch_gram_tf32_2sm(const float* zt_hi, const float* zt_lo, int64_t zrows, int64_t kp, const GramTask* segs,
                           int64_t nseg, const int4* pairs, int npairs, double* part, cudaStream_t s);
+
+// K1Q + K2q (fp64, CVG_FP64_KIND=i8; k_gram_i8.cu): per-(segment, column) exponents from the
+// segment's max |z| (segmax), then bucket/shift/scale/cut into `slices` int8 digits laid out
+// Zq[t][row / 64][col][64]; the tcgen05 kind::i8 Gram sums the slice pairs t + u < slices into
+// int32 TMEM and drains each (segment, 128 x 64 tile) once into the fp64 partial.
+// blkseg[b]: segment of Z's 64-row block b.  tiles: {I, J | write mask << 16}.
+void launch_segmax(int dtype, const void* x, int64_t ldx, const void* y, int64_t ldy, int64_t k, int64_t m,
+                   const int64_t* src_row, const GramTask* segs, int64_t nseg, int64_t kp, int64_t c_begin,
+                   int64_t c_end, int64_t nsrc, const double* shift, int* segexp, cudaStream_t s);
+void launch_reorder_q(int dtype, int slices, const void* x, int64_t ldx, const void* y, int64_t ldy, int64_t k,
+                      int64_t m, const int64_t* src_row, int64_t zrows, int64_t kp, int64_t c_begin, int64_t c_end,
+                      int64_t nsrc, const double* shift, const int* blkseg, const int* segexp, int8_t* zq,
+                      int* nonfinite, cudaStream_t s);
+bool launch_gram_i8(int slices, const int8_t* zq, const int* segexp, int64_t zrows, int64_t kp, const GramTask* segs,
+                    int64_t nseg, const int2* tiles, int ntiles, double* part, cudaStream_t s);
 
 inline int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
 inline int64_t padded_cols(int64_t k, int64_t m, int dtype = 0) {

@@ -237,12 +237,24 @@ bool Plan::fp32_tf32() {
   return v;
 }
 
+// fp64 operand kind: int8 digit slices on kind::i8 (CVG_FP64_KIND=i8) or DMMA (dmma).
+// Read at plan creation, so one process can A/B both.
+static bool fp64_i8_env() {
+  const char* e = std::getenv("CVG_FP64_KIND");
+  return e && std::string(e) == "i8";
+}
+static int i8_slices_env() {
+  const char* e = std::getenv("CVG_I8_SLICES");
+  return e && std::atoi(e) == 6 ? 6 : 7;
+}
+
 // The fp16 path's row group G (one exponent per group and column, one fp32 TMEM
 // chunk) is also the fold padding and segment alignment.  Largest of 256 / 128 /
 // 64 whose padding stays within 1/8 of the 64-row minimum; a function of the
 // global fold sizes only, so every rank plan picks the same G.
 void Plan::choose_row_step() {
   row_step_ = kRowStep;
+  if (dtype_ == 0 && i8_) row_step_ = 64;  // one int8 Gram stage
   if (!f16_path()) return;
   auto padded = [&](int64_t g) {
     int64_t t = 0;
@@ -265,7 +277,8 @@ int64_t Plan::chunk_rows() const {
     return (int64_t)(r > 0 ? r : 0);
   }();
   if (env > 0) return round_up(env, row_step_);
-  return round_up(dtype_ == 0 ? kChunkRows : f16_path() ? kChunkRowsF32 : kChunkRowsTf32, row_step_);
+  return round_up(i8_path() ? kChunkRowsI8 : dtype_ == 0 ? kChunkRows : f16_path() ? kChunkRowsF32 : kChunkRowsTf32,
+                  row_step_);
 }
 
 // Rows per segment of a fold of `count` rows: the fold is cut into
@@ -310,6 +323,24 @@ Status Plan::create(cvg_context* ctx, int dtype, int64_t n, int64_t k, int64_t m
   kp_ = padded_cols(k, m, dtype);
   tiles_ = gram_tiles(k, m, kp_);
   tiles128_ = dtype == 1 ? gram_tiles(k, m, kp_, kTileF32) : std::vector<int2>{};
+  i8_ = dtype == 0 && fp64_i8_env();
+  slices_ = i8_slices_env();
+  tilesq_.clear();
+  if (i8_) {  // 128 x 64 int8-Gram tiles covering the needed upper 64-tiles (i, j): I = i / 2, J = j
+    for (const int2& t : tiles_) {
+      const int I = t.x / 2, bit = 1 << (t.x & 1);
+      int2* hit = nullptr;
+      for (int2& q : tilesq_)
+        if (q.x == I && (q.y & 0xffff) == t.y) hit = &q;
+      if (hit)
+        hit->y |= bit << 16;
+      else
+        tilesq_.push_back(make_int2(I, t.y | (bit << 16)));
+    }
+    CVG_TRY(tilesq_d_.ensure(tilesq_.size() * sizeof(int2)));
+    CVG_CK(cudaMemcpyAsync(tilesq_d_.as<int2>(), tilesq_.data(), tilesq_.size() * sizeof(int2), cudaMemcpyHostToDevice,
+                           ctx->stream));
+  }
   out_tiles_.clear();
   for (const int2& t : tiles_)
     if ((int64_t)t.x * kTile < k) out_tiles_.push_back(t);
@@ -432,6 +463,7 @@ Status Plan::bind_labels(const int32_t* d_labels, bool validate, bool require_sc
     return Status::Err(2, "label " + std::to_string(label) + " at sample " + std::to_string(bad + 1) +
                               " is outside {1.." + std::to_string(p_) + "}");
   }
+  small_ = false;
   if (validate) {
     for (int32_t f = 0; f < p_; ++f)
       if (counts_[f] == 0) return Status::Err(2, "fold " + std::to_string(f + 1) + " is empty");
@@ -532,6 +564,14 @@ Status Plan::plan_segments() {
     CVG_TRY(zt_hi_.ensure(e * std::max<int64_t>(zrows_, row_step_) * kp_));
     CVG_TRY(zt_lo_.ensure(e * std::max<int64_t>(zrows_, row_step_) * kp_));
     if (f16_path()) CVG_TRY(unscale_.ensure(sizeof(float) * std::max<int64_t>(zrows_ / row_step_, 1) * kp_));
+  } else if (i8_path()) {  // int8 digit slices, per-(segment, column) exponents, 64-row block -> segment
+    CVG_TRY(zq_.ensure((size_t)slices_ * std::max<int64_t>(zrows_, 64) * kp_));
+    CVG_TRY(segexp_.ensure(sizeof(int) * std::max<size_t>(segs_.size(), 1) * kp_));
+    std::vector<int> bs(std::max<int64_t>(zrows_ / 64, 1), 0);
+    for (size_t sgi = 0; sgi < segs_.size(); ++sgi)
+      for (int64_t r = segs_[sgi].zrow; r < segs_[sgi].zrow + segs_[sgi].rows; r += 64) bs[r / 64] = (int)sgi;
+    CVG_TRY(blkseg_.ensure(sizeof(int) * bs.size()));
+    CVG_TRY(blkseg_stage_.upload({{bs.data(), sizeof(int) * bs.size(), blkseg_.as<void>()}}, s));
   } else {
     CVG_TRY(z_.ensure(sizeof(double) * std::max<int64_t>(zrows_, 1) * kp_));
   }
@@ -666,6 +706,32 @@ Status Plan::gram(const void* d_x, int64_t ldx, const void* d_y, int64_t ldy, co
       if (!ok) return Status::Err(5, "cuTensorMapEncodeTiled unavailable or rejected the operand layout");
       CVG_TRY(count_launch());
     }
+  } else if (i8_path()) {
+    // fp64 on int8 digit slices: segment exponents, K1Q, tcgen05 kind::i8 Gram.
+    if (zrows_ > 0) {
+      {
+        Timed t(ctx_, kReorder);
+        launch_segmax(dtype_, d_x, ldx, d_y, ldy, k_, m_, rows, segs_d_.as<GramTask>(), (int64_t)segs_.size(), kp_, 0,
+                      kp_, nsrc, shift, segexp_.as<int>(), s);
+      }
+      CVG_TRY(count_launch());
+      {
+        Timed t(ctx_, kReorder);
+        launch_reorder_q(dtype_, slices_, d_x, ldx, d_y, ldy, k_, m_, rows, zrows_, kp_, 0, kp_, nsrc, shift,
+                         blkseg_.as<int>(), segexp_.as<int>(), zq_.as<int8_t>(), flag_.as<int>(), s);
+      }
+      CVG_TRY(count_launch());
+    }
+    if (!segs_.empty()) {
+      bool ok;
+      {
+        Timed t(ctx_, kGram);
+        ok = launch_gram_i8(slices_, zq_.as<int8_t>(), segexp_.as<int>(), zrows_, kp_, segs_d_.as<GramTask>(),
+                            (int64_t)segs_.size(), tilesq_d_.as<int2>(), (int)tilesq_.size(), part_.as<double>(), s);
+      }
+      if (!ok) return Status::Err(5, "cuTensorMapEncodeTiled unavailable or rejected the operand layout");
+      CVG_TRY(count_launch());
+    }
   } else {
     // fp64: K1 builds the fold-bucketed, shifted copy Z.  (Gathering X rows
     // straight into the Gram's shared-memory stages, or overlapping K1 with K2
@@ -710,7 +776,13 @@ Status Plan::gram_host(const void* h_x, const void* h_y, void* d_x, void* d_y, c
   const size_t e = dtype_ == 1 ? 4 : 8;
   const int E = dtype_ == 1 ? kTileF32 : kTile;
   const int nt = (int)(kp_ / E);
-  const std::vector<int2>& tl = dtype_ == 1 ? tiles128_ : tiles_;
+  const std::vector<int2>& tl = dtype_ == 1 ? tiles128_ : i8_path() ? tilesq_ : tiles_;
+  // the last 64-column block a tile reads (int8 tiles: the A rows they write, and J)
+  auto last_col = [&](const int2& t) {
+    if (!i8_path()) return t.y;
+    const int j = t.y & 0xffff;
+    return std::max(j, 2 * t.x + ((t.y >> 17) & 1));
+  };
   // Slabs (in tile columns): [0, nt/2), [nt/2, nt-1), [nt-1, nt).  Tiles touching
   // the last-arriving column are the only Gram work exposed after the final copy
   // (nt of the nt(nt+1)/2 upper tiles); wide early slabs keep the 2-D copies at
@@ -724,7 +796,7 @@ Status Plan::gram_host(const void* h_x, const void* h_y, void* d_x, void* d_y, c
   std::vector<int> off{0};
   for (size_t sl = 0; sl + 1 < bounds.size(); ++sl) {
     for (const int2& t : tl)
-      if (t.y >= bounds[sl] && t.y < bounds[sl + 1]) byslab.push_back(t);
+      if (last_col(t) >= bounds[sl] && last_col(t) < bounds[sl + 1]) byslab.push_back(t);
     off.push_back((int)byslab.size());
   }
   CVG_TRY(tiles_bycol_d_.ensure(sizeof(int2) * std::max<size_t>(byslab.size(), 1)));
@@ -756,10 +828,17 @@ Status Plan::gram_host(const void* h_x, const void* h_y, void* d_x, void* d_y, c
     if (zrows_ > 0) {
       {
         Timed t(ctx_, kReorder);
-        if (f16_path())
+        if (f16_path()) {
           launch_reorder_split_h(dtype_, d_x, k_, d_y, m_, k_, m_, src_row_.as<int64_t>(), zrows_, kp_, z0, z1, src_n_,
                                  shift, (int)row_step_, zt_hi_.as<void>(), zt_lo_.as<void>(), unscale_.as<float>(),
                                  flag_.as<int>(), s);
+        } else if (i8_path()) {
+          launch_segmax(dtype_, d_x, k_, d_y, m_, k_, m_, src_row_.as<int64_t>(), segs_d_.as<GramTask>(),
+                        (int64_t)segs_.size(), kp_, z0, z1, src_n_, shift, segexp_.as<int>(), s);
+          CVG_TRY(count_launch());
+          launch_reorder_q(dtype_, slices_, d_x, k_, d_y, m_, k_, m_, src_row_.as<int64_t>(), zrows_, kp_, z0, z1,
+                           src_n_, shift, blkseg_.as<int>(), segexp_.as<int>(), zq_.as<int8_t>(), flag_.as<int>(), s);
+        }
         else if (dtype_ == 1)
           launch_reorder_split_t(dtype_, d_x, k_, d_y, m_, k_, m_, src_row_.as<int64_t>(), zrows_, kp_, z0, z1, shift,
                                  zt_hi_.as<float>(), zt_lo_.as<float>(), flag_.as<int>(), s);
@@ -777,6 +856,9 @@ Status Plan::gram_host(const void* h_x, const void* h_y, void* d_x, void* d_y, c
           ok = launch_gram_f16s(zt_hi_.as<void>(), zt_lo_.as<void>(), unscale_.as<float>(), (int)row_step_, zrows_,
                                 kp_, segs_d_.as<GramTask>(), (int64_t)segs_.size(), tiles_bycol_d_.as<int2>() + t0,
                                 t1 - t0, part_.as<double>(), s);
+        else if (i8_path())
+          ok = launch_gram_i8(slices_, zq_.as<int8_t>(), segexp_.as<int>(), zrows_, kp_, segs_d_.as<GramTask>(),
+                              (int64_t)segs_.size(), tiles_bycol_d_.as<int2>() + t0, t1 - t0, part_.as<double>(), s);
         else if (dtype_ == 1)
           ok = launch_gram_tf32(zt_hi_.as<float>(), zt_lo_.as<float>(), zrows_, kp_, segs_d_.as<GramTask>(),
                                 (int64_t)segs_.size(), tiles_bycol_d_.as<int2>() + t0, t1 - t0, part_.as<double>(), 3,

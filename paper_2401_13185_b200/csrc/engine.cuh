@@ -153,6 +153,9 @@ class Plan {
   int64_t seg_rows(int64_t count) const;
   bool f16_path() const { return dtype_ == 1 && !fp32_tf32(); }
   static bool fp32_tf32();
+  // fp64 Gram on tcgen05 kind::i8 (int8 digit slices, k_gram_i8.cu); small-fold mode keeps
+  // the DMMA path (its epilogue reads fp64 Z rows).
+  bool i8_path() const { return dtype_ == 0 && i8_ && !small_; }
   void choose_row_step();  // fold padding / segment alignment (fp16 path: its row group G)
 
   cvg_context* ctx_ = nullptr;
@@ -161,6 +164,9 @@ class Plan {
   int32_t p_ = 0, fb_ = 0, fe_ = 0;
   std::vector<int2> tiles_, out_tiles_, tiles128_;
   std::vector<int4> pairs128_;  // CTA-pair tiles for the cta_group::2 fp32 Gram
+  std::vector<int2> tilesq_;    // int8 Gram tiles {I (128 rows), J (64 columns) | write mask << 16}
+  bool i8_ = false;             // fp64 kind: int8 slices (CVG_FP64_KIND=i8) or DMMA
+  int slices_ = 7;              // int8 digits per value (CVG_I8_SLICES = 6 or 7)
   DevBuf pairs128_d_;
   std::vector<int64_t> counts_;  // per fold (all p) validation sizes
   std::vector<GramTask> segs_;
@@ -178,10 +184,10 @@ class Plan {
   TreeProgram group_tree_;
   DevBuf zero_g_, zero_nval_, zero_ptr_;
 
-  DevBuf tiles_d_, out_tiles_d_, tiles128_d_, zt_hi_, zt_lo_, unscale_, tile_counts_, fold_counts_, bad_, zbase_d_, src_row_, z_, part_, foldbuf_, local_,
+  DevBuf zq_, segexp_, blkseg_, tilesq_d_, tiles_d_, out_tiles_d_, tiles128_d_, zt_hi_, zt_lo_, unscale_, tile_counts_, fold_counts_, bad_, zbase_d_, src_row_, z_, part_, foldbuf_, local_,
       total_, shift_, flag_, tiles_bycol_d_, src_map_, segs_d_, foldptr_d_, nval_d_, st_mz_, st_sT_, st_sd_, cfg_d_;
   TreeProgram fold_tree_, local_tree_, rank_tree_;
-  PinnedStage seg_stage_, ptr_stage_, shift_stage_, cfg_stage_, col_stage_;
+  PinnedStage blkseg_stage_, seg_stage_, ptr_stage_, shift_stage_, cfg_stage_, col_stage_;
   std::vector<const double*> fold_ptrs_;
 };
 
