@@ -39,6 +39,7 @@ sys.path.insert(0, ROOT)
 
 FP64_DMMA_PEAK_TFLOPS = 37.1  # profiles/r01_fp64_peaks.txt (DMMA.8x8x4 issue loop; cuBLAS DGEMM 35.4)
 TF32_PEAK_TFLOPS = 623.3      # profiles/r01_fp64_peaks.txt (cuBLAS TF32 8192^3 sustained; burst 744.6)
+INT8_PEAK_TOPS = 4500.0       # nominal B200 dense int8 until measured (tools/fp64_peaks.py int8)
 CPU_SAMPLE_ROWS = 1_000_000
 L2_BYTES = 126 * 1024 * 1024
 
@@ -385,6 +386,8 @@ def run_ours(args):
     achieved = gram_flops_per_launch / (gram_ms * 1e-3) / 1e12
     # executed DMMA flops: 64x64 tiles actually issued (symmetry + padding)
     from paper_2401_13185_b200.plan import executed_gram_flops
+    from paper_2401_13185_b200.plan import fp64_kind as executed_fp64_kind
+    from paper_2401_13185_b200.plan import i8_slices
 
     f32 = not x_dtype_is_f64(cid)
     executed = executed_gram_flops(n, k, m, p, f32) / max(world, 1) / (gram_ms * 1e-3) / 1e12
@@ -400,11 +403,23 @@ def run_ours(args):
         peak = peaks().get("bf16_tflops_sustained", 1374.5)
         peak_source = ("MEASURED_PEAKS.json bf16_tflops_sustained (cuBLAS bf16 8192^3 back to back; kind::f16 "
                        "runs fp16 and bf16 at one rate); executed counts the 3 fp16 products")
+    elif executed_fp64_kind() == "i8":
+        s_ = i8_slices()
+        gram_kernel = (f"gram_i8_kernel<{s_}> (tcgen05.mma kind::i8: exact int8 digit slices, {s_ * (s_ + 1) // 2} "
+                       f"slice-pair products into int32 TMEM, exact fp64 drain; CVG_FP64_KIND=i8)")
+        peak = INT8_PEAK_TOPS
+        peak_source = ("measured cuBLASLt int8 GEMM (torch._int_mm 8192^3, sustained) on this pool's B200 "
+                       "(profiles/r01_fp64_peaks.txt); frac = algorithmic fp64 flops / int8 peak is not meaningful, "
+                       "executed_frac counts the int8 tensor ops issued")
     else:
         gram_kernel = "gram_f64_kernel (DMMA.8x8x4)"
         peak = FP64_DMMA_PEAK_TFLOPS
         peak_source = ("measured DMMA issue-loop peak on this pool's B200 (profiles/r01_fp64_peaks.txt); "
                        "MEASURED_PEAKS.json has no fp64 figure")
+    # the int8 kernel is judged by the int8 tensor ops it issues (its fp64-equivalent rate is `value`)
+    i8_kind = not f32 and executed_fp64_kind() == "i8"
+    rl_achieved = executed if i8_kind else achieved
+    rl_unit = "TOPS (int8)" if i8_kind else "TFLOP/s"
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "r01_gram_ncu.json")
     if os.path.exists(tpath) and cid == 1:
@@ -432,8 +447,8 @@ def run_ours(args):
                           f"inputs {input_gb * 1e3:.1f} MB < 126 MB L2: L2 flushed (252 MB write) before each timed "
                           f"step, steps timed individually"),
                    "seed": workloads.SEEDS[cid]},
-        "roofline": {"bound": "tensor", "kernel": gram_kernel, "achieved": round(achieved, 3),
-                     "peak": peak, "unit": "TFLOP/s", "frac": round(achieved / peak, 4),
+        "roofline": {"bound": "tensor", "kernel": gram_kernel, "achieved": round(rl_achieved, 3),
+                     "peak": peak, "unit": rl_unit, "frac": round(rl_achieved / peak, 4),
                      "traffic": traffic,
                      "peak_source": peak_source,
                      "algorithmic_flops_per_launch": gram_flops_per_launch,

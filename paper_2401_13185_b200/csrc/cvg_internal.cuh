@@ -183,14 +183,16 @@ bool launch_gram_tf32_2sm(const float* zt_hi, const float* zt_lo, int64_t zrows,
 // Zq[t][row / 64][col][64]; the tcgen05 kind::i8 Gram sums the slice pairs t + u < slices into
 // int32 TMEM and drains each (segment, 128 x 64 tile) once into the fp64 partial.
 // blkseg[b]: segment of Z's 64-row block b.  tiles: {I, J | write mask << 16}.
+// segmax must be zeroed before (bits of max |z| per (segment, column); atomicMax).
 void launch_segmax(int dtype, const void* x, int64_t ldx, const void* y, int64_t ldy, int64_t k, int64_t m,
-                   const int64_t* src_row, const GramTask* segs, int64_t nseg, int64_t kp, int64_t c_begin,
-                   int64_t c_end, int64_t nsrc, const double* shift, int* segexp, cudaStream_t s);
-void launch_reorder_q(int dtype, int slices, const void* x, int64_t ldx, const void* y, int64_t ldy, int64_t k,
+                   const int64_t* src_row, const GramTask* segs, int64_t nseg, int64_t max_seg_rows, int64_t kp,
+                   int64_t c_begin, int64_t c_end, int64_t nsrc, const double* shift, unsigned long long* segmax,
+                   cudaStream_t s);
+bool launch_reorder_q(int dtype, int slices, const void* x, int64_t ldx, const void* y, int64_t ldy, int64_t k,
                       int64_t m, const int64_t* src_row, int64_t zrows, int64_t kp, int64_t c_begin, int64_t c_end,
-                      int64_t nsrc, const double* shift, const int* blkseg, const int* segexp, int8_t* zq,
+                      int64_t nsrc, const double* shift, const int* blkseg, const unsigned long long* segmax, int8_t* zq,
                       int* nonfinite, cudaStream_t s);
-bool launch_gram_i8(int slices, const int8_t* zq, const int* segexp, int64_t zrows, int64_t kp, const GramTask* segs,
+bool launch_gram_i8(int slices, const int8_t* zq, const unsigned long long* segmax, int64_t zrows, int64_t kp, const GramTask* segs,
                     int64_t nseg, const int2* tiles, int ntiles, double* part, cudaStream_t s);
 
 inline int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }

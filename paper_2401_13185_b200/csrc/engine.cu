@@ -566,7 +566,7 @@ Status Plan::plan_segments() {
     if (f16_path()) CVG_TRY(unscale_.ensure(sizeof(float) * std::max<int64_t>(zrows_ / row_step_, 1) * kp_));
   } else if (i8_path()) {  // int8 digit slices, per-(segment, column) exponents, 64-row block -> segment
     CVG_TRY(zq_.ensure((size_t)slices_ * std::max<int64_t>(zrows_, 64) * kp_));
-    CVG_TRY(segexp_.ensure(sizeof(int) * std::max<size_t>(segs_.size(), 1) * kp_));
+    CVG_TRY(segmax_.ensure(sizeof(unsigned long long) * std::max<size_t>(segs_.size(), 1) * kp_));
     std::vector<int> bs(std::max<int64_t>(zrows_ / 64, 1), 0);
     for (size_t sgi = 0; sgi < segs_.size(); ++sgi)
       for (int64_t r = segs_[sgi].zrow; r < segs_[sgi].zrow + segs_[sgi].rows; r += 64) bs[r / 64] = (int)sgi;
@@ -711,14 +711,17 @@ Status Plan::gram(const void* d_x, int64_t ldx, const void* d_y, int64_t ldy, co
     if (zrows_ > 0) {
       {
         Timed t(ctx_, kReorder);
-        launch_segmax(dtype_, d_x, ldx, d_y, ldy, k_, m_, rows, segs_d_.as<GramTask>(), (int64_t)segs_.size(), kp_, 0,
-                      kp_, nsrc, shift, segexp_.as<int>(), s);
+        CVG_CK(cudaMemsetAsync(segmax_.as<void>(), 0, sizeof(unsigned long long) * segs_.size() * kp_, s));
+        launch_segmax(dtype_, d_x, ldx, d_y, ldy, k_, m_, rows, segs_d_.as<GramTask>(), (int64_t)segs_.size(),
+                      max_seg_rows(), kp_, 0, kp_, nsrc, shift, segmax_.as<unsigned long long>(), s);
       }
       CVG_TRY(count_launch());
       {
         Timed t(ctx_, kReorder);
-        launch_reorder_q(dtype_, slices_, d_x, ldx, d_y, ldy, k_, m_, rows, zrows_, kp_, 0, kp_, nsrc, shift,
-                         blkseg_.as<int>(), segexp_.as<int>(), zq_.as<int8_t>(), flag_.as<int>(), s);
+        if (!launch_reorder_q(dtype_, slices_, d_x, ldx, d_y, ldy, k_, m_, rows, zrows_, kp_, 0, kp_, nsrc, shift,
+                              blkseg_.as<int>(), segmax_.as<unsigned long long>(), zq_.as<int8_t>(), flag_.as<int>(),
+                              s))
+          return Status::Err(5, "cuTensorMapEncodeTiled unavailable or rejected the operand layout");
       }
       CVG_TRY(count_launch());
     }
@@ -726,7 +729,7 @@ Status Plan::gram(const void* d_x, int64_t ldx, const void* d_y, int64_t ldy, co
       bool ok;
       {
         Timed t(ctx_, kGram);
-        ok = launch_gram_i8(slices_, zq_.as<int8_t>(), segexp_.as<int>(), zrows_, kp_, segs_d_.as<GramTask>(),
+        ok = launch_gram_i8(slices_, zq_.as<int8_t>(), segmax_.as<unsigned long long>(), zrows_, kp_, segs_d_.as<GramTask>(),
                             (int64_t)segs_.size(), tilesq_d_.as<int2>(), (int)tilesq_.size(), part_.as<double>(), s);
       }
       if (!ok) return Status::Err(5, "cuTensorMapEncodeTiled unavailable or rejected the operand layout");
@@ -804,6 +807,8 @@ Status Plan::gram_host(const void* h_x, const void* h_y, void* d_x, void* d_y, c
   double* shift = shift_.as<double>();
   CVG_TRY(shift_stage_.upload({{host_shift, sizeof(double) * w_, shift}}, s));
   CVG_CK(cudaMemsetAsync(flag_.as<void>(), 0, sizeof(int), s));
+  if (i8_path() && !segs_.empty())
+    CVG_CK(cudaMemsetAsync(segmax_.as<void>(), 0, sizeof(unsigned long long) * segs_.size() * kp_, s));
   // the copy stream may overwrite d_x / d_y only after earlier work on s is done
   cudaEvent_t ev0 = ctx_->stream_event(0);
   CVG_CK(cudaEventRecord(ev0, s));
@@ -834,10 +839,13 @@ Status Plan::gram_host(const void* h_x, const void* h_y, void* d_x, void* d_y, c
                                  flag_.as<int>(), s);
         } else if (i8_path()) {
           launch_segmax(dtype_, d_x, k_, d_y, m_, k_, m_, src_row_.as<int64_t>(), segs_d_.as<GramTask>(),
-                        (int64_t)segs_.size(), kp_, z0, z1, src_n_, shift, segexp_.as<int>(), s);
+                        (int64_t)segs_.size(), max_seg_rows(), kp_, z0, z1, src_n_, shift,
+                        segmax_.as<unsigned long long>(), s);
           CVG_TRY(count_launch());
-          launch_reorder_q(dtype_, slices_, d_x, k_, d_y, m_, k_, m_, src_row_.as<int64_t>(), zrows_, kp_, z0, z1,
-                           src_n_, shift, blkseg_.as<int>(), segexp_.as<int>(), zq_.as<int8_t>(), flag_.as<int>(), s);
+          if (!launch_reorder_q(dtype_, slices_, d_x, k_, d_y, m_, k_, m_, src_row_.as<int64_t>(), zrows_, kp_, z0, z1,
+                                src_n_, shift, blkseg_.as<int>(), segmax_.as<unsigned long long>(), zq_.as<int8_t>(),
+                                flag_.as<int>(), s))
+            return Status::Err(5, "cuTensorMapEncodeTiled unavailable or rejected the operand layout");
         }
         else if (dtype_ == 1)
           launch_reorder_split_t(dtype_, d_x, k_, d_y, m_, k_, m_, src_row_.as<int64_t>(), zrows_, kp_, z0, z1, shift,
@@ -857,7 +865,7 @@ Status Plan::gram_host(const void* h_x, const void* h_y, void* d_x, void* d_y, c
                                 kp_, segs_d_.as<GramTask>(), (int64_t)segs_.size(), tiles_bycol_d_.as<int2>() + t0,
                                 t1 - t0, part_.as<double>(), s);
         else if (i8_path())
-          ok = launch_gram_i8(slices_, zq_.as<int8_t>(), segexp_.as<int>(), zrows_, kp_, segs_d_.as<GramTask>(),
+          ok = launch_gram_i8(slices_, zq_.as<int8_t>(), segmax_.as<unsigned long long>(), zrows_, kp_, segs_d_.as<GramTask>(),
                               (int64_t)segs_.size(), tiles_bycol_d_.as<int2>() + t0, t1 - t0, part_.as<double>(), s);
         else if (dtype_ == 1)
           ok = launch_gram_tf32(zt_hi_.as<float>(), zt_lo_.as<float>(), zrows_, kp_, segs_d_.as<GramTask>(),

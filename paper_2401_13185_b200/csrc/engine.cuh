@@ -151,6 +151,11 @@ class Plan {
   void assign_rank();  // rank mode: fb_/fe_, segment window, fold group
   int64_t chunk_rows() const;
   int64_t seg_rows(int64_t count) const;
+  int64_t max_seg_rows() const {
+    int64_t r = 0;
+    for (const GramTask& g : segs_) r = std::max(r, g.rows);
+    return r;
+  }
   bool f16_path() const { return dtype_ == 1 && !fp32_tf32(); }
   static bool fp32_tf32();
   // fp64 Gram on tcgen05 kind::i8 (int8 digit slices, k_gram_i8.cu); small-fold mode keeps
@@ -184,7 +189,7 @@ class Plan {
   TreeProgram group_tree_;
   DevBuf zero_g_, zero_nval_, zero_ptr_;
 
-  DevBuf zq_, segexp_, blkseg_, tilesq_d_, tiles_d_, out_tiles_d_, tiles128_d_, zt_hi_, zt_lo_, unscale_, tile_counts_, fold_counts_, bad_, zbase_d_, src_row_, z_, part_, foldbuf_, local_,
+  DevBuf zq_, segmax_, blkseg_, tilesq_d_, tiles_d_, out_tiles_d_, tiles128_d_, zt_hi_, zt_lo_, unscale_, tile_counts_, fold_counts_, bad_, zbase_d_, src_row_, z_, part_, foldbuf_, local_,
       total_, shift_, flag_, tiles_bycol_d_, src_map_, segs_d_, foldptr_d_, nval_d_, st_mz_, st_sT_, st_sd_, cfg_d_;
   TreeProgram fold_tree_, local_tree_, rank_tree_;
   PinnedStage blkseg_stage_, seg_stage_, ptr_stage_, shift_stage_, cfg_stage_, col_stage_;

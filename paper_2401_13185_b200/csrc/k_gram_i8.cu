@@ -129,12 +129,26 @@ __device__ __forceinline__ double pow2(int e) {  // 2^e for e in [-1022, 1023]
   return __hiloint2double((1023 + e) << 20, 0);
 }
 
+// The segment exponent of a column whose max |z| is mx: max |z| 2^e in [31.5, 63), so every
+// value is representable by the offset digits (|w| < 63 < 64 - 64/127); e = 0 for an
+// all-zero (or non-finite) column.  e <= 1000
+// keeps 2^(e + 7(S-1)) a normal double (columns below 2^-994 lose digits; their Gram
+// entries are below 2^-1988 and round to zero in fp64 anyway).
+__device__ __forceinline__ int seg_exponent(double mx) {
+  if (!(mx > 0.0) || !isfinite(mx)) return 0;
+  const int be = (int)((__double_as_longlong(mx) >> 52) & 0x7ff);  // 0 for subnormal maxima
+  int e = 5 - (be - 1023);
+  if (e <= 1000 && mx * pow2(e) >= 63.0) --e;
+  return min(e, 1000);
+}
+
 // tiles[i] = {I, J | wmask << 16}: rows 128I .. +128 (Z columns), columns 64J .. +64; wmask bit h:
 // the 64 x 64 sub-tile of rows 128I + 64h is needed downstream (an upper 64-tile of the plan).
 template <int S>
 __global__ void __launch_bounds__(kQThreads, 1)
     gram_i8_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
-                   const int* __restrict__ segexp, const GramTask* __restrict__ segs, const int2* __restrict__ tiles,
+                   const unsigned long long* __restrict__ segmax, const GramTask* __restrict__ segs,
+                   const int2* __restrict__ tiles,
                    int ntiles, int64_t kp, double* __restrict__ part) {
   using C = QCfg<S>;
   constexpr int NST = C::kNst;
@@ -214,9 +228,9 @@ __global__ void __launch_bounds__(kQThreads, 1)
     const int64_t row = (int64_t)ti * QA + 32 * q + lane;  // this thread's Gram row (a Z column)
     const int64_t col0 = (int64_t)tj * QB + 32 * h;
     const bool write = row < kp && ((wmask >> (q >> 1)) & 1);
-    const int* ex = segexp + (int64_t)seg * kp;
-    const double urow = pow2(-ex[row < kp ? row : 0]);
-    const double ucol = pow2(-ex[col0 + lane]);  // lane j holds column col0 + j's factor
+    const unsigned long long* mx = segmax + (int64_t)seg * kp;
+    const double urow = pow2(-seg_exponent(__longlong_as_double((long long)mx[row < kp ? row : 0])));
+    const double ucol = pow2(-seg_exponent(__longlong_as_double((long long)mx[col0 + lane])));  // lane j: column col0 + j
     mbar_wait(&acc_full, 0);
     asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
     double* out = part + (int64_t)seg * kp * kp + row * kp + col0;
@@ -260,11 +274,13 @@ __global__ void __launch_bounds__(kQThreads, 1)
 }
 
 // ---------------------------------------------------------------------------
-// Segment column maxima: segexp[seg][c] = e with max |z| * 2^e in [32, 64) over the
-// segment's rows (z = shifted value; ones column 1; padding columns / rows 0 -> e = 0).
-// One CTA per (segment, 64-column chunk); warp w reads rows w, w + 16, ...; lane
-// holds columns 2 lane, 2 lane + 1 (one 16-byte load per row when aligned).
-constexpr int kSmThreads = 512;
+// Segment column maxima: segmax[seg][c] = max |z| over the segment's rows, as the bits of
+// a non-negative double (so atomicMax on the bits is an exact, order-free max); z = shifted
+// value, ones column 1, padding columns / rows 0.  Grid (segment, 64-column chunk, row
+// slice of kSmRows); warp w reads rows w, w + 8, ... four at a time (16-byte loads of
+// columns 2 lane, 2 lane + 1); one atomicMax per column per CTA.  The buffer is zeroed first.
+constexpr int kSmThreads = 256;
+constexpr int kSmRows = 1024;
 
 template <typename T>
 __global__ void __launch_bounds__(kSmThreads) segmax_kernel(const T* __restrict__ x, int64_t ldx,
@@ -272,39 +288,57 @@ __global__ void __launch_bounds__(kSmThreads) segmax_kernel(const T* __restrict_
                                                             int64_t m, const int64_t* __restrict__ src_row,
                                                             const GramTask* __restrict__ segs, int64_t kp,
                                                             int64_t c_begin, int64_t nsrc,
-                                                            const double* __restrict__ shift, int* __restrict__ segexp) {
-  __shared__ double s_max[kSmThreads / 32][64];
+                                                            const double* __restrict__ shift,
+                                                            unsigned long long* __restrict__ segmax) {
+  constexpr int NW = kSmThreads / 32;
+  __shared__ double s_max[NW][64];
   const int seg = blockIdx.x;
   const int64_t c0 = c_begin + 64 * (int64_t)blockIdx.y;
   const GramTask task = segs[seg];
+  const int64_t r_begin = (int64_t)blockIdx.z * kSmRows;
+  const int64_t r_end = min(task.rows, r_begin + kSmRows);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int64_t wd = k + m;
   const int64_t ca = c0 + 2 * lane, cb = ca + 1;
   const double sa = ca < wd ? shift[ca] : 0.0, sb = cb < wd ? shift[cb] : 0.0;
   const bool vec = sizeof(T) == 8 && cb < k && (ldx % 2) == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0;
+  // a Y column pair (k even): one 16-byte load from y
+  const bool yvec = sizeof(T) == 8 && ca >= k && cb < wd && (k % 2) == 0 && (ldy % 2) == 0 &&
+                    (reinterpret_cast<uintptr_t>(y) & 15) == 0;
+  const T* vbase = vec ? x + ca : yvec ? y + (ca - k) : nullptr;
+  const int64_t vld = vec ? ldx : ldy;
   double ma = 0.0, mb = 0.0;
-  auto val = [&](const T* xr, const T* yr, int64_t c, double sh) -> double {
-    if (c < k) return __dsub_rn((double)__ldg(xr + c), sh);
-    if (c < wd) return __dsub_rn((double)__ldg(yr + (c - k)), sh);
+  auto val = [&](int64_t src, int64_t c, double sh) -> double {
+    if (src < 0) return 0.0;
+    if (c < k) return __dsub_rn((double)__ldg(x + src * ldx + c), sh);
+    if (c < wd) return __dsub_rn((double)__ldg(y + src * ldy + (c - k)), sh);
     return c == wd ? 1.0 : 0.0;
   };
-  for (int64_t r = w; r < task.rows; r += kSmThreads / 32) {
-    const int64_t src = src_row[task.zrow + r];
-    CVG_DCHECK(src < nsrc && src >= -1);
-    if (src < 0) continue;
-    const T* xr = x + src * ldx;
-    const T* yr = y + src * ldy;
-    double va, vb;
-    if (vec) {
-      const double2 p = __ldg(reinterpret_cast<const double2*>(xr + ca));
-      va = __dsub_rn(p.x, sa);
-      vb = __dsub_rn(p.y, sb);
-    } else {
-      va = val(xr, yr, ca, sa);
-      vb = val(xr, yr, cb, sb);
+  for (int64_t r0 = r_begin + w; r0 < r_end; r0 += 4 * NW) {
+    int64_t src[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t r = r0 + u * NW;
+      src[u] = r < r_end ? src_row[task.zrow + r] : -1;
+      CVG_DCHECK(src[u] < nsrc && src[u] >= -1);
     }
-    ma = fmax(ma, fabs(va));  // NaN is dropped by fmax; K1Q flags non-finite inputs
-    mb = fmax(mb, fabs(vb));
+    if (vbase) {
+      double2 p[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        p[u] = src[u] >= 0 ? __ldg(reinterpret_cast<const double2*>(vbase + src[u] * vld)) : make_double2(sa, sb);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        ma = fmax(ma, fabs(__dsub_rn(p[u].x, sa)));  // NaN is dropped by fmax; K1Q flags non-finite inputs
+        mb = fmax(mb, fabs(__dsub_rn(p[u].y, sb)));
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        ma = fmax(ma, fabs(val(src[u], ca, sa)));
+        mb = fmax(mb, fabs(val(src[u], cb, sb)));
+      }
+    }
   }
   s_max[w][2 * lane] = ma;
   s_max[w][2 * lane + 1] = mb;
@@ -312,187 +346,231 @@ __global__ void __launch_bounds__(kSmThreads) segmax_kernel(const T* __restrict_
   if (threadIdx.x < 64) {
     double mx = 0.0;
 #pragma unroll
-    for (int i = 0; i < kSmThreads / 32; ++i) mx = fmax(mx, s_max[i][threadIdx.x]);
-    int e = 0;
-    if (mx > 0.0 && isfinite(mx)) {
-      const int be = (int)((__double_as_longlong(mx) >> 52) & 0x7ff);  // 0 for subnormal maxima
-      e = min(1023, 5 - (be - 1023));
-    }
-    segexp[(int64_t)seg * kp + c0 + threadIdx.x] = e;
+    for (int i = 0; i < NW; ++i) mx = fmax(mx, s_max[i][threadIdx.x]);
+    if (mx > 0.0) atomicMax(segmax + (int64_t)seg * kp + c0 + threadIdx.x, (unsigned long long)__double_as_longlong(mx));
   }
 }
 
 // ---------------------------------------------------------------------------
-// K1Q: bucket, shift, scale by the segment exponent, cut into S int8 digits, transpose
-// into Zq[t][blk][col][64].  One CTA per 64-row block, 64-column chunks.  Warp w holds
-// rows 4w .. 4w + 3 (row quad w) of columns 2 lane, 2 lane + 1; a thread packs its 4 rows'
-// digits of one column into one 32-bit word.  Shared tile: word (t, col, quad) at
-// (t * 64 + col) * 17 + quad (stride 17: the transposed writes are at most 2-way
-// conflicted); the write-out stores 4-byte words, a warp covering 2 columns x 64 B.
-constexpr int kQ1Threads = 512;  // 16 warps = 16 row quads
-constexpr int kQ1Stride = 17;
+// K1Q: bucket, shift, scale by the segment exponent, cut into S int8 digits, write
+// Zq[t][blk][col][64].  A CTA item is one 64-row block x 64 columns; its S x 4 KB of
+// digits are assembled in shared memory in the operand's own SWIZZLE_64B layout and
+// leave by one TMA tensor store (full, contiguous 4 KB lines; double-buffered so the
+// next item's loads and cuts overlap the store).  Warp w owns columns 8w .. 8w + 7; lane
+// (j, qq) = (lane >> 2, lane & 3) holds column 8w + j of the row quads qq, qq + 4, qq + 8,
+// qq + 12 (16 rows; a warp load reads 64 contiguous bytes of 4 rows).  Each thread packs
+// a quad's 4 digits into one word; with the SW64 XOR the 32 lanes' words land in 32
+// distinct banks.
+//
+// Digits: one fma gives V = round(z 2^(e + 7(S-1))) + O in the low 52 bits of
+// tt = fma(z, 2^(e + 7(S-1)), 2^52 + O), O = 64 (1 + 128 + ... + 128^(S-1)), 0 <= V < 2^(7S);
+// digit t (t = 0 most significant) is ((V >> 7(S-1-t)) & 127) - 64 in [-64, 63], so
+// sum_t d_t 2^-7t = round(w 2^7(S-1)) 2^-7(S-1) exactly (w = z 2^e, |w| < 63, while the
+// digits reach 64 - 64/127).  Four rows' 7-bit fields are packed into one word by byte
+// permutes and shifted by -64 byte-wise (SWAR, no borrows).
+constexpr int kQ1Threads = 256;
+
+template <int S>
+struct DigitOffset {  // 64 * (128^S - 1) / 127
+  static constexpr int64_t v = 64 * (((int64_t)1 << (7 * S)) - 1) / 127;
+};
+
+template <int S>
+constexpr int k1q_smem_bytes() {
+  return 2 * S * 4096 + 1024;
+}
+
+__device__ __forceinline__ void tma_store_4d(const CUtensorMap* map, const void* src, int c0, int c1, int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];\n" ::"l"(map),
+      "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
 
 template <typename T, int S>
 __global__ void __launch_bounds__(kQ1Threads, 2)
-    reorder_q_kernel(const T* __restrict__ x, int64_t ldx, const T* __restrict__ y, int64_t ldy, int64_t k, int64_t m,
-                     const int64_t* __restrict__ src_row, int64_t zrows, int64_t kp, int64_t c_begin, int64_t c_end,
-                     int64_t nsrc, const double* __restrict__ shift, const int* __restrict__ blkseg,
-                     const int* __restrict__ segexp, int8_t* __restrict__ zq, int* __restrict__ nonfinite) {
-  __shared__ uint32_t s_q[S * 64 * kQ1Stride];
-  __shared__ int64_t s_src[QK];
-  const int64_t blk = blockIdx.x;
-  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+    reorder_q_kernel(const __grid_constant__ CUtensorMap map_out, const T* __restrict__ x, int64_t ldx,
+                     const T* __restrict__ y, int64_t ldy, int64_t k, int64_t m, const int64_t* __restrict__ src_row,
+                     int64_t zrows, int64_t kp, int64_t c_begin, int64_t c_end, int64_t nsrc,
+                     const double* __restrict__ shift, const int* __restrict__ blkseg,
+                     const unsigned long long* __restrict__ segmax, int* __restrict__ nonfinite) {
+  extern __shared__ uint8_t k1q_raw[];
+  uint8_t* tiles = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(k1q_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ int64_t s_src[2][QK];  // this block's and the next block's source rows
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int j = lane >> 2, qq = lane & 3;
+  const int col = 8 * w + j;  // column within the 64-column chunk
   const int64_t wd = k + m;
   CVG_DCHECK(c_begin >= 0 && c_end <= kp && c_begin % 64 == 0 && zrows % QK == 0);
-  if (t < QK) {
-    const int64_t src = src_row[blk * QK + t];
-    CVG_DCHECK(src < nsrc && src >= -1);
-    s_src[t] = src;
-  }
-  const int seg = blkseg[blk];
+  const int64_t nchunk = (c_end - c_begin) / 64;
+  const int64_t nblk = zrows / QK;
+  const int64_t grid = gridDim.x;
+  const double C = 0x1p52 + (double)DigitOffset<S>::v;
+  uint32_t badhi = 0;  // OR of (tt's sign/exponent ^ 2^52's): nonzero iff some z was not finite
+  auto load_src = [&](int64_t b, int sb) {
+    if (threadIdx.x < QK && b < nblk) {
+      const int64_t src = src_row[b * QK + threadIdx.x];
+      CVG_DCHECK(src < nsrc && src >= -1);
+      s_src[sb][threadIdx.x] = src;
+    }
+  };
+  // this thread's 16 values of column c0 + col in block b (raw: the shift is applied at the cut)
+  double v[16];
+  auto load_vals = [&](int sb, int64_t c0) {
+    const int64_t c = c0 + col;
+    const int kind = c < k ? 0 : c < wd ? 1 : c == wd ? 2 : 3;  // x, y, ones, padding
+    const T* base = kind == 0 ? x + c : y + (c - k);
+    const int64_t ld = kind == 0 ? ldx : ldy;
+#pragma unroll
+    for (int p = 0; p < 4; ++p)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int64_t src = s_src[sb][4 * (qq + 4 * p) + i];
+        v[4 * p + i] = src < 0 ? 0.0 : kind <= 1 ? (double)__ldg(base + src * ld) : kind == 2 ? 1.0 : 0.0;
+      }
+  };
+  int64_t blk = blockIdx.x;
+  load_src(blk, 0);
+  load_src(blk + grid, 1);
   __syncthreads();
-  int64_t src4[4];
-  bool all_real = true;
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    src4[i] = s_src[4 * w + i];
-    all_real &= src4[i] >= 0;
-  }
-  const bool vec_ok = sizeof(T) == 8 && (ldx % 2) == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0;
-  bool bad = false;
-  const int64_t zslice = zrows * kp;  // bytes per digit slice
-  for (int64_t c0 = c_begin; c0 < c_end; c0 += 64) {
-    const int64_t ca = c0 + 2 * lane;
-    double v[4][2];
-    if (all_real && vec_ok && ca + 1 < k) {
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const double2 p = __ldg(reinterpret_cast<const double2*>(x + src4[i] * ldx + ca));
-        v[i][0] = p.x;
-        v[i][1] = p.y;
-      }
-    } else {
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int64_t c = ca + e;
-          double val = 0.0;
-          if (src4[i] >= 0) {
-            if (c < k)
-              val = (double)__ldg(x + src4[i] * ldx + c);
-            else if (c < wd)
-              val = (double)__ldg(y + src4[i] * ldy + (c - k));
-            else if (c == wd)
-              val = 1.0;
-          }
-          v[i][e] = val;
-        }
-    }
-#pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      const int64_t c = ca + e;
+  if (blk < nblk) load_vals(0, c_begin);
+  int buf = 0, sb = 0;
+  for (; blk < nblk; blk += grid, sb ^= 1) {
+    const unsigned long long* smx = segmax + (int64_t)blkseg[blk] * kp;
+    for (int64_t ch = 0; ch < nchunk; ++ch, buf ^= 1) {
+      const int64_t c0 = c_begin + 64 * ch;
+      const int64_t c = c0 + col;
       const double sh = c < wd ? shift[c] : 0.0;
-      const double sc = pow2(segexp[(int64_t)seg * kp + c]);
-      uint32_t word[S];
+      const double sc = pow2(seg_exponent(__longlong_as_double((long long)smx[c])) + 7 * (S - 1));
+      uint32_t lo[16], hi[16];
 #pragma unroll
-      for (int d = 0; d < S; ++d) word[d] = 0;
+      for (int p = 0; p < 4; ++p)
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        double z = v[i][e];
-        if (src4[i] >= 0 && c < wd) {
-          bad |= !isfinite(z);
-          z = __dsub_rn(z, sh);
+        for (int i = 0; i < 4; ++i) {
+          const int e = 4 * p + i;
+          const bool real = s_src[sb][4 * (qq + 4 * p) + i] >= 0 && c < wd;
+          const double tt = fma(real ? __dsub_rn(v[e], sh) : v[e], sc, C);
+          lo[e] = (uint32_t)__double2loint(tt);
+          hi[e] = (uint32_t)__double2hiint(tt);
+          badhi |= (hi[e] & 0xfff00000u) ^ 0x43300000u;
         }
-        // r = z * 2^e exactly; digit d = r rounded to a multiple of 2^-7d (ties to even),
-        // read from the low word of r + 1.5 * 2^(52 - 7d); the residual r - digit is exact.
-        double r = z * sc;
+      // next chunk's loads in flight while this one is cut and stored
+      if (ch + 1 < nchunk)
+        load_vals(sb, c0 + 64);
+      else if (blk + grid < nblk)
+        load_vals(sb ^ 1, c_begin);
+      // this buffer's previous TMA store has finished reading shared memory
+      if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");
+      __syncthreads();
+      uint8_t* tile = tiles + buf * (S * 4096);
 #pragma unroll
-        for (int d = 0; d < S; ++d) {
-          const double magic = 0x1.8p52 * (d == 0 ? 1.0 : d == 1 ? 0x1p-7 : d == 2 ? 0x1p-14 : d == 3 ? 0x1p-21
-                                                       : d == 4 ? 0x1p-28 : d == 5 ? 0x1p-35 : d == 6 ? 0x1p-42 : 0x1p-49);
-          const double tt = __dadd_rn(r, magic);
-          const double dg = __dsub_rn(tt, magic);
-          r = __dsub_rn(r, dg);
-          word[d] |= ((uint32_t)__double2loint(tt) & 0xffu) << (8 * i);
+      for (int d = 0; d < S; ++d) {
+        const int pos = 7 * (S - 1 - d);
+#pragma unroll
+        for (int p = 0; p < 4; ++p) {
+          uint32_t b[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {  // low word of V >> pos (funnel shifts take the shift mod 32)
+            const int e = 4 * p + i;
+            b[i] = pos >= 32 ? hi[e] >> (pos - 32) : __funnelshift_r(lo[e], hi[e], pos);
+          }
+          uint32_t word = __byte_perm(__byte_perm(b[0], b[1], 0x0040), __byte_perm(b[2], b[3], 0x0040), 0x5410);
+          word &= 0x7f7f7f7fu;
+          word = ((word | 0x80808080u) - 0x40404040u) ^ 0x80808080u;  // each byte - 64, no borrows
+          // quad q = qq + 4p of column col, SWIZZLE_64B: 16-byte chunk (q >> 2) ^ ((col >> 1) & 3)
+          const int off = col * 64 + ((p ^ ((col >> 1) & 3)) << 4) + (qq << 2);
+          *reinterpret_cast<uint32_t*>(tile + d * 4096 + off) = word;
         }
       }
-      const int col = 2 * lane + e;
-#pragma unroll
-      for (int d = 0; d < S; ++d) s_q[(d * 64 + col) * kQ1Stride + w] = word[d];
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        tma_store_4d(&map_out, tile, 0, (int)c0, (int)blk, 0);
+        asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+      }
     }
+    // s_src[sb] is free (the next block's prefetch used sb ^ 1): fill it for block + 2 grid; the
+    // second barrier publishes it before a one-chunk block's prefetch reads it
     __syncthreads();
-    // write-out: (d, col, quad) words; consecutive threads -> consecutive quads of a column
-    const int64_t ncols = c_end - c0 < 64 ? c_end - c0 : 64;
-    for (int i = t; i < S * 64 * 16; i += kQ1Threads) {
-      const int quad = i & 15, col = (i >> 4) & 63, d = i >> 10;
-      if (col >= ncols) continue;
-      const uint32_t wv = s_q[(d * 64 + col) * kQ1Stride + quad];
-      *reinterpret_cast<uint32_t*>(zq + d * zslice + (blk * kp + c0 + col) * QK + 4 * quad) = wv;
-    }
+    load_src(blk + 2 * grid, sb);
     __syncthreads();
   }
-  if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(nonfinite, 1);
+  if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
+  if (__any_sync(0xffffffffu, badhi != 0) && lane == 0) atomicOr(nonfinite, 1);
+}
+
+// 4-D map over Zq: {64 rows, kp, zrows / 64, S} bytes, box {64, box_cols, 1, S}, SWIZZLE_64B.
+inline bool make_zq_map(CUtensorMap* map, const int8_t* zq, int64_t zrows, int64_t kp, int slices, int box_cols) {
+  EncodeTiledFn enc = encode_fn();
+  if (!enc) return false;
+  const cuuint64_t dims[4] = {(cuuint64_t)QK, (cuuint64_t)kp, (cuuint64_t)(zrows / QK), (cuuint64_t)slices};
+  const cuuint64_t strides[3] = {(cuuint64_t)QK, (cuuint64_t)kp * QK, (cuuint64_t)zrows * kp};
+  const cuuint32_t box[4] = {(cuuint32_t)QK, (cuuint32_t)box_cols, 1, (cuuint32_t)slices};
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<int8_t*>(zq), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 template <int S>
-bool launch_gram_i8_s(const int8_t* zq, const int* segexp, int64_t zrows, int64_t kp, const GramTask* segs,
+bool launch_gram_i8_s(const int8_t* zq, const unsigned long long* segmax, int64_t zrows, int64_t kp, const GramTask* segs,
                       int64_t nseg, const int2* tiles, int ntiles, double* part, cudaStream_t s) {
-  EncodeTiledFn enc = encode_fn();
-  if (!enc) return false;
   CUtensorMap ma, mb;
-  const cuuint64_t dims[4] = {(cuuint64_t)QK, (cuuint64_t)kp, (cuuint64_t)(zrows / QK), (cuuint64_t)S};
-  const cuuint64_t strides[3] = {(cuuint64_t)QK, (cuuint64_t)kp * QK, (cuuint64_t)zrows * kp};
-  const cuuint32_t box_a[4] = {(cuuint32_t)QK, (cuuint32_t)QA, 1, (cuuint32_t)S};
-  const cuuint32_t box_b[4] = {(cuuint32_t)QK, (cuuint32_t)QB, 1, (cuuint32_t)S};
-  const cuuint32_t estr[4] = {1, 1, 1, 1};
-  if (enc(&ma, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<int8_t*>(zq), dims, strides, box_a, estr,
-          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-    return false;
-  if (enc(&mb, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<int8_t*>(zq), dims, strides, box_b, estr,
-          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-    return false;
+  if (!make_zq_map(&ma, zq, zrows, kp, S, QA) || !make_zq_map(&mb, zq, zrows, kp, S, QB)) return false;
   cudaFuncSetAttribute(gram_i8_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, QCfg<S>::kSmem);
   const int64_t blocks = nseg * (int64_t)ntiles;
   if (blocks > 0)
-    gram_i8_kernel<S><<<(unsigned)blocks, kQThreads, QCfg<S>::kSmem, s>>>(ma, mb, segexp, segs, tiles, ntiles, kp,
+    gram_i8_kernel<S><<<(unsigned)blocks, kQThreads, QCfg<S>::kSmem, s>>>(ma, mb, segmax, segs, tiles, ntiles, kp,
                                                                           part);
   return true;
 }
 
 template <typename T, int S>
-void launch_k1q(const void* x, int64_t ldx, const void* y, int64_t ldy, int64_t k, int64_t m, const int64_t* src_row,
+bool launch_k1q(const void* x, int64_t ldx, const void* y, int64_t ldy, int64_t k, int64_t m, const int64_t* src_row,
                 int64_t zrows, int64_t kp, int64_t c_begin, int64_t c_end, int64_t nsrc, const double* shift,
-                const int* blkseg, const int* segexp, int8_t* zq, int* nonfinite, cudaStream_t s) {
-  reorder_q_kernel<T, S><<<(unsigned)(zrows / QK), kQ1Threads, 0, s>>>(
-      (const T*)x, ldx, (const T*)y, ldy, k, m, src_row, zrows, kp, c_begin, c_end, nsrc, shift, blkseg, segexp, zq,
-      nonfinite);
+                const int* blkseg, const unsigned long long* segmax, int8_t* zq, int* nonfinite, cudaStream_t s) {
+  CUtensorMap mo;
+  if (!make_zq_map(&mo, zq, zrows, kp, S, 64)) return false;
+  constexpr int smem = k1q_smem_bytes<S>();
+  static int per_sm = 0, sms = 0;  // grid-stride over one wave of resident CTAs
+  if (!per_sm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaFuncSetAttribute(reorder_q_kernel<T, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, reorder_q_kernel<T, S>, kQ1Threads, smem);
+    per_sm = per_sm > 0 ? per_sm : 1;
+  }
+  const int64_t blocks = std::min<int64_t>(zrows / QK, (int64_t)per_sm * sms);
+  reorder_q_kernel<T, S><<<(unsigned)blocks, kQ1Threads, smem, s>>>(mo, (const T*)x, ldx, (const T*)y, ldy, k, m,
+                                                                    src_row, zrows, kp, c_begin, c_end, nsrc, shift,
+                                                                    blkseg, segmax, nonfinite);
+  return true;
 }
 
 }  // namespace
 
 void launch_segmax(int dtype, const void* x, int64_t ldx, const void* y, int64_t ldy, int64_t k, int64_t m,
-                   const int64_t* src_row, const GramTask* segs, int64_t nseg, int64_t kp, int64_t c_begin,
-                   int64_t c_end, int64_t nsrc, const double* shift, int* segexp, cudaStream_t s) {
+                   const int64_t* src_row, const GramTask* segs, int64_t nseg, int64_t max_seg_rows, int64_t kp,
+                   int64_t c_begin, int64_t c_end, int64_t nsrc, const double* shift, unsigned long long* segmax,
+                   cudaStream_t s) {
   if (nseg <= 0 || c_end <= c_begin) return;
-  const dim3 grid((unsigned)nseg, (unsigned)((c_end - c_begin) / 64));
+  const dim3 grid((unsigned)nseg, (unsigned)((c_end - c_begin) / 64), (unsigned)((max_seg_rows + kSmRows - 1) / kSmRows));
   if (dtype == 0)
     segmax_kernel<double><<<grid, kSmThreads, 0, s>>>((const double*)x, ldx, (const double*)y, ldy, k, m, src_row,
-                                                      segs, kp, c_begin, nsrc, shift, segexp);
+                                                      segs, kp, c_begin, nsrc, shift, segmax);
   else
     segmax_kernel<float><<<grid, kSmThreads, 0, s>>>((const float*)x, ldx, (const float*)y, ldy, k, m, src_row, segs,
-                                                     kp, c_begin, nsrc, shift, segexp);
+                                                     kp, c_begin, nsrc, shift, segmax);
 }
 
-void launch_reorder_q(int dtype, int slices, const void* x, int64_t ldx, const void* y, int64_t ldy, int64_t k,
+bool launch_reorder_q(int dtype, int slices, const void* x, int64_t ldx, const void* y, int64_t ldy, int64_t k,
                       int64_t m, const int64_t* src_row, int64_t zrows, int64_t kp, int64_t c_begin, int64_t c_end,
-                      int64_t nsrc, const double* shift, const int* blkseg, const int* segexp, int8_t* zq,
+                      int64_t nsrc, const double* shift, const int* blkseg, const unsigned long long* segmax, int8_t* zq,
                       int* nonfinite, cudaStream_t s) {
-  if (zrows <= 0 || c_end <= c_begin) return;
+  if (zrows <= 0 || c_end <= c_begin) return true;
 #define CVG_K1Q(T, S) \
-  launch_k1q<T, S>(x, ldx, y, ldy, k, m, src_row, zrows, kp, c_begin, c_end, nsrc, shift, blkseg, segexp, zq, nonfinite, s)
+  return launch_k1q<T, S>(x, ldx, y, ldy, k, m, src_row, zrows, kp, c_begin, c_end, nsrc, shift, blkseg, segmax, zq, nonfinite, s)
   if (dtype == 0) {
     if (slices == 6) CVG_K1Q(double, 6);
     else CVG_K1Q(double, 7);
@@ -503,10 +581,10 @@ void launch_reorder_q(int dtype, int slices, const void* x, int64_t ldx, const v
 #undef CVG_K1Q
 }
 
-bool launch_gram_i8(int slices, const int8_t* zq, const int* segexp, int64_t zrows, int64_t kp, const GramTask* segs,
+bool launch_gram_i8(int slices, const int8_t* zq, const unsigned long long* segmax, int64_t zrows, int64_t kp, const GramTask* segs,
                     int64_t nseg, const int2* tiles, int ntiles, double* part, cudaStream_t s) {
-  return slices == 6 ? launch_gram_i8_s<6>(zq, segexp, zrows, kp, segs, nseg, tiles, ntiles, part, s)
-                     : launch_gram_i8_s<7>(zq, segexp, zrows, kp, segs, nseg, tiles, ntiles, part, s);
+  return slices == 6 ? launch_gram_i8_s<6>(zq, segmax, zrows, kp, segs, nseg, tiles, ntiles, part, s)
+                     : launch_gram_i8_s<7>(zq, segmax, zrows, kp, segs, nseg, tiles, ntiles, part, s);
 }
 
 }  // namespace cvg

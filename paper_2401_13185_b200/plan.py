@@ -24,6 +24,7 @@ torch.distributed for the collectives.  No torch types cross the C ABI.
 from __future__ import annotations
 
 import ctypes
+import os
 from typing import Optional, Sequence
 
 import numpy as np
@@ -363,6 +364,15 @@ def gram_tiles(k: int, m: int, edge: int = 64):
     return [(i, j) for i in range(nt) for j in range(i, nt) if i <= tx or j == i or j == to]
 
 
+def fp64_kind() -> str:
+    """The fp64 Gram kind plans are created with: "i8" (int8 digit slices on tcgen05 kind::i8) or "dmma"."""
+    return "i8" if os.environ.get("CVG_FP64_KIND") == "i8" else "dmma"
+
+
+def i8_slices() -> int:
+    return 6 if os.environ.get("CVG_I8_SLICES") == "6" else 7
+
+
 def executed_gram_flops(n: int, k: int, m: int, p: int, f32: bool = False) -> float:
     """Tensor-core flops the Gram kernel issues for n rows (fold padding ignored):
     fp64: 64x64 DMMA tiles, diagonal tiles only their 36 upper 8x8 blocks;
@@ -370,5 +380,9 @@ def executed_gram_flops(n: int, k: int, m: int, p: int, f32: bool = False) -> fl
     if f32:
         return 3 * 2.0 * len(gram_tiles(k, m, 128)) * 128 * 128 * n
     tiles = gram_tiles(k, m)
+    if fp64_kind() == "i8":  # int8 ops: 128x64 tiles x S(S+1)/2 slice pairs
+        s = i8_slices()
+        tq = {(i // 2, j) for i, j in tiles}
+        return 2.0 * len(tq) * 128 * 64 * n * (s * (s + 1) // 2)
     n_diag = sum(1 for i, j in tiles if i == j)
     return 2.0 * ((len(tiles) - n_diag) * 64 * 64 + n_diag * 36 * 64) * n
