@@ -237,11 +237,12 @@ bool Plan::fp32_tf32() {
   return v;
 }
 
-// fp64 operand kind: int8 digit slices on kind::i8 (CVG_FP64_KIND=i8) or DMMA (dmma).
-// Read at plan creation, so one process can A/B both.
+// fp64 operand kind: exact int8 digit slices on tcgen05 kind::i8 (default; k_gram_i8.cu) or,
+// with CVG_FP64_KIND=dmma, the fp64 DMMA Gram (k_gram_f64.cu).  Read at plan creation, so one
+// process can A/B both.
 static bool fp64_i8_env() {
   const char* e = std::getenv("CVG_FP64_KIND");
-  return e && std::string(e) == "i8";
+  return !(e && std::string(e) == "dmma");
 }
 static int i8_slices_env() {
   const char* e = std::getenv("CVG_I8_SLICES");

@@ -170,7 +170,7 @@ class Plan {
   std::vector<int2> tiles_, out_tiles_, tiles128_;
   std::vector<int4> pairs128_;  // CTA-pair tiles for the cta_group::2 fp32 Gram
   std::vector<int2> tilesq_;    // int8 Gram tiles {I (128 rows), J (64 columns) | write mask << 16}
-  bool i8_ = false;             // fp64 kind: int8 slices (CVG_FP64_KIND=i8) or DMMA
+  bool i8_ = false;             // fp64 kind: int8 slices (default) or DMMA (CVG_FP64_KIND=dmma)
   int slices_ = 7;              // int8 digits per value (CVG_I8_SLICES = 6 or 7)
   DevBuf pairs128_d_;
   std::vector<int64_t> counts_;  // per fold (all p) validation sizes

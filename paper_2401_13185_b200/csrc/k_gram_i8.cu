@@ -32,6 +32,8 @@
 //   warp 1      TMEM owner + MMA issuer: S(S+1)/2 slice pairs x 2 K-steps per stage,
 //               pair (t, u) into accumulator t + u (S x 64 int32 TMEM columns)
 //   warps 2..9  drain once per tile: Horner over the S accumulators, exact unscale
+#include <cstdlib>
+
 #include "cvg_internal.cuh"
 #include "tc_util.cuh"
 
@@ -46,12 +48,14 @@ constexpr int QK = 64;                  // rows per stage = 64 B of int8 (one SW
 constexpr int kQEpiWarps = 8;           // 4 TMEM lane quarters x 2 column halves
 constexpr int kQThreads = 64 + 32 * kQEpiWarps;
 
-template <int S>
+// KS rows per pipeline stage: 64 (one SW64 atom row of a 64-row block) or 32 (half of it, SW32):
+// S = 7 fits 2 stages of 64 rows (84 KB each) or 5 of 32 rows (42 KB).
+template <int S, int KS>
 struct QCfg {
-  static constexpr int kA = QA * QK;                      // 8 KB per slice
-  static constexpr int kB = QB * QK;                      // 4 KB per slice
+  static constexpr int kA = QA * KS;                      // per slice
+  static constexpr int kB = QB * KS;
   static constexpr int kStage = S * (kA + kB);
-  static constexpr int kNst = (227 * 1024 - 2048) / kStage;  // 3 stages for S = 6, 2 for S = 7
+  static constexpr int kNst = (227 * 1024 - 2048) / kStage;
   static constexpr int kSmem = kNst * kStage + 1024;
 };
 
@@ -105,10 +109,13 @@ __device__ __forceinline__ void mma_slices(uint32_t tmem_d, uint64_t a0, uint64_
   }
 }
 
-// K-major, 64B-swizzled operand: 8-row atoms of 512 B (SBO), version 1 (sm_100), layout 4 = SWIZZLE_64B.
-__device__ __forceinline__ uint64_t kmajor_sw64_desc(const void* tile) {
+// K-major swizzled operand with KS-byte rows: 8-row atoms of 8 KS bytes (SBO), version 1 (sm_100);
+// layout 4 = SWIZZLE_64B (KS = 64), 6 = SWIZZLE_32B (KS = 32).
+template <int KS>
+__device__ __forceinline__ uint64_t kmajor_sw_desc(const void* tile) {
   const uint64_t addr = smem_u32(tile);
-  return ((addr >> 4) & 0x3FFFull) | (1ull << 16) | ((512ull >> 4) << 32) | (1ull << 46) | (4ull << 61);
+  return ((addr >> 4) & 0x3FFFull) | (1ull << 16) | ((uint64_t)(8 * KS >> 4) << 32) | (1ull << 46) |
+         ((KS == 64 ? 4ull : 6ull) << 61);
 }
 
 __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2,
@@ -144,14 +151,15 @@ __device__ __forceinline__ int seg_exponent(double mx) {
 
 // tiles[i] = {I, J | wmask << 16}: rows 128I .. +128 (Z columns), columns 64J .. +64; wmask bit h:
 // the 64 x 64 sub-tile of rows 128I + 64h is needed downstream (an upper 64-tile of the plan).
-template <int S>
+template <int S, int KS>
 __global__ void __launch_bounds__(kQThreads, 1)
     gram_i8_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                    const unsigned long long* __restrict__ segmax, const GramTask* __restrict__ segs,
                    const int2* __restrict__ tiles,
                    int ntiles, int64_t kp, double* __restrict__ part) {
-  using C = QCfg<S>;
+  using C = QCfg<S, KS>;
   constexpr int NST = C::kNst;
+  constexpr int kPer = QK / KS;  // stages per 64-row block
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   __shared__ __align__(8) uint64_t full_bar[NST], empty_bar[NST], acc_full;
@@ -167,7 +175,7 @@ __global__ void __launch_bounds__(kQThreads, 1)
   const GramTask task{uniform(task0.zrow), uniform(task0.rows)};
   CVG_DCHECK(task.zrow % QK == 0 && task.rows % QK == 0 && task.rows > 0);
   CVG_DCHECK(ti >= 0 && 2 * ti <= tj && (int64_t)tj * QB < kp);
-  const int nsteps = (int)(task.rows / QK);
+  const int nsteps = (int)(task.rows / KS);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
@@ -196,11 +204,11 @@ __global__ void __launch_bounds__(kQThreads, 1)
     for (int it = 0; it < nsteps; ++it) {
       const int s = it % NST;
       mbar_wait(&empty_bar[s], ((uint32_t)(it / NST) & 1u) ^ 1u);
-      const int blk = (int)(task.zrow / QK) + it;
+      const int blk = (int)(task.zrow / QK) + it / kPer, r0 = (it % kPer) * KS;
       if (elect_one()) {
         mbar_expect_tx(&full_bar[s], bytes);
-        tma_load_4d(opA(s), &map_a, &full_bar[s], 0, ti * QA, blk, 0);
-        if (!self) tma_load_4d(opB(s), &map_b, &full_bar[s], 0, tj * QB, blk, 0);
+        tma_load_4d(opA(s), &map_a, &full_bar[s], r0, ti * QA, blk, 0);
+        if (!self) tma_load_4d(opB(s), &map_b, &full_bar[s], r0, tj * QB, blk, 0);
       }
       __syncwarp();
     }
@@ -209,12 +217,12 @@ __global__ void __launch_bounds__(kQThreads, 1)
       const int s = it % NST;
       mbar_wait(&full_bar[s], (uint32_t)(it / NST) & 1u);
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-      const uint64_t a0 = kmajor_sw64_desc(opA(s));
-      const uint64_t b0 = self ? kmajor_sw64_desc(opA(s) + inner * QB * QK) : kmajor_sw64_desc(opB(s));
+      const uint64_t a0 = kmajor_sw_desc<KS>(opA(s));
+      const uint64_t b0 = self ? kmajor_sw_desc<KS>(opA(s) + inner * QB * KS) : kmajor_sw_desc<KS>(opB(s));
       const uint64_t a_step = (uint64_t)(C::kA >> 4), b_step = (uint64_t)((self ? C::kA : C::kB) >> 4);
       if (elect_one()) {
 #pragma unroll
-        for (int k = 0; k < QK / 32; ++k)  // K = 32 int8 = 32 B per MMA: +2 in 16-byte descriptor units
+        for (int k = 0; k < KS / 32; ++k)  // K = 32 int8 = 32 B per MMA: +2 in 16-byte descriptor units
           mma_slices<S, 0>(tmem_d, a0 + 2ull * k, a_step, b0 + 2ull * k, b_step, it == 0 && k == 0);
         mma_commit(&empty_bar[s]);  // frees the stage once these MMAs have read it
         if (it == nsteps - 1) mma_commit(&acc_full);
@@ -277,10 +285,10 @@ __global__ void __launch_bounds__(kQThreads, 1)
 // Segment column maxima: segmax[seg][c] = max |z| over the segment's rows, as the bits of
 // a non-negative double (so atomicMax on the bits is an exact, order-free max); z = shifted
 // value, ones column 1, padding columns / rows 0.  Grid (segment, 64-column chunk, row
-// slice of kSmRows); warp w reads rows w, w + 8, ... four at a time (16-byte loads of
-// columns 2 lane, 2 lane + 1); one atomicMax per column per CTA.  The buffer is zeroed first.
+// slice of `slice` rows: 128 .. 1024, so small problems still spread over the SMs); warp w
+// reads rows w, w + 8, ... four at a time (16-byte loads of columns 2 lane, 2 lane + 1); one
+// atomicMax per column per CTA.  The buffer is zeroed first.
 constexpr int kSmThreads = 256;
-constexpr int kSmRows = 1024;
 
 template <typename T>
 __global__ void __launch_bounds__(kSmThreads) segmax_kernel(const T* __restrict__ x, int64_t ldx,
@@ -288,15 +296,15 @@ __global__ void __launch_bounds__(kSmThreads) segmax_kernel(const T* __restrict_
                                                             int64_t m, const int64_t* __restrict__ src_row,
                                                             const GramTask* __restrict__ segs, int64_t kp,
                                                             int64_t c_begin, int64_t nsrc,
-                                                            const double* __restrict__ shift,
+                                                            const double* __restrict__ shift, int64_t slice,
                                                             unsigned long long* __restrict__ segmax) {
   constexpr int NW = kSmThreads / 32;
   __shared__ double s_max[NW][64];
   const int seg = blockIdx.x;
   const int64_t c0 = c_begin + 64 * (int64_t)blockIdx.y;
   const GramTask task = segs[seg];
-  const int64_t r_begin = (int64_t)blockIdx.z * kSmRows;
-  const int64_t r_end = min(task.rows, r_begin + kSmRows);
+  const int64_t r_begin = (int64_t)blockIdx.z * slice;
+  const int64_t r_end = min(task.rows, r_begin + slice);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int64_t wd = k + m;
   const int64_t ca = c0 + 2 * lane, cb = ca + 1;
@@ -500,28 +508,29 @@ __global__ void __launch_bounds__(kQ1Threads, 2)
 }
 
 // 4-D map over Zq: {64 rows, kp, zrows / 64, S} bytes, box {64, box_cols, 1, S}, SWIZZLE_64B.
-inline bool make_zq_map(CUtensorMap* map, const int8_t* zq, int64_t zrows, int64_t kp, int slices, int box_cols) {
+inline bool make_zq_map(CUtensorMap* map, const int8_t* zq, int64_t zrows, int64_t kp, int slices, int box_cols,
+                        int box_rows = QK) {
   EncodeTiledFn enc = encode_fn();
   if (!enc) return false;
   const cuuint64_t dims[4] = {(cuuint64_t)QK, (cuuint64_t)kp, (cuuint64_t)(zrows / QK), (cuuint64_t)slices};
   const cuuint64_t strides[3] = {(cuuint64_t)QK, (cuuint64_t)kp * QK, (cuuint64_t)zrows * kp};
-  const cuuint32_t box[4] = {(cuuint32_t)QK, (cuuint32_t)box_cols, 1, (cuuint32_t)slices};
+  const cuuint32_t box[4] = {(cuuint32_t)box_rows, (cuuint32_t)box_cols, 1, (cuuint32_t)slices};
   const cuuint32_t estr[4] = {1, 1, 1, 1};
   return enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<int8_t*>(zq), dims, strides, box, estr,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, box_rows == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int S>
+template <int S, int KS>
 bool launch_gram_i8_s(const int8_t* zq, const unsigned long long* segmax, int64_t zrows, int64_t kp, const GramTask* segs,
                       int64_t nseg, const int2* tiles, int ntiles, double* part, cudaStream_t s) {
   CUtensorMap ma, mb;
-  if (!make_zq_map(&ma, zq, zrows, kp, S, QA) || !make_zq_map(&mb, zq, zrows, kp, S, QB)) return false;
-  cudaFuncSetAttribute(gram_i8_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, QCfg<S>::kSmem);
+  if (!make_zq_map(&ma, zq, zrows, kp, S, QA, KS) || !make_zq_map(&mb, zq, zrows, kp, S, QB, KS)) return false;
+  using C = QCfg<S, KS>;
+  cudaFuncSetAttribute(gram_i8_kernel<S, KS>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
   const int64_t blocks = nseg * (int64_t)ntiles;
   if (blocks > 0)
-    gram_i8_kernel<S><<<(unsigned)blocks, kQThreads, QCfg<S>::kSmem, s>>>(ma, mb, segmax, segs, tiles, ntiles, kp,
-                                                                          part);
+    gram_i8_kernel<S, KS><<<(unsigned)blocks, kQThreads, C::kSmem, s>>>(ma, mb, segmax, segs, tiles, ntiles, kp, part);
   return true;
 }
 
@@ -555,13 +564,17 @@ void launch_segmax(int dtype, const void* x, int64_t ldx, const void* y, int64_t
                    int64_t c_begin, int64_t c_end, int64_t nsrc, const double* shift, unsigned long long* segmax,
                    cudaStream_t s) {
   if (nseg <= 0 || c_end <= c_begin) return;
-  const dim3 grid((unsigned)nseg, (unsigned)((c_end - c_begin) / 64), (unsigned)((max_seg_rows + kSmRows - 1) / kSmRows));
+  // row slices: ~4096+ CTAs in all, 128 .. 1024 rows each
+  const int64_t nchunk = (c_end - c_begin) / 64;
+  int64_t slice = 1024;
+  while (slice > 128 && nseg * nchunk * ((max_seg_rows + slice - 1) / slice) < 4096) slice /= 2;
+  const dim3 grid((unsigned)nseg, (unsigned)nchunk, (unsigned)((max_seg_rows + slice - 1) / slice));
   if (dtype == 0)
     segmax_kernel<double><<<grid, kSmThreads, 0, s>>>((const double*)x, ldx, (const double*)y, ldy, k, m, src_row,
-                                                      segs, kp, c_begin, nsrc, shift, segmax);
+                                                      segs, kp, c_begin, nsrc, shift, slice, segmax);
   else
     segmax_kernel<float><<<grid, kSmThreads, 0, s>>>((const float*)x, ldx, (const float*)y, ldy, k, m, src_row, segs,
-                                                     kp, c_begin, nsrc, shift, segmax);
+                                                     kp, c_begin, nsrc, shift, slice, segmax);
 }
 
 bool launch_reorder_q(int dtype, int slices, const void* x, int64_t ldx, const void* y, int64_t ldy, int64_t k,
@@ -581,10 +594,23 @@ bool launch_reorder_q(int dtype, int slices, const void* x, int64_t ldx, const v
 #undef CVG_K1Q
 }
 
-bool launch_gram_i8(int slices, const int8_t* zq, const unsigned long long* segmax, int64_t zrows, int64_t kp, const GramTask* segs,
-                    int64_t nseg, const int2* tiles, int ntiles, double* part, cudaStream_t s) {
-  return slices == 6 ? launch_gram_i8_s<6>(zq, segmax, zrows, kp, segs, nseg, tiles, ntiles, part, s)
-                     : launch_gram_i8_s<7>(zq, segmax, zrows, kp, segs, nseg, tiles, ntiles, part, s);
+// Pipeline stage rows: 64 (SW64; S = 7 fits 2 stages of 84 KB) or, with CVG_I8_STAGE_ROWS=32, 32 (SW32; 5
+// stages of 42 KB).  c1 Gram 2.94 vs 3.35 ms, c4 12.9 vs 16.0 ms: fewer, longer MMA runs per barrier win.
+static int i8_stage_rows() {
+  static const int v = [] {
+    const char* e = std::getenv("CVG_I8_STAGE_ROWS");
+    return e && std::atoi(e) == 32 ? 32 : 64;
+  }();
+  return v;
+}
+
+bool launch_gram_i8(int slices, const int8_t* zq, const unsigned long long* segmax, int64_t zrows, int64_t kp,
+                    const GramTask* segs, int64_t nseg, const int2* tiles, int ntiles, double* part, cudaStream_t s) {
+  if (i8_stage_rows() == 64)
+    return slices == 6 ? launch_gram_i8_s<6, 64>(zq, segmax, zrows, kp, segs, nseg, tiles, ntiles, part, s)
+                       : launch_gram_i8_s<7, 64>(zq, segmax, zrows, kp, segs, nseg, tiles, ntiles, part, s);
+  return slices == 6 ? launch_gram_i8_s<6, 32>(zq, segmax, zrows, kp, segs, nseg, tiles, ntiles, part, s)
+                     : launch_gram_i8_s<7, 32>(zq, segmax, zrows, kp, segs, nseg, tiles, ntiles, part, s);
 }
 
 }  // namespace cvg

@@ -365,8 +365,9 @@ def gram_tiles(k: int, m: int, edge: int = 64):
 
 
 def fp64_kind() -> str:
-    """The fp64 Gram kind plans are created with: "i8" (int8 digit slices on tcgen05 kind::i8) or "dmma"."""
-    return "i8" if os.environ.get("CVG_FP64_KIND") == "i8" else "dmma"
+    """The fp64 Gram kind plans are created with: "i8" (exact int8 digit slices on tcgen05 kind::i8,
+    the default) or "dmma" (CVG_FP64_KIND=dmma: fp64 DMMA tiles)."""
+    return "dmma" if os.environ.get("CVG_FP64_KIND") == "dmma" else "i8"
 
 
 def i8_slices() -> int:
