@@ -59,13 +59,15 @@ struct QCfg {
   static constexpr int kSmem = kNst * kStage + 1024;
 };
 
-// kind::i8, signed A and B, int32 accumulate, both K-major, M = 128, N = 64.
-constexpr uint32_t kIdescI8 =
-    (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(QB >> 3) << 17) | ((uint32_t)(QA >> 4) << 24);
+// kind::i8, signed A and B, int32 accumulate, both K-major, M = 128, N = 64 * NS.
+template <int NS>
+constexpr uint32_t idesc_i8() {
+  return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(NS * QB >> 3) << 17) | ((uint32_t)(QA >> 4) << 24);
+}
 
 // CU: A-operand collector use -- 0 none, 1 fill, 2 use, 3 lastuse (consecutive MMAs of one A slice
 // keep it in the collector instead of re-reading shared memory).
-template <int CU>
+template <int CU, int NS>
 __device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t accumulate) {
 #define CVG_MMA_I8(Q)                                                       \
   asm volatile(                                                             \
@@ -74,7 +76,7 @@ __device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t a, uint64_t b, 
       "setp.ne.b32 p, %4, 0;\n"                                             \
       "tcgen05.mma.cta_group::1.kind::i8" Q " [%0], %1, %2, %3, p;\n"       \
       "}\n" ::"r"(tmem_d),                                                  \
-      "l"(a), "l"(b), "r"(kIdescI8), "r"(accumulate))
+      "l"(a), "l"(b), "r"(idesc_i8<NS>()), "r"(accumulate))
   if constexpr (CU == 1)
     CVG_MMA_I8(".collector::a::fill");
   else if constexpr (CU == 2)
@@ -90,21 +92,26 @@ __device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t a, uint64_t b, 
 #define CVG_I8_COLLECTOR 1
 #endif
 
-// pair (t, u) into accumulator t + u; A slice t held in the collector across its u run
-template <int S, int T, int U>
-__device__ __forceinline__ void mma_pairs(uint32_t tmem_d, uint64_t a, uint64_t b0, uint64_t b_step, bool first) {
-  if constexpr (T + U < S) {
-    constexpr int last = S - 1 - T;
-    constexpr int cu = !CVG_I8_COLLECTOR || last == 0 ? 0 : U == 0 ? 1 : U == last ? 3 : 2;
-    mma_i8<cu>(tmem_d + (uint32_t)((T + U) * QB), a, b0 + U * b_step, (first && T == 0) ? 0u : 1u);
-    mma_pairs<S, T, U + 1>(tmem_d, a, b0, b_step, first);
+// Pairs (t, u), u = 0 .. S-1-t, go into accumulators t + u, which sit side by side in TMEM
+// (accumulator d = columns 64d .. 64d + 63), and the B slices u sit side by side in shared
+// memory (one 64-column K-major tile each, SBO-uniform): so NS consecutive pairs are ONE
+// MMA with N = 64 NS (NS <= 4, N <= 256) -- 10 MMAs per K-step instead of 28 for S = 7.
+// A slice t stays in the collector across its run.
+template <int S, int T, int U0>
+__device__ __forceinline__ void mma_runs(uint32_t tmem_d, uint64_t a, uint64_t b0, uint64_t b_step, bool first) {
+  if constexpr (U0 < S - T) {
+    constexpr int NS = (S - T - U0) < 4 ? (S - T - U0) : 4;
+    constexpr bool only = U0 == 0 && NS == S - T;  // the whole run is one MMA
+    constexpr int cu = !CVG_I8_COLLECTOR || only ? 0 : U0 == 0 ? 1 : U0 + NS == S - T ? 3 : 2;
+    mma_i8<cu, NS>(tmem_d + (uint32_t)((T + U0) * QB), a, b0 + U0 * b_step, (first && T == 0) ? 0u : 1u);
+    mma_runs<S, T, U0 + NS>(tmem_d, a, b0, b_step, first);
   }
 }
 template <int S, int T>
 __device__ __forceinline__ void mma_slices(uint32_t tmem_d, uint64_t a0, uint64_t a_step, uint64_t b0, uint64_t b_step,
                                            bool first) {
   if constexpr (T < S) {
-    mma_pairs<S, T, 0>(tmem_d, a0 + T * a_step, b0, b_step, first);
+    mma_runs<S, T, 0>(tmem_d, a0 + T * a_step, b0, b_step, first);
     mma_slices<S, T + 1>(tmem_d, a0, a_step, b0, b_step, first);
   }
 }
@@ -168,9 +175,8 @@ __global__ void __launch_bounds__(kQThreads, 1)
   const int seg = blockIdx.x / ntiles;
   const int2 tile0 = tiles[blockIdx.x - seg * ntiles];
   const int ti = uniform(tile0.x), tj = uniform(tile0.y & 0xffff), wmask = uniform(tile0.y >> 16);
-  // B inside A's 128 columns (tj == 2ti or 2ti + 1): B is a slice of the A stage, no B load
-  const int inner = tj - 2 * ti;
-  const bool self = inner == 0 || inner == 1;
+  // B is always loaded into its own stage slices (even when it lies inside A's 128 columns): the
+  // merged-N MMAs need the S B slices side by side
   const GramTask task0 = segs[seg];
   const GramTask task{uniform(task0.zrow), uniform(task0.rows)};
   CVG_DCHECK(task.zrow % QK == 0 && task.rows % QK == 0 && task.rows > 0);
@@ -200,7 +206,7 @@ __global__ void __launch_bounds__(kQThreads, 1)
   auto opB = [&](int s) { return smem + s * C::kStage + S * C::kA; };
 
   if (warp == 0) {  // ---- TMA producer (whole warp waits; one elected lane issues)
-    const uint32_t bytes = (uint32_t)(S * C::kA + (self ? 0 : S * C::kB));
+    const uint32_t bytes = (uint32_t)(S * (C::kA + C::kB));
     for (int it = 0; it < nsteps; ++it) {
       const int s = it % NST;
       mbar_wait(&empty_bar[s], ((uint32_t)(it / NST) & 1u) ^ 1u);
@@ -208,7 +214,7 @@ __global__ void __launch_bounds__(kQThreads, 1)
       if (elect_one()) {
         mbar_expect_tx(&full_bar[s], bytes);
         tma_load_4d(opA(s), &map_a, &full_bar[s], r0, ti * QA, blk, 0);
-        if (!self) tma_load_4d(opB(s), &map_b, &full_bar[s], r0, tj * QB, blk, 0);
+        tma_load_4d(opB(s), &map_b, &full_bar[s], r0, tj * QB, blk, 0);
       }
       __syncwarp();
     }
@@ -218,8 +224,8 @@ __global__ void __launch_bounds__(kQThreads, 1)
       mbar_wait(&full_bar[s], (uint32_t)(it / NST) & 1u);
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
       const uint64_t a0 = kmajor_sw_desc<KS>(opA(s));
-      const uint64_t b0 = self ? kmajor_sw_desc<KS>(opA(s) + inner * QB * KS) : kmajor_sw_desc<KS>(opB(s));
-      const uint64_t a_step = (uint64_t)(C::kA >> 4), b_step = (uint64_t)((self ? C::kA : C::kB) >> 4);
+      const uint64_t b0 = kmajor_sw_desc<KS>(opB(s));
+      const uint64_t a_step = (uint64_t)(C::kA >> 4), b_step = (uint64_t)(C::kB >> 4);
       if (elect_one()) {
 #pragma unroll
         for (int k = 0; k < KS / 32; ++k)  // K = 32 int8 = 32 B per MMA: +2 in 16-byte descriptor units
