@@ -395,7 +395,14 @@ def run_ours(args):
     f32 = not x_dtype_is_f64(cid)
     executed = executed_gram_flops(n, k, m, p, f32) / max(world, 1) / (gram_ms * 1e-3) / 1e12
     tf32_kind = os.environ.get("CVG_FP32_KIND") == "tf32"
-    if f32 and tf32_kind:
+    f32_i8 = f32 and os.environ.get("CVG_FP32_KIND") == "i8"
+    if f32_i8:
+        s_ = i8_slices(True)
+        gram_kernel = (f"gram_i8_kernel<{s_}> (fp32 inputs as exact int8 digit slices on tcgen05 kind::i8, "
+                       f"{s_ * (s_ + 1) // 2} slice-pair products; CVG_FP32_KIND=i8)")
+        peak = INT8_PEAK_TOPS
+        peak_source = "NVIDIA nominal dense int8 (4.5 POPS); achieved = int8 tensor ops issued per second"
+    elif f32 and tf32_kind:
         gram_kernel = "gram_tf32_kernel (tcgen05.mma kind::tf32, 3xTF32, TMEM accumulators; CVG_FP32_KIND=tf32)"
         peak = TF32_PEAK_TFLOPS
         peak_source = ("measured cuBLAS TF32 GEMM (8192^3, sustained) on this pool's B200 "
@@ -421,7 +428,7 @@ def run_ours(args):
         peak_source = ("measured DMMA issue-loop peak on this pool's B200 (profiles/r01_fp64_peaks.txt); "
                        "MEASURED_PEAKS.json has no fp64 figure")
     # the int8 kernel is judged by the int8 tensor ops it issues (its fp64-equivalent rate is `value`)
-    i8_kind = not f32 and executed_fp64_kind() == "i8"
+    i8_kind = (not f32 and executed_fp64_kind() == "i8") or f32_i8
     rl_achieved = executed if i8_kind else achieved
     rl_unit = "TOPS (int8)" if i8_kind else "TFLOP/s"
     traffic = None
@@ -439,7 +446,7 @@ def run_ours(args):
     z_elem = 4 if (f32 and not tf32_kind) else 8  # Z: fp64 | fp16 hi + lo | tf32 hi + lo
     reorder_bytes = n * (k + m) * x_elt + n * (-(-(k + m + 1) // tile) * tile) * z_elem
     if i8_kind:  # segment max (one read of x | y) + K1Q (read x | y, write S int8 digit slices)
-        reorder_bytes = 2 * n * (k + m) * x_elt + n * (-(-(k + m + 1) // 64) * 64) * i8_slices()
+        reorder_bytes = 2 * n * (k + m) * x_elt + n * (-(-(k + m + 1) // tile) * tile) * i8_slices(f32)
     epi_bytes = len(masks) * (2 * p * k * (k + m) * 8) + k * (k + m) * 8
     line = {
         "metric": "all_fold_cv_gram_gflops", "value": round(value, 3), "unit": "GFLOP/s", "n_gpus": world,

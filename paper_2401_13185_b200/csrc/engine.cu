@@ -248,6 +248,16 @@ static int i8_slices_env() {
   const char* e = std::getenv("CVG_I8_SLICES");
   return e && std::atoi(e) == 6 ? 6 : 7;
 }
+// fp32 inputs on the int8 digit path (CVG_FP32_KIND=i8): 4 digits (27 bits below each segment column's
+// max, fp32 carries 24) or, with CVG_I8_SLICES_F32=3, 3 digits (20 bits; ~1e-6, inside the 1e-4 gate).
+static bool fp32_i8_env() {
+  const char* e = std::getenv("CVG_FP32_KIND");
+  return e && std::string(e) == "i8";
+}
+static int i8_slices_f32_env() {
+  const char* e = std::getenv("CVG_I8_SLICES_F32");
+  return e && std::atoi(e) == 3 ? 3 : 4;
+}
 
 // The fp16 path's row group G (one exponent per group and column, one fp32 TMEM
 // chunk) is also the fold padding and segment alignment.  Largest of 256 / 128 /
@@ -255,7 +265,7 @@ static int i8_slices_env() {
 // global fold sizes only, so every rank plan picks the same G.
 void Plan::choose_row_step() {
   row_step_ = kRowStep;
-  if (dtype_ == 0 && i8_) row_step_ = 64;  // one int8 Gram stage
+  if (i8_) row_step_ = 64;  // one int8 Gram stage
   if (!f16_path()) return;
   auto padded = [&](int64_t g) {
     int64_t t = 0;
@@ -324,8 +334,8 @@ Status Plan::create(cvg_context* ctx, int dtype, int64_t n, int64_t k, int64_t m
   kp_ = padded_cols(k, m, dtype);
   tiles_ = gram_tiles(k, m, kp_);
   tiles128_ = dtype == 1 ? gram_tiles(k, m, kp_, kTileF32) : std::vector<int2>{};
-  i8_ = dtype == 0 && fp64_i8_env();
-  slices_ = i8_slices_env();
+  i8_ = dtype == 0 ? fp64_i8_env() : fp32_i8_env();
+  slices_ = dtype == 0 ? i8_slices_env() : i8_slices_f32_env();
   tilesq_.clear();
   if (i8_) {  // 128 x 64 int8-Gram tiles covering the needed upper 64-tiles (i, j): I = i / 2, J = j
     for (const int2& t : tiles_) {
@@ -560,7 +570,7 @@ Status Plan::plan_segments() {
   cudaStream_t s = ctx_->stream;
   CVG_TRY(zbase_d_.ensure(sizeof(int64_t) * std::max(nown, 1)));
   CVG_TRY(src_row_.ensure(sizeof(int64_t) * std::max<int64_t>(zrows_, 1)));
-  if (dtype_ == 1) {  // blocked-transposed hi / lo operands for the tcgen05 Gram (fp16 or TF32)
+  if (dtype_ == 1 && !i8_path()) {  // blocked-transposed hi / lo operands for the tcgen05 Gram (fp16 or TF32)
     const size_t e = f16_path() ? 2 : 4;
     CVG_TRY(zt_hi_.ensure(e * std::max<int64_t>(zrows_, row_step_) * kp_));
     CVG_TRY(zt_lo_.ensure(e * std::max<int64_t>(zrows_, row_step_) * kp_));
@@ -669,7 +679,7 @@ Status Plan::gram(const void* d_x, int64_t ldx, const void* d_y, int64_t ldy, co
     CVG_TRY(count_launch());
   }
   CVG_CK(cudaMemsetAsync(flag_.as<void>(), 0, sizeof(int), s));
-  if (dtype_ == 1) {
+  if (dtype_ == 1 && !i8_path()) {
     // fp32: K1H / K1T (bucket, shift, split, blocked transpose) then the tcgen05 Gram.
     if (zrows_ > 0) {
       {
@@ -778,9 +788,9 @@ Status Plan::gram_host(const void* h_x, const void* h_y, void* d_x, void* d_y, c
   cudaStream_t s = ctx_->stream;
   CVG_TRY(ctx_->ensure_copy_stream());
   const size_t e = dtype_ == 1 ? 4 : 8;
-  const int E = dtype_ == 1 ? kTileF32 : kTile;
+  const int E = dtype_ == 1 && !i8_path() ? kTileF32 : kTile;
   const int nt = (int)(kp_ / E);
-  const std::vector<int2>& tl = dtype_ == 1 ? tiles128_ : i8_path() ? tilesq_ : tiles_;
+  const std::vector<int2>& tl = i8_path() ? tilesq_ : dtype_ == 1 ? tiles128_ : tiles_;
   // the last 64-column block a tile reads (int8 tiles: the A rows they write, and J)
   auto last_col = [&](const int2& t) {
     if (!i8_path()) return t.y;

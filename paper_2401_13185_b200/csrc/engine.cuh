@@ -156,11 +156,11 @@ class Plan {
     for (const GramTask& g : segs_) r = std::max(r, g.rows);
     return r;
   }
-  bool f16_path() const { return dtype_ == 1 && !fp32_tf32(); }
+  bool f16_path() const { return dtype_ == 1 && !fp32_tf32() && !i8_; }
   static bool fp32_tf32();
   // fp64 Gram on tcgen05 kind::i8 (int8 digit slices, k_gram_i8.cu); small-fold mode keeps
   // the DMMA path (its epilogue reads fp64 Z rows).
-  bool i8_path() const { return dtype_ == 0 && i8_ && !small_; }
+  bool i8_path() const { return i8_ && !small_; }
   void choose_row_step();  // fold padding / segment alignment (fp16 path: its row group G)
 
   cvg_context* ctx_ = nullptr;
@@ -170,8 +170,8 @@ class Plan {
   std::vector<int2> tiles_, out_tiles_, tiles128_;
   std::vector<int4> pairs128_;  // CTA-pair tiles for the cta_group::2 fp32 Gram
   std::vector<int2> tilesq_;    // int8 Gram tiles {I (128 rows), J (64 columns) | write mask << 16}
-  bool i8_ = false;             // fp64 kind: int8 slices (default) or DMMA (CVG_FP64_KIND=dmma)
-  int slices_ = 7;              // int8 digits per value (CVG_I8_SLICES = 6 or 7)
+  bool i8_ = false;             // int8 digit slices: fp64 default (CVG_FP64_KIND=dmma: DMMA); fp32 with CVG_FP32_KIND=i8
+  int slices_ = 7;              // int8 digits per value (fp64: CVG_I8_SLICES = 6 | 7; fp32: CVG_I8_SLICES_F32 = 3 | 4)
   DevBuf pairs128_d_;
   std::vector<int64_t> counts_;  // per fold (all p) validation sizes
   std::vector<GramTask> segs_;

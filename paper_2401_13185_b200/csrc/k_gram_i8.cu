@@ -383,6 +383,9 @@ __global__ void __launch_bounds__(kSmThreads) segmax_kernel(const T* __restrict_
 // digits reach 64 - 64/127).  Four rows' 7-bit fields are packed into one word by byte
 // permutes and shifted by -64 byte-wise (SWAR, no borrows).
 constexpr int kQ1Threads = 256;
+#ifndef CVG_K1Q_MIN_BLOCKS
+#define CVG_K1Q_MIN_BLOCKS 2
+#endif
 
 template <int S>
 struct DigitOffset {  // 64 * (128^S - 1) / 127
@@ -402,7 +405,7 @@ __device__ __forceinline__ void tma_store_4d(const CUtensorMap* map, const void*
 }
 
 template <typename T, int S>
-__global__ void __launch_bounds__(kQ1Threads, 2)
+__global__ void __launch_bounds__(kQ1Threads, CVG_K1Q_MIN_BLOCKS)
     reorder_q_kernel(const __grid_constant__ CUtensorMap map_out, const T* __restrict__ x, int64_t ldx,
                      const T* __restrict__ y, int64_t ldy, int64_t k, int64_t m, const int64_t* __restrict__ src_row,
                      int64_t zrows, int64_t kp, int64_t c_begin, int64_t c_end, int64_t nsrc,
@@ -594,8 +597,8 @@ bool launch_reorder_q(int dtype, int slices, const void* x, int64_t ldx, const v
     if (slices == 6) CVG_K1Q(double, 6);
     else CVG_K1Q(double, 7);
   } else {
-    if (slices == 6) CVG_K1Q(float, 6);
-    else CVG_K1Q(float, 7);
+    if (slices == 3) CVG_K1Q(float, 3);
+    else CVG_K1Q(float, 4);
   }
 #undef CVG_K1Q
 }
@@ -612,11 +615,16 @@ static int i8_stage_rows() {
 
 bool launch_gram_i8(int slices, const int8_t* zq, const unsigned long long* segmax, int64_t zrows, int64_t kp,
                     const GramTask* segs, int64_t nseg, const int2* tiles, int ntiles, double* part, cudaStream_t s) {
-  if (i8_stage_rows() == 64)
-    return slices == 6 ? launch_gram_i8_s<6, 64>(zq, segmax, zrows, kp, segs, nseg, tiles, ntiles, part, s)
-                       : launch_gram_i8_s<7, 64>(zq, segmax, zrows, kp, segs, nseg, tiles, ntiles, part, s);
-  return slices == 6 ? launch_gram_i8_s<6, 32>(zq, segmax, zrows, kp, segs, nseg, tiles, ntiles, part, s)
-                     : launch_gram_i8_s<7, 32>(zq, segmax, zrows, kp, segs, nseg, tiles, ntiles, part, s);
+#define CVG_GRAM_I8(S)                                                                                       \
+  return i8_stage_rows() == 64 ? launch_gram_i8_s<S, 64>(zq, segmax, zrows, kp, segs, nseg, tiles, ntiles, part, s) \
+                               : launch_gram_i8_s<S, 32>(zq, segmax, zrows, kp, segs, nseg, tiles, ntiles, part, s)
+  switch (slices) {
+    case 3: CVG_GRAM_I8(3);
+    case 4: CVG_GRAM_I8(4);
+    case 6: CVG_GRAM_I8(6);
+    default: CVG_GRAM_I8(7);
+  }
+#undef CVG_GRAM_I8
 }
 
 }  // namespace cvg

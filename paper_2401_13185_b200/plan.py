@@ -370,19 +370,27 @@ def fp64_kind() -> str:
     return "dmma" if os.environ.get("CVG_FP64_KIND") == "dmma" else "i8"
 
 
-def i8_slices() -> int:
+def i8_slices(f32: bool = False) -> int:
+    if f32:
+        return 3 if os.environ.get("CVG_I8_SLICES_F32") == "3" else 4
     return 6 if os.environ.get("CVG_I8_SLICES") == "6" else 7
+
+
+def fp32_kind() -> str:
+    """The fp32 Gram kind: "f16" (scaled fp16 hi/lo on kind::f16, default), "tf32" or "i8" (CVG_FP32_KIND)."""
+    v = os.environ.get("CVG_FP32_KIND")
+    return v if v in ("tf32", "i8") else "f16"
 
 
 def executed_gram_flops(n: int, k: int, m: int, p: int, f32: bool = False) -> float:
     """Tensor-core flops the Gram kernel issues for n rows (fold padding ignored):
     fp64: 64x64 DMMA tiles, diagonal tiles only their 36 upper 8x8 blocks;
     fp32: 128x128 tcgen05 tiles x 3 products (fp16 hi/lo split by default, TF32 with CVG_FP32_KIND=tf32)."""
-    if f32:
+    if f32 and fp32_kind() != "i8":
         return 3 * 2.0 * len(gram_tiles(k, m, 128)) * 128 * 128 * n
     tiles = gram_tiles(k, m)
-    if fp64_kind() == "i8":  # int8 ops: 128x64 tiles x S(S+1)/2 slice pairs
-        s = i8_slices()
+    if f32 or fp64_kind() == "i8":  # int8 ops: 128x64 tiles x S(S+1)/2 slice pairs
+        s = i8_slices(f32)
         tq = {(i // 2, j) for i, j in tiles}
         return 2.0 * len(tq) * 128 * 64 * n * (s * (s + 1) // 2)
     n_diag = sum(1 for i, j in tiles if i == j)
