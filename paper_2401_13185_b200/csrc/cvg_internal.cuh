@@ -183,17 +183,22 @@ bool launch_gram_tf32_2sm(const float* zt_hi, const float* zt_lo, int64_t zrows,
 // Zq[t][row / 64][col][64]; the tcgen05 kind::i8 Gram sums the slice pairs t + u < slices into
 // int32 TMEM and drains each (segment, 128 x 64 tile) once into the fp64 partial.
 // blkseg[b]: segment of Z's 64-row block b.  tiles: {I, J | write mask << 16}.
-// segmax must be zeroed before (bits of max |z| per (segment, column); atomicMax).
+// segmax must be zeroed before (bits of max |z| per (segment, column); atomicMax).  stride > 1: the
+// max over rows 0, stride, 2 stride, ... of each segment (the exponents then keep 2x headroom);
+// only != null: just the segments with only[seg] set (the exact pass, on top of the sampled max).
 void launch_segmax(int dtype, const void* x, int64_t ldx, const void* y, int64_t ldy, int64_t k, int64_t m,
                    const int64_t* src_row, const GramTask* segs, int64_t nseg, int64_t max_seg_rows, int64_t kp,
-                   int64_t c_begin, int64_t c_end, int64_t nsrc, const double* shift, unsigned long long* segmax,
-                   cudaStream_t s);
+                   int64_t c_begin, int64_t c_end, int64_t nsrc, const double* shift, int stride, const int* only,
+                   unsigned long long* segmax, cudaStream_t s);
+// ovf != null (sampled exponents): a value outside the digits' range sets ovf[its segment];
+// ovf == null: sets *nonfinite.
 bool launch_reorder_q(int dtype, int slices, const void* x, int64_t ldx, const void* y, int64_t ldy, int64_t k,
                       int64_t m, const int64_t* src_row, int64_t zrows, int64_t kp, int64_t c_begin, int64_t c_end,
-                      int64_t nsrc, const double* shift, const int* blkseg, const unsigned long long* segmax, int8_t* zq,
-                      int* nonfinite, cudaStream_t s);
-bool launch_gram_i8(int slices, const int8_t* zq, const unsigned long long* segmax, int64_t zrows, int64_t kp, const GramTask* segs,
-                    int64_t nseg, const int2* tiles, int ntiles, double* part, cudaStream_t s);
+                      int64_t nsrc, const double* shift, const int* blkseg, const unsigned long long* segmax,
+                      int headroom, int* ovf, int8_t* zq, int* nonfinite, cudaStream_t s);
+bool launch_gram_i8(int slices, const int8_t* zq, const unsigned long long* segmax, int headroom, int64_t zrows,
+                    int64_t kp, const GramTask* segs, int64_t nseg, const int2* tiles, int ntiles, double* part,
+                    cudaStream_t s);
 
 inline int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
 inline int64_t padded_cols(int64_t k, int64_t m, int dtype = 0) {

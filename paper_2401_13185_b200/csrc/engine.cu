@@ -250,6 +250,12 @@ static int i8_slices_env() {
 }
 // fp32 inputs on the int8 digit path (CVG_FP32_KIND=i8): 4 digits (27 bits below each segment column's
 // max, fp32 carries 24) or, with CVG_I8_SLICES_F32=3, 3 digits (20 bits; ~1e-6, inside the 1e-4 gate).
+// Row-sample stride of the int8 path's segment maxima (CVG_I8_SAMPLE; 1 = every row, one exact pass).
+static int i8_sample_env() {
+  const char* e = std::getenv("CVG_I8_SAMPLE");
+  const int v = e ? std::atoi(e) : 16;
+  return v >= 1 ? v : 16;
+}
 static bool fp32_i8_env() {
   const char* e = std::getenv("CVG_FP32_KIND");
   return e && std::string(e) == "i8";
@@ -336,6 +342,7 @@ Status Plan::create(cvg_context* ctx, int dtype, int64_t n, int64_t k, int64_t m
   tiles128_ = dtype == 1 ? gram_tiles(k, m, kp_, kTileF32) : std::vector<int2>{};
   i8_ = dtype == 0 ? fp64_i8_env() : fp32_i8_env();
   slices_ = dtype == 0 ? i8_slices_env() : i8_slices_f32_env();
+  sample_ = i8_sample_env();
   tilesq_.clear();
   if (i8_) {  // 128 x 64 int8-Gram tiles covering the needed upper 64-tiles (i, j): I = i / 2, J = j
     for (const int2& t : tiles_) {
@@ -578,6 +585,7 @@ Status Plan::plan_segments() {
   } else if (i8_path()) {  // int8 digit slices, per-(segment, column) exponents, 64-row block -> segment
     CVG_TRY(zq_.ensure((size_t)slices_ * std::max<int64_t>(zrows_, 64) * kp_));
     CVG_TRY(segmax_.ensure(sizeof(unsigned long long) * std::max<size_t>(segs_.size(), 1) * kp_));
+    CVG_TRY(ovf_.ensure(sizeof(int) * std::max<size_t>(segs_.size(), 1)));
     std::vector<int> bs(std::max<int64_t>(zrows_ / 64, 1), 0);
     for (size_t sgi = 0; sgi < segs_.size(); ++sgi)
       for (int64_t r = segs_[sgi].zrow; r < segs_[sgi].zrow + segs_[sgi].rows; r += 64) bs[r / 64] = (int)sgi;
@@ -720,32 +728,13 @@ Status Plan::gram(const void* d_x, int64_t ldx, const void* d_y, int64_t ldy, co
   } else if (i8_path()) {
     // fp64 on int8 digit slices: segment exponents, K1Q, tcgen05 kind::i8 Gram.
     if (zrows_ > 0) {
-      {
-        Timed t(ctx_, kReorder);
-        CVG_CK(cudaMemsetAsync(segmax_.as<void>(), 0, sizeof(unsigned long long) * segs_.size() * kp_, s));
-        launch_segmax(dtype_, d_x, ldx, d_y, ldy, k_, m_, rows, segs_d_.as<GramTask>(), (int64_t)segs_.size(),
-                      max_seg_rows(), kp_, 0, kp_, nsrc, shift, segmax_.as<unsigned long long>(), s);
-      }
-      CVG_TRY(count_launch());
-      {
-        Timed t(ctx_, kReorder);
-        if (!launch_reorder_q(dtype_, slices_, d_x, ldx, d_y, ldy, k_, m_, rows, zrows_, kp_, 0, kp_, nsrc, shift,
-                              blkseg_.as<int>(), segmax_.as<unsigned long long>(), zq_.as<int8_t>(), flag_.as<int>(),
-                              s))
-          return Status::Err(5, "cuTensorMapEncodeTiled unavailable or rejected the operand layout");
-      }
-      CVG_TRY(count_launch());
+      CVG_CK(cudaMemsetAsync(segmax_.as<void>(), 0, sizeof(unsigned long long) * segs_.size() * kp_, s));
+      if (sample_ > 1) CVG_CK(cudaMemsetAsync(ovf_.as<void>(), 0, sizeof(int) * segs_.size(), s));
+      CVG_TRY(i8_prep(d_x, ldx, d_y, ldy, rows, nsrc, 0, kp_, false));
     }
-    if (!segs_.empty()) {
-      bool ok;
-      {
-        Timed t(ctx_, kGram);
-        ok = launch_gram_i8(slices_, zq_.as<int8_t>(), segmax_.as<unsigned long long>(), zrows_, kp_, segs_d_.as<GramTask>(),
-                            (int64_t)segs_.size(), tilesq_d_.as<int2>(), (int)tilesq_.size(), part_.as<double>(), s);
-      }
-      if (!ok) return Status::Err(5, "cuTensorMapEncodeTiled unavailable or rejected the operand layout");
-      CVG_TRY(count_launch());
-    }
+    CVG_TRY(i8_gram(tilesq_d_.as<int2>(), (int)tilesq_.size()));
+    CVG_TRY(gram_trees());
+    return i8_exact_pass(d_x, ldx, d_y, ldy, rows, nsrc);
   } else {
     // fp64: K1 builds the fold-bucketed, shifted copy Z.  (Gathering X rows
     // straight into the Gram's shared-memory stages, or overlapping K1 with K2
@@ -767,6 +756,63 @@ Status Plan::gram(const void* d_x, int64_t ldx, const void* d_y, int64_t ldy, co
       CVG_TRY(count_launch());
     }
   }
+  return gram_trees();
+}
+
+// One int8-path preparation pass over Z columns [c0, c1): segment maxima (a row sample of stride
+// sample_, or -- exact pass -- every row of the segments flagged in ovf_, on top of the sampled max),
+// then K1Q (sampled pass: out-of-range values flag their segment; exact pass: the non-finite flag).
+Status Plan::i8_prep(const void* d_x, int64_t ldx, const void* d_y, int64_t ldy, const int64_t* rows, int64_t nsrc,
+                     int64_t c0, int64_t c1, bool exact) {
+  cudaStream_t s = ctx_->stream;
+  const bool sampled = sample_ > 1;
+  {
+    Timed t(ctx_, kReorder);
+    launch_segmax(dtype_, d_x, ldx, d_y, ldy, k_, m_, rows, segs_d_.as<GramTask>(), (int64_t)segs_.size(),
+                  max_seg_rows(), kp_, c0, c1, nsrc, shift_.as<double>(), exact ? 1 : sample_,
+                  exact ? ovf_.as<int>() : nullptr, segmax_.as<unsigned long long>(), s);
+  }
+  CVG_TRY(count_launch());
+  {
+    Timed t(ctx_, kReorder);
+    if (!launch_reorder_q(dtype_, slices_, d_x, ldx, d_y, ldy, k_, m_, rows, zrows_, kp_, c0, c1, nsrc,
+                          shift_.as<double>(), blkseg_.as<int>(), segmax_.as<unsigned long long>(), sampled ? 1 : 0,
+                          sampled && !exact ? ovf_.as<int>() : nullptr, zq_.as<int8_t>(), flag_.as<int>(), s))
+      return Status::Err(5, "cuTensorMapEncodeTiled unavailable or rejected the operand layout");
+  }
+  return count_launch();
+}
+
+Status Plan::i8_gram(const int2* tiles, int ntiles) {
+  if (segs_.empty() || ntiles == 0) return Status::Ok();
+  bool ok;
+  {
+    Timed t(ctx_, kGram);
+    ok = launch_gram_i8(slices_, zq_.as<int8_t>(), segmax_.as<unsigned long long>(), sample_ > 1 ? 1 : 0, zrows_, kp_,
+                        segs_d_.as<GramTask>(), (int64_t)segs_.size(), tiles, ntiles, part_.as<double>(),
+                        ctx_->stream);
+  }
+  if (!ok) return Status::Err(5, "cuTensorMapEncodeTiled unavailable or rejected the operand layout");
+  return count_launch();
+}
+
+// Sampled exponents only: if any segment held a value beyond 2x its sampled max (or a nonzero value
+// in a column whose sample was all zero), redo those segments' maxima over every row, then K1Q and the
+// Gram for all columns (unflagged segments reproduce the same bits) and the trees.  The decision is per
+// segment and depends on the segment's rows only, so results stay bit-identical across GPU counts.
+Status Plan::i8_exact_pass(const void* d_x, int64_t ldx, const void* d_y, int64_t ldy, const int64_t* rows,
+                           int64_t nsrc) {
+  if (sample_ <= 1 || segs_.empty()) return Status::Ok();
+  cudaStream_t s = ctx_->stream;
+  ovf_host_.resize(segs_.size());
+  CVG_CK(cudaMemcpyAsync(ovf_host_.data(), ovf_.as<int>(), sizeof(int) * segs_.size(), cudaMemcpyDeviceToHost, s));
+  CVG_CK(cudaStreamSynchronize(s));
+  int64_t flagged = 0;
+  for (int v : ovf_host_) flagged += v != 0;
+  exact_segments_ = flagged;
+  if (!flagged) return Status::Ok();
+  CVG_TRY(i8_prep(d_x, ldx, d_y, ldy, rows, nsrc, 0, kp_, true));
+  CVG_TRY(i8_gram(tilesq_d_.as<int2>(), (int)tilesq_.size()));
   return gram_trees();
 }
 
@@ -818,8 +864,10 @@ Status Plan::gram_host(const void* h_x, const void* h_y, void* d_x, void* d_y, c
   double* shift = shift_.as<double>();
   CVG_TRY(shift_stage_.upload({{host_shift, sizeof(double) * w_, shift}}, s));
   CVG_CK(cudaMemsetAsync(flag_.as<void>(), 0, sizeof(int), s));
-  if (i8_path() && !segs_.empty())
+  if (i8_path() && !segs_.empty()) {
     CVG_CK(cudaMemsetAsync(segmax_.as<void>(), 0, sizeof(unsigned long long) * segs_.size() * kp_, s));
+    if (sample_ > 1) CVG_CK(cudaMemsetAsync(ovf_.as<void>(), 0, sizeof(int) * segs_.size(), s));
+  }
   // the copy stream may overwrite d_x / d_y only after earlier work on s is done
   cudaEvent_t ev0 = ctx_->stream_event(0);
   CVG_CK(cudaEventRecord(ev0, s));
@@ -841,22 +889,15 @@ Status Plan::gram_host(const void* h_x, const void* h_y, void* d_x, void* d_y, c
     CVG_CK(cudaEventRecord(ev, ctx_->copy_stream));
     CVG_CK(cudaStreamWaitEvent(s, ev, 0));
     const int t0 = off[slab], t1 = off[slab + 1];
-    if (zrows_ > 0) {
+    if (zrows_ > 0 && i8_path()) {
+      CVG_TRY(i8_prep(d_x, k_, d_y, m_, src_row_.as<int64_t>(), src_n_, z0, z1, false));
+    } else if (zrows_ > 0) {
       {
         Timed t(ctx_, kReorder);
         if (f16_path()) {
           launch_reorder_split_h(dtype_, d_x, k_, d_y, m_, k_, m_, src_row_.as<int64_t>(), zrows_, kp_, z0, z1, src_n_,
                                  shift, (int)row_step_, zt_hi_.as<void>(), zt_lo_.as<void>(), unscale_.as<float>(),
                                  flag_.as<int>(), s);
-        } else if (i8_path()) {
-          launch_segmax(dtype_, d_x, k_, d_y, m_, k_, m_, src_row_.as<int64_t>(), segs_d_.as<GramTask>(),
-                        (int64_t)segs_.size(), max_seg_rows(), kp_, z0, z1, src_n_, shift,
-                        segmax_.as<unsigned long long>(), s);
-          CVG_TRY(count_launch());
-          if (!launch_reorder_q(dtype_, slices_, d_x, k_, d_y, m_, k_, m_, src_row_.as<int64_t>(), zrows_, kp_, z0, z1,
-                                src_n_, shift, blkseg_.as<int>(), segmax_.as<unsigned long long>(), zq_.as<int8_t>(),
-                                flag_.as<int>(), s))
-            return Status::Err(5, "cuTensorMapEncodeTiled unavailable or rejected the operand layout");
         }
         else if (dtype_ == 1)
           launch_reorder_split_t(dtype_, d_x, k_, d_y, m_, k_, m_, src_row_.as<int64_t>(), zrows_, kp_, z0, z1, shift,
@@ -876,8 +917,9 @@ Status Plan::gram_host(const void* h_x, const void* h_y, void* d_x, void* d_y, c
                                 kp_, segs_d_.as<GramTask>(), (int64_t)segs_.size(), tiles_bycol_d_.as<int2>() + t0,
                                 t1 - t0, part_.as<double>(), s);
         else if (i8_path())
-          ok = launch_gram_i8(slices_, zq_.as<int8_t>(), segmax_.as<unsigned long long>(), zrows_, kp_, segs_d_.as<GramTask>(),
-                              (int64_t)segs_.size(), tiles_bycol_d_.as<int2>() + t0, t1 - t0, part_.as<double>(), s);
+          ok = launch_gram_i8(slices_, zq_.as<int8_t>(), segmax_.as<unsigned long long>(), sample_ > 1 ? 1 : 0, zrows_,
+                              kp_, segs_d_.as<GramTask>(), (int64_t)segs_.size(), tiles_bycol_d_.as<int2>() + t0,
+                              t1 - t0, part_.as<double>(), s);
         else if (dtype_ == 1)
           ok = launch_gram_tf32(zt_hi_.as<float>(), zt_lo_.as<float>(), zrows_, kp_, segs_d_.as<GramTask>(),
                                 (int64_t)segs_.size(), tiles_bycol_d_.as<int2>() + t0, t1 - t0, part_.as<double>(), 3,
@@ -890,7 +932,8 @@ Status Plan::gram_host(const void* h_x, const void* h_y, void* d_x, void* d_y, c
       CVG_TRY(count_launch());
     }
   }
-  return gram_trees();
+  CVG_TRY(gram_trees());
+  return i8_path() ? i8_exact_pass(d_x, k_, d_y, m_, src_row_.as<int64_t>(), src_n_) : Status::Ok();
 }
 
 Status Plan::finish(const double* d_rank_partials, int32_t n_ranks, const double* total_override,

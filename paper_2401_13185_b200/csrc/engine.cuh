@@ -138,6 +138,10 @@ class Plan {
  private:
   Status plan_segments();
   Status gram_trees();
+  Status i8_prep(const void* d_x, int64_t ldx, const void* d_y, int64_t ldy, const int64_t* rows, int64_t nsrc,
+                 int64_t c0, int64_t c1, bool exact);
+  Status i8_gram(const int2* tiles, int ntiles);
+  Status i8_exact_pass(const void* d_x, int64_t ldx, const void* d_y, int64_t ldy, const int64_t* rows, int64_t nsrc);
   static bool small_folds_enabled();
   SmallFolds small_folds() const {
     SmallFolds sf;
@@ -171,6 +175,9 @@ class Plan {
   std::vector<int4> pairs128_;  // CTA-pair tiles for the cta_group::2 fp32 Gram
   std::vector<int2> tilesq_;    // int8 Gram tiles {I (128 rows), J (64 columns) | write mask << 16}
   bool i8_ = false;             // int8 digit slices: fp64 default (CVG_FP64_KIND=dmma: DMMA); fp32 with CVG_FP32_KIND=i8
+  int sample_ = 16;             // int8 path: segment maxima over every sample_-th row (CVG_I8_SAMPLE; 1 = exact)
+  int64_t exact_segments_ = 0;  // segments the last gram redid from their exact max
+  std::vector<int> ovf_host_;
   int slices_ = 7;              // int8 digits per value (fp64: CVG_I8_SLICES = 6 | 7; fp32: CVG_I8_SLICES_F32 = 3 | 4)
   DevBuf pairs128_d_;
   std::vector<int64_t> counts_;  // per fold (all p) validation sizes
@@ -189,7 +196,7 @@ class Plan {
   TreeProgram group_tree_;
   DevBuf zero_g_, zero_nval_, zero_ptr_;
 
-  DevBuf zq_, segmax_, blkseg_, tilesq_d_, tiles_d_, out_tiles_d_, tiles128_d_, zt_hi_, zt_lo_, unscale_, tile_counts_, fold_counts_, bad_, zbase_d_, src_row_, z_, part_, foldbuf_, local_,
+  DevBuf zq_, segmax_, ovf_, blkseg_, tilesq_d_, tiles_d_, out_tiles_d_, tiles128_d_, zt_hi_, zt_lo_, unscale_, tile_counts_, fold_counts_, bad_, zbase_d_, src_row_, z_, part_, foldbuf_, local_,
       total_, shift_, flag_, tiles_bycol_d_, src_map_, segs_d_, foldptr_d_, nval_d_, st_mz_, st_sT_, st_sd_, cfg_d_;
   TreeProgram fold_tree_, local_tree_, rank_tree_;
   PinnedStage blkseg_stage_, seg_stage_, ptr_stage_, shift_stage_, cfg_stage_, col_stage_;

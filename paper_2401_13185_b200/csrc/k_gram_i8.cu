@@ -144,15 +144,16 @@ __device__ __forceinline__ double pow2(int e) {  // 2^e for e in [-1022, 1023]
 }
 
 // The segment exponent of a column whose max |z| is mx: max |z| 2^e in [31.5, 63), so every
-// value is representable by the offset digits (|w| < 63 < 64 - 64/127); e = 0 for an
-// all-zero (or non-finite) column.  e <= 1000
-// keeps 2^(e + 7(S-1)) a normal double (columns below 2^-994 lose digits; their Gram
-// entries are below 2^-1988 and round to zero in fp64 anyway).
-__device__ __forceinline__ int seg_exponent(double mx) {
+// value is representable by the offset digits (|w| < 63 < 64 - 64/127); with `headroom` (mx is
+// the max over a row sample) in [15.75, 31.5), so values up to 2x the sampled max still fit
+// (larger ones are caught by K1Q and the segment is redone from its exact max).  e = 0 for an
+// all-zero (or non-finite) column.  e <= 1000 keeps 2^(e + 7(S-1)) a normal double (columns
+// below 2^-994 lose digits; their Gram entries are below 2^-1988 and round to zero in fp64 anyway).
+__device__ __forceinline__ int seg_exponent(double mx, int headroom) {
   if (!(mx > 0.0) || !isfinite(mx)) return 0;
   const int be = (int)((__double_as_longlong(mx) >> 52) & 0x7ff);  // 0 for subnormal maxima
-  int e = 5 - (be - 1023);
-  if (e <= 1000 && mx * pow2(e) >= 63.0) --e;
+  int e = (headroom ? 4 : 5) - (be - 1023);
+  if (e <= 1000 && mx * pow2(e) >= (headroom ? 31.5 : 63.0)) --e;
   return min(e, 1000);
 }
 
@@ -163,7 +164,7 @@ __global__ void __launch_bounds__(kQThreads, 1)
     gram_i8_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                    const unsigned long long* __restrict__ segmax, const GramTask* __restrict__ segs,
                    const int2* __restrict__ tiles,
-                   int ntiles, int64_t kp, double* __restrict__ part) {
+                   int ntiles, int64_t kp, double* __restrict__ part, int headroom) {
   using C = QCfg<S, KS>;
   constexpr int NST = C::kNst;
   constexpr int kPer = QK / KS;  // stages per 64-row block
@@ -243,8 +244,9 @@ __global__ void __launch_bounds__(kQThreads, 1)
     const int64_t col0 = (int64_t)tj * QB + 32 * h;
     const bool write = row < kp && ((wmask >> (q >> 1)) & 1);
     const unsigned long long* mx = segmax + (int64_t)seg * kp;
-    const double urow = pow2(-seg_exponent(__longlong_as_double((long long)mx[row < kp ? row : 0])));
-    const double ucol = pow2(-seg_exponent(__longlong_as_double((long long)mx[col0 + lane])));  // lane j: column col0 + j
+    const double urow = pow2(-seg_exponent(__longlong_as_double((long long)mx[row < kp ? row : 0]), headroom));
+    const double ucol =
+        pow2(-seg_exponent(__longlong_as_double((long long)mx[col0 + lane]), headroom));  // lane j: column col0 + j
     mbar_wait(&acc_full, 0);
     asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
     double* out = part + (int64_t)seg * kp * kp + row * kp + col0;
@@ -303,14 +305,20 @@ __global__ void __launch_bounds__(kSmThreads) segmax_kernel(const T* __restrict_
                                                             const GramTask* __restrict__ segs, int64_t kp,
                                                             int64_t c_begin, int64_t nsrc,
                                                             const double* __restrict__ shift, int64_t slice,
+                                                            int stride, const int* __restrict__ only,
                                                             unsigned long long* __restrict__ segmax) {
   constexpr int NW = kSmThreads / 32;
   __shared__ double s_max[NW][64];
   const int seg = blockIdx.x;
+  if (only && !only[seg]) return;  // exact pass: only the segments whose sample fell short
   const int64_t c0 = c_begin + 64 * (int64_t)blockIdx.y;
   const GramTask task = segs[seg];
+  // sampled row indices j (rows j * stride of the segment), sliced over blockIdx.z; a segment keeps at
+  // least 512 sampled rows (short segments are scanned whole)
+  stride = (int)max((int64_t)1, min((int64_t)stride, task.rows / 512));
+  const int64_t nj = (task.rows + stride - 1) / stride;
   const int64_t r_begin = (int64_t)blockIdx.z * slice;
-  const int64_t r_end = min(task.rows, r_begin + slice);
+  const int64_t r_end = min(nj, r_begin + slice);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int64_t wd = k + m;
   const int64_t ca = c0 + 2 * lane, cb = ca + 1;
@@ -333,7 +341,7 @@ __global__ void __launch_bounds__(kSmThreads) segmax_kernel(const T* __restrict_
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const int64_t r = r0 + u * NW;
-      src[u] = r < r_end ? src_row[task.zrow + r] : -1;
+      src[u] = r < r_end ? src_row[task.zrow + r * stride] : -1;
       CVG_DCHECK(src[u] < nsrc && src[u] >= -1);
     }
     if (vbase) {
@@ -410,7 +418,16 @@ __global__ void __launch_bounds__(kQ1Threads, CVG_K1Q_MIN_BLOCKS)
                      const T* __restrict__ y, int64_t ldy, int64_t k, int64_t m, const int64_t* __restrict__ src_row,
                      int64_t zrows, int64_t kp, int64_t c_begin, int64_t c_end, int64_t nsrc,
                      const double* __restrict__ shift, const int* __restrict__ blkseg,
-                     const unsigned long long* __restrict__ segmax, int* __restrict__ nonfinite) {
+                     const unsigned long long* __restrict__ segmax, int headroom, int* __restrict__ ovf,
+                     int* __restrict__ nonfinite) {
+  // Out of range: tt outside [2^52, 2^53) (a non-finite z, or w below the digits' range) or V >= 2^(7S)
+  // (w above it).  With sampled exponents (ovf != null) that marks the block's segment for the exact
+  // pass; otherwise (exact exponents, where only a non-finite z can get there) it is the
+  // non-finite-input flag (DatasetPair's allFinite, core.hpp:43-44).
+  constexpr uint32_t kHiMask = 7 * S >= 52 ? 0xfff00000u
+                               : 7 * S >= 32 ? (0xfff00000u | (0x000fffffu & ~((1u << (7 * S - 32)) - 1u)))
+                                             : 0xffffffffu;
+  constexpr uint32_t kLoMask = 7 * S >= 32 ? 0u : ~((1u << (7 * S)) - 1u);
   extern __shared__ uint8_t k1q_raw[];
   uint8_t* tiles = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(k1q_raw) + 1023) & ~uintptr_t(1023));
   __shared__ int64_t s_src[2][QK];  // this block's and the next block's source rows
@@ -423,7 +440,7 @@ __global__ void __launch_bounds__(kQ1Threads, CVG_K1Q_MIN_BLOCKS)
   const int64_t nblk = zrows / QK;
   const int64_t grid = gridDim.x;
   const double C = 0x1p52 + (double)DigitOffset<S>::v;
-  uint32_t badhi = 0;  // OR of (tt's sign/exponent ^ 2^52's): nonzero iff some z was not finite
+  uint32_t oor = 0;  // out-of-range bits of this block's values
   auto load_src = [&](int64_t b, int sb) {
     if (threadIdx.x < QK && b < nblk) {
       const int64_t src = src_row[b * QK + threadIdx.x];
@@ -453,12 +470,16 @@ __global__ void __launch_bounds__(kQ1Threads, CVG_K1Q_MIN_BLOCKS)
   if (blk < nblk) load_vals(0, c_begin);
   int buf = 0, sb = 0;
   for (; blk < nblk; blk += grid, sb ^= 1) {
-    const unsigned long long* smx = segmax + (int64_t)blkseg[blk] * kp;
+    const int seg = blkseg[blk];
+    const unsigned long long* smx = segmax + (int64_t)seg * kp;
     for (int64_t ch = 0; ch < nchunk; ++ch, buf ^= 1) {
       const int64_t c0 = c_begin + 64 * ch;
       const int64_t c = c0 + col;
       const double sh = c < wd ? shift[c] : 0.0;
-      const double sc = pow2(seg_exponent(__longlong_as_double((long long)smx[c])) + 7 * (S - 1));
+      const unsigned long long mxb = smx[c];
+      const double sc = pow2(seg_exponent(__longlong_as_double((long long)mxb), headroom) + 7 * (S - 1));
+      // a sampled max of 0 cannot scale the column: any nonzero value sends the segment to the exact pass
+      const bool zero_col = ovf && mxb == 0ull;
       uint32_t lo[16], hi[16];
 #pragma unroll
       for (int p = 0; p < 4; ++p)
@@ -466,10 +487,12 @@ __global__ void __launch_bounds__(kQ1Threads, CVG_K1Q_MIN_BLOCKS)
         for (int i = 0; i < 4; ++i) {
           const int e = 4 * p + i;
           const bool real = s_src[sb][4 * (qq + 4 * p) + i] >= 0 && c < wd;
-          const double tt = fma(real ? __dsub_rn(v[e], sh) : v[e], sc, C);
+          const double z = real ? __dsub_rn(v[e], sh) : v[e];
+          const double tt = fma(z, sc, C);
           lo[e] = (uint32_t)__double2loint(tt);
           hi[e] = (uint32_t)__double2hiint(tt);
-          badhi |= (hi[e] & 0xfff00000u) ^ 0x43300000u;
+          oor |= ((hi[e] ^ 0x43300000u) & kHiMask) | (lo[e] & kLoMask);
+          if (zero_col) oor |= z != 0.0;
         }
       // next chunk's loads in flight while this one is cut and stored
       if (ch + 1 < nchunk)
@@ -506,6 +529,8 @@ __global__ void __launch_bounds__(kQ1Threads, CVG_K1Q_MIN_BLOCKS)
         asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
       }
     }
+    if (__any_sync(0xffffffffu, oor != 0u) && lane == 0) atomicOr(ovf ? ovf + seg : nonfinite, 1);
+    oor = 0;
     // s_src[sb] is free (the next block's prefetch used sb ^ 1): fill it for block + 2 grid; the
     // second barrier publishes it before a one-chunk block's prefetch reads it
     __syncthreads();
@@ -513,7 +538,6 @@ __global__ void __launch_bounds__(kQ1Threads, CVG_K1Q_MIN_BLOCKS)
     __syncthreads();
   }
   if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
-  if (__any_sync(0xffffffffu, badhi != 0) && lane == 0) atomicOr(nonfinite, 1);
 }
 
 // 4-D map over Zq: {64 rows, kp, zrows / 64, S} bytes, box {64, box_cols, 1, S}, SWIZZLE_64B.
@@ -531,22 +555,24 @@ inline bool make_zq_map(CUtensorMap* map, const int8_t* zq, int64_t zrows, int64
 }
 
 template <int S, int KS>
-bool launch_gram_i8_s(const int8_t* zq, const unsigned long long* segmax, int64_t zrows, int64_t kp, const GramTask* segs,
-                      int64_t nseg, const int2* tiles, int ntiles, double* part, cudaStream_t s) {
+bool launch_gram_i8_s(const int8_t* zq, const unsigned long long* segmax, int headroom, int64_t zrows, int64_t kp,
+                      const GramTask* segs, int64_t nseg, const int2* tiles, int ntiles, double* part, cudaStream_t s) {
   CUtensorMap ma, mb;
   if (!make_zq_map(&ma, zq, zrows, kp, S, QA, KS) || !make_zq_map(&mb, zq, zrows, kp, S, QB, KS)) return false;
   using C = QCfg<S, KS>;
   cudaFuncSetAttribute(gram_i8_kernel<S, KS>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
   const int64_t blocks = nseg * (int64_t)ntiles;
   if (blocks > 0)
-    gram_i8_kernel<S, KS><<<(unsigned)blocks, kQThreads, C::kSmem, s>>>(ma, mb, segmax, segs, tiles, ntiles, kp, part);
+    gram_i8_kernel<S, KS><<<(unsigned)blocks, kQThreads, C::kSmem, s>>>(ma, mb, segmax, segs, tiles, ntiles, kp, part,
+                                                                                 headroom);
   return true;
 }
 
 template <typename T, int S>
 bool launch_k1q(const void* x, int64_t ldx, const void* y, int64_t ldy, int64_t k, int64_t m, const int64_t* src_row,
                 int64_t zrows, int64_t kp, int64_t c_begin, int64_t c_end, int64_t nsrc, const double* shift,
-                const int* blkseg, const unsigned long long* segmax, int8_t* zq, int* nonfinite, cudaStream_t s) {
+                const int* blkseg, const unsigned long long* segmax, int headroom, int* ovf, int8_t* zq, int* nonfinite,
+                cudaStream_t s) {
   CUtensorMap mo;
   if (!make_zq_map(&mo, zq, zrows, kp, S, 64)) return false;
   constexpr int smem = k1q_smem_bytes<S>();
@@ -562,7 +588,7 @@ bool launch_k1q(const void* x, int64_t ldx, const void* y, int64_t ldy, int64_t 
   const int64_t blocks = std::min<int64_t>(zrows / QK, (int64_t)per_sm * sms);
   reorder_q_kernel<T, S><<<(unsigned)blocks, kQ1Threads, smem, s>>>(mo, (const T*)x, ldx, (const T*)y, ldy, k, m,
                                                                     src_row, zrows, kp, c_begin, c_end, nsrc, shift,
-                                                                    blkseg, segmax, nonfinite);
+                                                                    blkseg, segmax, headroom, ovf, nonfinite);
   return true;
 }
 
@@ -570,9 +596,12 @@ bool launch_k1q(const void* x, int64_t ldx, const void* y, int64_t ldy, int64_t 
 
 void launch_segmax(int dtype, const void* x, int64_t ldx, const void* y, int64_t ldy, int64_t k, int64_t m,
                    const int64_t* src_row, const GramTask* segs, int64_t nseg, int64_t max_seg_rows, int64_t kp,
-                   int64_t c_begin, int64_t c_end, int64_t nsrc, const double* shift, unsigned long long* segmax,
-                   cudaStream_t s) {
+                   int64_t c_begin, int64_t c_end, int64_t nsrc, const double* shift, int stride, const int* only,
+                   unsigned long long* segmax, cudaStream_t s) {
   if (nseg <= 0 || c_end <= c_begin) return;
+  // bound on any segment's sampled rows: segments below 1024 rows are scanned whole (stride 1), longer ones
+  // keep >= 512 rows at a stride of at most `stride`
+  max_seg_rows = std::max<int64_t>(std::min<int64_t>(max_seg_rows, 1024), (max_seg_rows + stride - 1) / stride) + 1;
   // row slices: ~4096+ CTAs in all, 128 .. 1024 rows each
   const int64_t nchunk = (c_end - c_begin) / 64;
   int64_t slice = 1024;
@@ -580,19 +609,19 @@ void launch_segmax(int dtype, const void* x, int64_t ldx, const void* y, int64_t
   const dim3 grid((unsigned)nseg, (unsigned)nchunk, (unsigned)((max_seg_rows + slice - 1) / slice));
   if (dtype == 0)
     segmax_kernel<double><<<grid, kSmThreads, 0, s>>>((const double*)x, ldx, (const double*)y, ldy, k, m, src_row,
-                                                      segs, kp, c_begin, nsrc, shift, slice, segmax);
+                                                      segs, kp, c_begin, nsrc, shift, slice, stride, only, segmax);
   else
     segmax_kernel<float><<<grid, kSmThreads, 0, s>>>((const float*)x, ldx, (const float*)y, ldy, k, m, src_row, segs,
-                                                     kp, c_begin, nsrc, shift, slice, segmax);
+                                                     kp, c_begin, nsrc, shift, slice, stride, only, segmax);
 }
 
 bool launch_reorder_q(int dtype, int slices, const void* x, int64_t ldx, const void* y, int64_t ldy, int64_t k,
                       int64_t m, const int64_t* src_row, int64_t zrows, int64_t kp, int64_t c_begin, int64_t c_end,
-                      int64_t nsrc, const double* shift, const int* blkseg, const unsigned long long* segmax, int8_t* zq,
-                      int* nonfinite, cudaStream_t s) {
+                      int64_t nsrc, const double* shift, const int* blkseg, const unsigned long long* segmax,
+                      int headroom, int* ovf, int8_t* zq, int* nonfinite, cudaStream_t s) {
   if (zrows <= 0 || c_end <= c_begin) return true;
 #define CVG_K1Q(T, S) \
-  return launch_k1q<T, S>(x, ldx, y, ldy, k, m, src_row, zrows, kp, c_begin, c_end, nsrc, shift, blkseg, segmax, zq, nonfinite, s)
+  return launch_k1q<T, S>(x, ldx, y, ldy, k, m, src_row, zrows, kp, c_begin, c_end, nsrc, shift, blkseg, segmax, headroom, ovf, zq, nonfinite, s)
   if (dtype == 0) {
     if (slices == 6) CVG_K1Q(double, 6);
     else CVG_K1Q(double, 7);
@@ -613,11 +642,12 @@ static int i8_stage_rows() {
   return v;
 }
 
-bool launch_gram_i8(int slices, const int8_t* zq, const unsigned long long* segmax, int64_t zrows, int64_t kp,
-                    const GramTask* segs, int64_t nseg, const int2* tiles, int ntiles, double* part, cudaStream_t s) {
+bool launch_gram_i8(int slices, const int8_t* zq, const unsigned long long* segmax, int headroom, int64_t zrows,
+                    int64_t kp, const GramTask* segs, int64_t nseg, const int2* tiles, int ntiles, double* part,
+                    cudaStream_t s) {
 #define CVG_GRAM_I8(S)                                                                                       \
-  return i8_stage_rows() == 64 ? launch_gram_i8_s<S, 64>(zq, segmax, zrows, kp, segs, nseg, tiles, ntiles, part, s) \
-                               : launch_gram_i8_s<S, 32>(zq, segmax, zrows, kp, segs, nseg, tiles, ntiles, part, s)
+  return i8_stage_rows() == 64 ? launch_gram_i8_s<S, 64>(zq, segmax, headroom, zrows, kp, segs, nseg, tiles, ntiles, part, s) \
+                               : launch_gram_i8_s<S, 32>(zq, segmax, headroom, zrows, kp, segs, nseg, tiles, ntiles, part, s)
   switch (slices) {
     case 3: CVG_GRAM_I8(3);
     case 4: CVG_GRAM_I8(4);
