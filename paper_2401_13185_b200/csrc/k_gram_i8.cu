@@ -390,7 +390,13 @@ __global__ void __launch_bounds__(kSmThreads) segmax_kernel(const T* __restrict_
 // sum_t d_t 2^-7t = round(w 2^7(S-1)) 2^-7(S-1) exactly (w = z 2^e, |w| < 63, while the
 // digits reach 64 - 64/127).  Four rows' 7-bit fields are packed into one word by byte
 // permutes and shifted by -64 byte-wise (SWAR, no borrows).
-constexpr int kQ1Threads = 256;
+// PQ row quads per thread: 4 (256 threads, 16 rows per thread) or 2 (512 threads, 8 rows: twice the warps
+// to interleave loads with the cut).
+#ifndef CVG_K1Q_PQ
+#define CVG_K1Q_PQ 4
+#endif
+constexpr int kQ1PQ = CVG_K1Q_PQ;
+constexpr int kQ1Threads = 256 * 4 / kQ1PQ;
 #ifndef CVG_K1Q_MIN_BLOCKS
 #define CVG_K1Q_MIN_BLOCKS 2
 #endif
@@ -433,7 +439,9 @@ __global__ void __launch_bounds__(kQ1Threads, CVG_K1Q_MIN_BLOCKS)
   __shared__ int64_t s_src[2][QK];  // this block's and the next block's source rows
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int j = lane >> 2, qq = lane & 3;
-  const int col = 8 * w + j;  // column within the 64-column chunk
+  const int col = 8 * (w & 7) + j;  // column within the 64-column chunk
+  const int p0 = (w >> 3) * kQ1PQ;  // this thread's row quads: qq + 4p, p = p0 .. p0 + PQ - 1
+  constexpr int NV = 4 * kQ1PQ;
   const int64_t wd = k + m;
   CVG_DCHECK(c_begin >= 0 && c_end <= kp && c_begin % 64 == 0 && zrows % QK == 0);
   const int64_t nchunk = (c_end - c_begin) / 64;
@@ -448,19 +456,19 @@ __global__ void __launch_bounds__(kQ1Threads, CVG_K1Q_MIN_BLOCKS)
       s_src[sb][threadIdx.x] = src;
     }
   };
-  // this thread's 16 values of column c0 + col in block b (raw: the shift is applied at the cut)
-  double v[16];
+  // this thread's NV values of column c0 + col in block b (raw: the shift is applied at the cut)
+  double v[NV];
   auto load_vals = [&](int sb, int64_t c0) {
     const int64_t c = c0 + col;
     const int kind = c < k ? 0 : c < wd ? 1 : c == wd ? 2 : 3;  // x, y, ones, padding
     const T* base = kind == 0 ? x + c : y + (c - k);
     const int64_t ld = kind == 0 ? ldx : ldy;
 #pragma unroll
-    for (int p = 0; p < 4; ++p)
+    for (int pp = 0; pp < kQ1PQ; ++pp)
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
-        const int64_t src = s_src[sb][4 * (qq + 4 * p) + i];
-        v[4 * p + i] = src < 0 ? 0.0 : kind <= 1 ? (double)__ldg(base + src * ld) : kind == 2 ? 1.0 : 0.0;
+        const int64_t src = s_src[sb][4 * (qq + 4 * (p0 + pp)) + i];
+        v[4 * pp + i] = src < 0 ? 0.0 : kind <= 1 ? (double)__ldg(base + src * ld) : kind == 2 ? 1.0 : 0.0;
       }
   };
   int64_t blk = blockIdx.x;
@@ -480,13 +488,13 @@ __global__ void __launch_bounds__(kQ1Threads, CVG_K1Q_MIN_BLOCKS)
       const double sc = pow2(seg_exponent(__longlong_as_double((long long)mxb), headroom) + 7 * (S - 1));
       // a sampled max of 0 cannot scale the column: any nonzero value sends the segment to the exact pass
       const bool zero_col = ovf && mxb == 0ull;
-      uint32_t lo[16], hi[16];
+      uint32_t lo[NV], hi[NV];
 #pragma unroll
-      for (int p = 0; p < 4; ++p)
+      for (int pp = 0; pp < kQ1PQ; ++pp)
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-          const int e = 4 * p + i;
-          const bool real = s_src[sb][4 * (qq + 4 * p) + i] >= 0 && c < wd;
+          const int e = 4 * pp + i;
+          const bool real = s_src[sb][4 * (qq + 4 * (p0 + pp)) + i] >= 0 && c < wd;
           const double z = real ? __dsub_rn(v[e], sh) : v[e];
           const double tt = fma(z, sc, C);
           lo[e] = (uint32_t)__double2loint(tt);
@@ -507,11 +515,12 @@ __global__ void __launch_bounds__(kQ1Threads, CVG_K1Q_MIN_BLOCKS)
       for (int d = 0; d < S; ++d) {
         const int pos = 7 * (S - 1 - d);
 #pragma unroll
-        for (int p = 0; p < 4; ++p) {
+        for (int pp = 0; pp < kQ1PQ; ++pp) {
+          const int p = p0 + pp;
           uint32_t b[4];
 #pragma unroll
           for (int i = 0; i < 4; ++i) {  // low word of V >> pos (funnel shifts take the shift mod 32)
-            const int e = 4 * p + i;
+            const int e = 4 * pp + i;
             b[i] = pos >= 32 ? hi[e] >> (pos - 32) : __funnelshift_r(lo[e], hi[e], pos);
           }
           uint32_t word = __byte_perm(__byte_perm(b[0], b[1], 0x0040), __byte_perm(b[2], b[3], 0x0040), 0x5410);
