@@ -445,8 +445,9 @@ def run_ours(args):
     tile = 128 if f32 else 64
     z_elem = 4 if (f32 and not tf32_kind) else 8  # Z: fp64 | fp16 hi + lo | tf32 hi + lo
     reorder_bytes = n * (k + m) * x_elt + n * (-(-(k + m + 1) // tile) * tile) * z_elem
-    if i8_kind:  # segment max (one read of x | y) + K1Q (read x | y, write S int8 digit slices)
-        reorder_bytes = 2 * n * (k + m) * x_elt + n * (-(-(k + m + 1) // tile) * tile) * i8_slices(f32)
+    if i8_kind:  # segment maxima over a 1/CVG_I8_SAMPLE row sample + K1Q (read x | y, write S int8 digit slices)
+        sample = max(1, int(os.environ.get("CVG_I8_SAMPLE", "16") or 16))
+        reorder_bytes = int(n * (k + m) * x_elt * (1 + 1 / sample)) + n * (-(-(k + m + 1) // tile) * tile) * i8_slices(f32)
     epi_bytes = len(masks) * (2 * p * k * (k + m) * 8) + k * (k + m) * 8
     line = {
         "metric": "all_fold_cv_gram_gflops", "value": round(value, 3), "unit": "GFLOP/s", "n_gpus": world,
