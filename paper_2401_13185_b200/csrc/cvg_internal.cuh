@@ -37,9 +37,9 @@ constexpr int64_t kChunkRowsF32 = 32768;
 // 3xTF32 operands (CVG_FP32_KIND=tf32, 8 B per element): 32768 -> 44.9 ms, 16384 -> 44.5, 12288 -> 42.9,
 // 8192 -> 44.2 on c3 (shorter segments re-read less from DRAM; the tree over more partials eats the rest).
 constexpr int64_t kChunkRowsTf32 = 12288;
-// int8-slice fp64 Gram (CVG_FP64_KIND=i8): exact int32 TMEM sums need S * 4096 * rows < 2^31
-// (rows < 74,898 at S = 7); the exponent is per (segment, column).
-constexpr int64_t kChunkRowsI8 = 32768;
+// int8-slice fp64 Gram (default fp64 kind): exact int32 TMEM sums need S * 2^14 * rows < 2^31 for base-256
+// digits in [-128, 127] (rows < 21,845 at S = 6); the exponent is per (segment, column).
+constexpr int64_t kChunkRowsI8 = 16384;
 constexpr int kTileF32 = 128;             // tcgen05 tile edge (M = N = 128)
 constexpr int kTileRowsPerWarp = 1024; // rows per warp in the bucketing passes
 

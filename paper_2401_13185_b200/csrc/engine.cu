@@ -244,12 +244,12 @@ static bool fp64_i8_env() {
   const char* e = std::getenv("CVG_FP64_KIND");
   return !(e && std::string(e) == "dmma");
 }
-static int i8_slices_env() {
+static int i8_slices_env() {  // base-256 digits: 6 (48 bits, default) or 5 (40 bits)
   const char* e = std::getenv("CVG_I8_SLICES");
-  return e && std::atoi(e) == 6 ? 6 : 7;
+  return e && std::atoi(e) == 5 ? 5 : 6;
 }
-// fp32 inputs on the int8 digit path (CVG_FP32_KIND=i8): 4 digits (27 bits below each segment column's
-// max, fp32 carries 24) or, with CVG_I8_SLICES_F32=3, 3 digits (20 bits; ~1e-6, inside the 1e-4 gate).
+// fp32 inputs on the int8 digit path (CVG_FP32_KIND=i8): 4 base-256 digits (32 bits below each segment
+// column's max, fp32 carries 24) or, with CVG_I8_SLICES_F32=3, 3 digits (24 bits).
 // Row-sample stride of the int8 path's segment maxima (CVG_I8_SAMPLE; 1 = every row, one exact pass).
 static int i8_sample_env() {
   const char* e = std::getenv("CVG_I8_SAMPLE");

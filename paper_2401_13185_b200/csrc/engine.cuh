@@ -178,7 +178,7 @@ class Plan {
   int sample_ = 16;             // int8 path: segment maxima over every sample_-th row (CVG_I8_SAMPLE; 1 = exact)
   int64_t exact_segments_ = 0;  // segments the last gram redid from their exact max
   std::vector<int> ovf_host_;
-  int slices_ = 7;              // int8 digits per value (fp64: CVG_I8_SLICES = 6 | 7; fp32: CVG_I8_SLICES_F32 = 3 | 4)
+  int slices_ = 6;              // base-256 int8 digits per value (fp64: CVG_I8_SLICES = 5 | 6; fp32: CVG_I8_SLICES_F32 = 3 | 4)
   DevBuf pairs128_d_;
   std::vector<int64_t> counts_;  // per fold (all p) validation sizes
   std::vector<GramTask> segs_;

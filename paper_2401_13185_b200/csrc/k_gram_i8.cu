@@ -143,17 +143,17 @@ __device__ __forceinline__ double pow2(int e) {  // 2^e for e in [-1022, 1023]
   return __hiloint2double((1023 + e) << 20, 0);
 }
 
-// The segment exponent of a column whose max |z| is mx: max |z| 2^e in [31.5, 63), so every
-// value is representable by the offset digits (|w| < 63 < 64 - 64/127); with `headroom` (mx is
-// the max over a row sample) in [15.75, 31.5), so values up to 2x the sampled max still fit
+// The segment exponent of a column whose max |z| is mx: max |z| 2^e in [63.5, 127), so every
+// value is representable by the offset digits (|w| < 127 < 128 - 128/255); with `headroom` (mx is
+// the max over a row sample) in [31.75, 63.5), so values up to 2x the sampled max still fit
 // (larger ones are caught by K1Q and the segment is redone from its exact max).  e = 0 for an
 // all-zero (or non-finite) column.  e <= 1000 keeps 2^(e + 7(S-1)) a normal double (columns
 // below 2^-994 lose digits; their Gram entries are below 2^-1988 and round to zero in fp64 anyway).
 __device__ __forceinline__ int seg_exponent(double mx, int headroom) {
   if (!(mx > 0.0) || !isfinite(mx)) return 0;
   const int be = (int)((__double_as_longlong(mx) >> 52) & 0x7ff);  // 0 for subnormal maxima
-  int e = (headroom ? 4 : 5) - (be - 1023);
-  if (e <= 1000 && mx * pow2(e) >= (headroom ? 31.5 : 63.0)) --e;
+  int e = (headroom ? 5 : 6) - (be - 1023);
+  if (e <= 1000 && mx * pow2(e) >= (headroom ? 63.5 : 127.0)) --e;
   return min(e, 1000);
 }
 
@@ -264,7 +264,7 @@ __global__ void __launch_bounds__(kQThreads, 1)
         uint32_t r[16];
         tmem_ld16(tmem_d + ((uint32_t)(32 * q) << 16) + (uint32_t)(d * QB + 32 * h + c0), r);
 #pragma unroll
-        for (int j = 0; j < 16; ++j) f[j] = fma(f[j], 0x1p-7, i2d_exact(r[j]));  // f * 2^-7 exact
+        for (int j = 0; j < 16; ++j) f[j] = fma(f[j], 0x1p-8, i2d_exact(r[j]));  // f * 2^-8 exact
       }
       if (write) {
 #pragma unroll
@@ -402,8 +402,8 @@ constexpr int kQ1Threads = 256 * 4 / kQ1PQ;
 #endif
 
 template <int S>
-struct DigitOffset {  // 64 * (128^S - 1) / 127
-  static constexpr int64_t v = 64 * (((int64_t)1 << (7 * S)) - 1) / 127;
+struct DigitOffset {  // 128 * (256^S - 1) / 255: 0x80 in every byte of V
+  static constexpr int64_t v = 128 * (((int64_t)1 << (8 * S)) - 1) / 255;
 };
 
 template <int S>
@@ -430,10 +430,9 @@ __global__ void __launch_bounds__(kQ1Threads, CVG_K1Q_MIN_BLOCKS)
   // (w above it).  With sampled exponents (ovf != null) that marks the block's segment for the exact
   // pass; otherwise (exact exponents, where only a non-finite z can get there) it is the
   // non-finite-input flag (DatasetPair's allFinite, core.hpp:43-44).
-  constexpr uint32_t kHiMask = 7 * S >= 52 ? 0xfff00000u
-                               : 7 * S >= 32 ? (0xfff00000u | (0x000fffffu & ~((1u << (7 * S - 32)) - 1u)))
-                                             : 0xffffffffu;
-  constexpr uint32_t kLoMask = 7 * S >= 32 ? 0u : ~((1u << (7 * S)) - 1u);
+  static_assert(8 * S <= 48, "digits must fit the 52-bit window");
+  constexpr uint32_t kHiMask = 8 * S >= 32 ? (0xfff00000u | (0x000fffffu & ~((1u << (8 * S - 32)) - 1u))) : 0xffffffffu;
+  constexpr uint32_t kLoMask = 8 * S >= 32 ? 0u : ~((1u << (8 * S)) - 1u);
   extern __shared__ uint8_t k1q_raw[];
   uint8_t* tiles = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(k1q_raw) + 1023) & ~uintptr_t(1023));
   __shared__ int64_t s_src[2][QK];  // this block's and the next block's source rows
@@ -485,7 +484,7 @@ __global__ void __launch_bounds__(kQ1Threads, CVG_K1Q_MIN_BLOCKS)
       const int64_t c = c0 + col;
       const double sh = c < wd ? shift[c] : 0.0;
       const unsigned long long mxb = smx[c];
-      const double sc = pow2(seg_exponent(__longlong_as_double((long long)mxb), headroom) + 7 * (S - 1));
+      const double sc = pow2(seg_exponent(__longlong_as_double((long long)mxb), headroom) + 8 * (S - 1));
       // a sampled max of 0 cannot scale the column: any nonzero value sends the segment to the exact pass
       const bool zero_col = ovf && mxb == 0ull;
       uint32_t lo[NV], hi[NV];
@@ -512,24 +511,30 @@ __global__ void __launch_bounds__(kQ1Threads, CVG_K1Q_MIN_BLOCKS)
       __syncthreads();
       uint8_t* tile = tiles + buf * (S * 4096);
 #pragma unroll
-      for (int d = 0; d < S; ++d) {
-        const int pos = 7 * (S - 1 - d);
-#pragma unroll
-        for (int pp = 0; pp < kQ1PQ; ++pp) {
-          const int p = p0 + pp;
-          uint32_t b[4];
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {  // low word of V >> pos (funnel shifts take the shift mod 32)
-            const int e = 4 * pp + i;
-            b[i] = pos >= 32 ? hi[e] >> (pos - 32) : __funnelshift_r(lo[e], hi[e], pos);
-          }
-          uint32_t word = __byte_perm(__byte_perm(b[0], b[1], 0x0040), __byte_perm(b[2], b[3], 0x0040), 0x5410);
-          word &= 0x7f7f7f7fu;
-          word = ((word | 0x80808080u) - 0x40404040u) ^ 0x80808080u;  // each byte - 64, no borrows
-          // quad q = qq + 4p of column col, SWIZZLE_64B: 16-byte chunk (q >> 2) ^ ((col >> 1) & 3)
-          const int off = col * 64 + ((p ^ ((col >> 1) & 3)) << 4) + (qq << 2);
-          *reinterpret_cast<uint32_t*>(tile + d * 4096 + off) = word;
+      for (int pp = 0; pp < kQ1PQ; ++pp) {
+        const int p = p0 + pp;
+        // quad q = qq + 4p of column col, SWIZZLE_64B: 16-byte chunk (q >> 2) ^ ((col >> 1) & 3)
+        const int off = col * 64 + ((p ^ ((col >> 1) & 3)) << 4) + (qq << 2);
+        // 4 x 4 byte transposes: word b = byte b of the 4 rows' V (low word: bytes 0-3, high word: 4-5)
+        const uint32_t* L = lo + 4 * pp;
+        const uint32_t* H = hi + 4 * pp;
+        uint32_t wb[8];
+        {
+          const uint32_t x0 = __byte_perm(L[0], L[1], 0x5140), x1 = __byte_perm(L[0], L[1], 0x7362);
+          const uint32_t y0 = __byte_perm(L[2], L[3], 0x5140), y1 = __byte_perm(L[2], L[3], 0x7362);
+          wb[0] = __byte_perm(x0, y0, 0x5410);
+          wb[1] = __byte_perm(x0, y0, 0x7632);
+          wb[2] = __byte_perm(x1, y1, 0x5410);
+          wb[3] = __byte_perm(x1, y1, 0x7632);
         }
+        if constexpr (S > 4) {
+          const uint32_t x0 = __byte_perm(H[0], H[1], 0x5140), y0 = __byte_perm(H[2], H[3], 0x5140);
+          wb[4] = __byte_perm(x0, y0, 0x5410);
+          wb[5] = __byte_perm(x0, y0, 0x7632);
+        }
+#pragma unroll
+        for (int d = 0; d < S; ++d)  // digit d = byte S-1-d; offset binary -> two's complement: ^ 0x80
+          *reinterpret_cast<uint32_t*>(tile + d * 4096 + off) = wb[S - 1 - d] ^ 0x80808080u;
       }
       asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
       __syncthreads();
@@ -632,8 +637,8 @@ bool launch_reorder_q(int dtype, int slices, const void* x, int64_t ldx, const v
 #define CVG_K1Q(T, S) \
   return launch_k1q<T, S>(x, ldx, y, ldy, k, m, src_row, zrows, kp, c_begin, c_end, nsrc, shift, blkseg, segmax, headroom, ovf, zq, nonfinite, s)
   if (dtype == 0) {
-    if (slices == 6) CVG_K1Q(double, 6);
-    else CVG_K1Q(double, 7);
+    if (slices == 5) CVG_K1Q(double, 5);
+    else CVG_K1Q(double, 6);
   } else {
     if (slices == 3) CVG_K1Q(float, 3);
     else CVG_K1Q(float, 4);
@@ -660,8 +665,8 @@ bool launch_gram_i8(int slices, const int8_t* zq, const unsigned long long* segm
   switch (slices) {
     case 3: CVG_GRAM_I8(3);
     case 4: CVG_GRAM_I8(4);
-    case 6: CVG_GRAM_I8(6);
-    default: CVG_GRAM_I8(7);
+    case 5: CVG_GRAM_I8(5);
+    default: CVG_GRAM_I8(6);
   }
 #undef CVG_GRAM_I8
 }

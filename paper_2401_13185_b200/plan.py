@@ -373,7 +373,7 @@ def fp64_kind() -> str:
 def i8_slices(f32: bool = False) -> int:
     if f32:
         return 3 if os.environ.get("CVG_I8_SLICES_F32") == "3" else 4
-    return 6 if os.environ.get("CVG_I8_SLICES") == "6" else 7
+    return 5 if os.environ.get("CVG_I8_SLICES") == "5" else 6
 
 
 def fp32_kind() -> str:
