@@ -2,22 +2,21 @@
 //
 // sm_100 has no fp64 tcgen05 kind; the DMMA path (k_gram_f64.cu) tops out at the
 // FP64 tensor rate (~37 TFLOP/s).  The int8 tensor rate is ~4.5 POPS, so each
-// shifted fp64 value is cut into S signed 7-bit digits and the Gram is formed from
-// exact integer products:
+// shifted fp64 value is cut into S signed base-256 digits and the Gram is formed
+// from exact integer products:
 //
-//   per (segment, column) exponent e:  w = z * 2^e  with  max |w| in [32, 64)
-//   w ~= d_0 + d_1 2^-7 + ... + d_{S-1} 2^-7(S-1),   |d_t| <= 64  (int8)
-//   sum_rows w_a w_b ~= sum_{t+u <= S-1} 2^-7(t+u) sum_rows d_t[a] d_u[b]
+//   per (segment, column) exponent e:  w = z * 2^e  with  |w| < 127
+//   w ~= d_0 + d_1 2^-8 + ... + d_{S-1} 2^-8(S-1),   d_t in [-128, 127]  (int8)
+//   sum_rows w_a w_b ~= sum_{t+u <= S-1} 2^-8(t+u) sum_rows d_t[a] d_u[b]
 //
-// Every digit is exact (d_t = round-to-nearest of the exact residual, which is
-// formed without error in fp64), every int8 x int8 product and its int32 TMEM sum
-// is exact (|sum| <= S * 4096 * rows < 2^31 for rows <= kChunkRowsI8), and the
-// drain turns the S diagonal accumulators into fp64 with one rounding per step of a
-// fixed Horner chain.  The only approximation is the digit cut: each w keeps
-// 7(S-1) + 6 bits below its column's segment maximum (relative error <= 2^-7(S-1)-1
-// of that maximum), and the dropped products t + u >= S weigh <= S 2^-7S of
-// max|w_a| max|w_b|.  S = 7 keeps the error at the level of fp64 accumulation
-// itself (~1e-15 relative to the column norms).
+// The digits are exact (the bytes of V = round(w 2^8(S-1)) + offset), every int8 x
+// int8 product and its int32 TMEM sum is exact (|sum| <= S * 2^14 * rows < 2^31 for
+// rows <= kChunkRowsI8), and the drain turns the S diagonal accumulators into fp64
+// with one rounding per step of a fixed Horner chain.  The only approximation is the
+// digit cut: each w keeps 8(S-1) + 6..7 bits below its column's segment maximum, and
+// the dropped products t + u >= S weigh <= S 2^-8S of max|w_a| max|w_b|.  S = 6 (48
+// bits, 21 slice pairs) keeps the error at the level of fp64 accumulation itself
+// (~1e-14 relative to the column norms).
 //
 // The exponent is a function of the segment's rows only (segmax_kernel), so a
 // segment's partial -- and every sum built from the partials -- is bit-identical
@@ -30,7 +29,8 @@
 // K2q roles (10 warps, 1 CTA per SM, one (segment, 128 x 64 output tile) per CTA):
 //   warp 0      TMA producer: A (128 Gram rows) and B (64 Gram columns) slices
 //   warp 1      TMEM owner + MMA issuer: S(S+1)/2 slice pairs x 2 K-steps per stage,
-//               pair (t, u) into accumulator t + u (S x 64 int32 TMEM columns)
+//               pair (t, u) into accumulator t + u (S x 64 int32 TMEM columns); the pairs of
+//               one A slice with adjacent B slices are one MMA of N = 64 .. 256
 //   warps 2..9  drain once per tile: Horner over the S accumulators, exact unscale
 #include <cstdlib>
 
@@ -107,11 +107,20 @@ __device__ __forceinline__ void mma_runs(uint32_t tmem_d, uint64_t a, uint64_t b
     mma_runs<S, T, U0 + NS>(tmem_d, a, b0, b_step, first);
   }
 }
+// Accumulators: S diagonals t + u <= S-1, plus (S even) the square pair (S/2, S/2) of diagonal S: the
+// dropped pairs t + u >= S are zero-mean products of independent digits except these squares, so
+// keeping the first one removes the truncation's bias on the Gram diagonal (the next, diagonal S+2,
+// weighs 2^-16 less).
+template <int S>
+constexpr int kNAcc = S + (S % 2 == 0 ? 1 : 0);
+
 template <int S, int T>
 __device__ __forceinline__ void mma_slices(uint32_t tmem_d, uint64_t a0, uint64_t a_step, uint64_t b0, uint64_t b_step,
                                            bool first) {
   if constexpr (T < S) {
     mma_runs<S, T, 0>(tmem_d, a0 + T * a_step, b0, b_step, first);
+    if constexpr (S % 2 == 0 && T == S / 2)  // the square pair (S/2, S/2) into accumulator S
+      mma_i8<0, 1>(tmem_d + (uint32_t)(S * QB), a0 + T * a_step, b0 + T * b_step, first ? 0u : 1u);
     mma_slices<S, T + 1>(tmem_d, a0, a_step, b0, b_step, first);
   }
 }
@@ -255,12 +264,12 @@ __global__ void __launch_bounds__(kQThreads, 1)
       double f[16];
       {
         uint32_t r[16];
-        tmem_ld16(tmem_d + ((uint32_t)(32 * q) << 16) + (uint32_t)((S - 1) * QB + 32 * h + c0), r);
+        tmem_ld16(tmem_d + ((uint32_t)(32 * q) << 16) + (uint32_t)((kNAcc<S> - 1) * QB + 32 * h + c0), r);
 #pragma unroll
         for (int j = 0; j < 16; ++j) f[j] = i2d_exact(r[j]);
       }
 #pragma unroll
-      for (int d = S - 2; d >= 0; --d) {
+      for (int d = kNAcc<S> - 2; d >= 0; --d) {
         uint32_t r[16];
         tmem_ld16(tmem_d + ((uint32_t)(32 * q) << 16) + (uint32_t)(d * QB + 32 * h + c0), r);
 #pragma unroll
@@ -381,15 +390,15 @@ __global__ void __launch_bounds__(kSmThreads) segmax_kernel(const T* __restrict_
 // next item's loads and cuts overlap the store).  Warp w owns columns 8w .. 8w + 7; lane
 // (j, qq) = (lane >> 2, lane & 3) holds column 8w + j of the row quads qq, qq + 4, qq + 8,
 // qq + 12 (16 rows; a warp load reads 64 contiguous bytes of 4 rows).  Each thread packs
-// a quad's 4 digits into one word; with the SW64 XOR the 32 lanes' words land in 32
-// distinct banks.
+// a quad's 4 digits of one position into one word; with the SW64 XOR the 32 lanes' words
+// land in 32 distinct banks.
 //
-// Digits: one fma gives V = round(z 2^(e + 7(S-1))) + O in the low 52 bits of
-// tt = fma(z, 2^(e + 7(S-1)), 2^52 + O), O = 64 (1 + 128 + ... + 128^(S-1)), 0 <= V < 2^(7S);
-// digit t (t = 0 most significant) is ((V >> 7(S-1-t)) & 127) - 64 in [-64, 63], so
-// sum_t d_t 2^-7t = round(w 2^7(S-1)) 2^-7(S-1) exactly (w = z 2^e, |w| < 63, while the
-// digits reach 64 - 64/127).  Four rows' 7-bit fields are packed into one word by byte
-// permutes and shifted by -64 byte-wise (SWAR, no borrows).
+// Digits: one fma gives V = round(z 2^(e + 8(S-1))) + O in the low 52 bits of
+// tt = fma(z, 2^(e + 8(S-1)), 2^52 + O), O = 128 (1 + 256 + ... + 256^(S-1)) (0x80 in every byte),
+// 0 <= V < 2^(8S); digit t (t = 0 most significant) is byte S-1-t of V minus 128 -- as int8, the
+// byte XOR 0x80 -- so sum_t d_t 2^-8t = round(w 2^8(S-1)) 2^-8(S-1) exactly (|w| < 127, while the
+// digits reach 128 - 128/255).  Four rows' digits of one byte position are one word of a 4 x 4
+// byte transpose (8 byte permutes for bytes 0-3, 4 for bytes 4-5).
 // PQ row quads per thread: 4 (256 threads, 16 rows per thread) or 2 (512 threads, 8 rows: twice the warps
 // to interleave loads with the cut).
 #ifndef CVG_K1Q_PQ
