@@ -390,7 +390,7 @@ def run_ours(args):
     # executed DMMA flops: 64x64 tiles actually issued (symmetry + padding)
     from paper_2401_13185_b200.plan import executed_gram_flops
     from paper_2401_13185_b200.plan import fp64_kind as executed_fp64_kind
-    from paper_2401_13185_b200.plan import i8_slices
+    from paper_2401_13185_b200.plan import i8_pairs, i8_slices
 
     f32 = not x_dtype_is_f64(cid)
     executed = executed_gram_flops(n, k, m, p, f32) / max(world, 1) / (gram_ms * 1e-3) / 1e12
@@ -399,7 +399,7 @@ def run_ours(args):
     if f32_i8:
         s_ = i8_slices(True)
         gram_kernel = (f"gram_i8_kernel<{s_}> (fp32 inputs as exact int8 digit slices on tcgen05 kind::i8, "
-                       f"{s_ * (s_ + 1) // 2} slice-pair products; CVG_FP32_KIND=i8)")
+                       f"{i8_pairs(s_)} slice-pair products; CVG_FP32_KIND=i8)")
         peak = INT8_PEAK_TOPS
         peak_source = "NVIDIA nominal dense int8 (4.5 POPS); achieved = int8 tensor ops issued per second"
     elif f32 and tf32_kind:
@@ -415,12 +415,12 @@ def run_ours(args):
                        "runs fp16 and bf16 at one rate); executed counts the 3 fp16 products")
     elif executed_fp64_kind() == "i8":
         s_ = i8_slices()
-        gram_kernel = (f"gram_i8_kernel<{s_}> (tcgen05.mma kind::i8: exact int8 digit slices, {s_ * (s_ + 1) // 2} "
-                       f"slice-pair products into int32 TMEM, exact fp64 drain; CVG_FP64_KIND=i8)")
+        gram_kernel = (f"gram_i8_kernel<{s_}, 64> (tcgen05.mma kind::i8: exact base-256 int8 digit slices, "
+                       f"{i8_pairs(s_)} slice-pair products into int32 TMEM, exact fp64 drain)")
         peak = INT8_PEAK_TOPS
         peak_source = ("NVIDIA nominal dense int8 (4.5 POPS); measured cuBLASLt int8 reaches 3078 burst / 2423 "
                        "sustained here (profiles/r01_fp64_peaks.txt), below this kernel. achieved = int8 tensor "
-                       "ops issued per second (128x64 tiles x S(S+1)/2 slice pairs); the fp64-equivalent "
+                       "ops issued per second (128x64 tiles x slice pairs); the fp64-equivalent "
                        "algorithmic rate is the line's value")
     else:
         gram_kernel = "gram_f64_kernel (DMMA.8x8x4)"
@@ -469,8 +469,8 @@ def run_ours(args):
                      "executed_tflops": round(executed, 3),
                      "executed_frac": round(executed / peak, 4),
                      "note": "algorithmic flops = 2NK(K+M) (BASELINE metric). executed counts what the tensor "
-                             "cores issue: fp64 int8 kind: 128x64 tiles covering the upper 64x64 tiles x S(S+1)/2 "
-                             "int8 slice pairs (TOPS); fp64 DMMA kind: upper 64x64 tiles, diagonal tiles their upper "
+                             "cores issue: fp64 int8 kind: 128x64 tiles covering the upper 64x64 tiles x 22 int8 "
+                             "slice pairs (TOPS); fp64 DMMA kind: upper 64x64 tiles, diagonal tiles their upper "
                              "8x8 blocks; fp32: upper 128x128 tiles x 3 fp16 products"},
         "kernels_ms_per_step": per_kernel,
         "hbm_rooflines": {

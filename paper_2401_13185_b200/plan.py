@@ -376,6 +376,11 @@ def i8_slices(f32: bool = False) -> int:
     return 5 if os.environ.get("CVG_I8_SLICES") == "5" else 6
 
 
+def i8_pairs(s: int) -> int:
+    """Slice pairs the int8 Gram multiplies: t + u <= s-1, plus the square (s/2, s/2) for even s."""
+    return s * (s + 1) // 2 + (1 if s % 2 == 0 else 0)
+
+
 def fp32_kind() -> str:
     """The fp32 Gram kind: "f16" (scaled fp16 hi/lo on kind::f16, default), "tf32" or "i8" (CVG_FP32_KIND)."""
     v = os.environ.get("CVG_FP32_KIND")
@@ -389,9 +394,8 @@ def executed_gram_flops(n: int, k: int, m: int, p: int, f32: bool = False) -> fl
     if f32 and fp32_kind() != "i8":
         return 3 * 2.0 * len(gram_tiles(k, m, 128)) * 128 * 128 * n
     tiles = gram_tiles(k, m)
-    if f32 or fp64_kind() == "i8":  # int8 ops: 128x64 tiles x S(S+1)/2 slice pairs
-        s = i8_slices(f32)
+    if f32 or fp64_kind() == "i8":  # int8 ops: 128x64 tiles x slice pairs
         tq = {(i // 2, j) for i, j in tiles}
-        return 2.0 * len(tq) * 128 * 64 * n * (s * (s + 1) // 2)
+        return 2.0 * len(tq) * 128 * 64 * n * i8_pairs(i8_slices(f32))
     n_diag = sum(1 for i, j in tiles if i == j)
     return 2.0 * ((len(tiles) - n_diag) * 64 * 64 + n_diag * 36 * 64) * n
