@@ -97,14 +97,14 @@ __device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t a, uint64_t b, 
 // memory (one 64-column K-major tile each, SBO-uniform): so NS consecutive pairs are ONE
 // MMA with N = 64 NS (NS <= 4, N <= 256) -- 10 MMAs per K-step instead of 28 for S = 7.
 // A slice t stays in the collector across its run.
-template <int S, int T, int U0>
+template <int S, int T, int U0, int LEN = S - T>
 __device__ __forceinline__ void mma_runs(uint32_t tmem_d, uint64_t a, uint64_t b0, uint64_t b_step, bool first) {
-  if constexpr (U0 < S - T) {
-    constexpr int NS = (S - T - U0) < 4 ? (S - T - U0) : 4;
-    constexpr bool only = U0 == 0 && NS == S - T;  // the whole run is one MMA
-    constexpr int cu = !CVG_I8_COLLECTOR || only ? 0 : U0 == 0 ? 1 : U0 + NS == S - T ? 3 : 2;
+  if constexpr (U0 < LEN) {
+    constexpr int NS = (LEN - U0) < 4 ? (LEN - U0) : 4;
+    constexpr bool only = U0 == 0 && NS == LEN;  // the whole run is one MMA
+    constexpr int cu = !CVG_I8_COLLECTOR || only ? 0 : U0 == 0 ? 1 : U0 + NS == LEN ? 3 : 2;
     mma_i8<cu, NS>(tmem_d + (uint32_t)((T + U0) * QB), a, b0 + U0 * b_step, (first && T == 0) ? 0u : 1u);
-    mma_runs<S, T, U0 + NS>(tmem_d, a, b0, b_step, first);
+    mma_runs<S, T, U0 + NS, LEN>(tmem_d, a, b0, b_step, first);
   }
 }
 // Accumulators: S diagonals t + u <= S-1, plus (S even) the square pair (S/2, S/2) of diagonal S: the
@@ -118,9 +118,18 @@ template <int S, int T>
 __device__ __forceinline__ void mma_slices(uint32_t tmem_d, uint64_t a0, uint64_t a_step, uint64_t b0, uint64_t b_step,
                                            bool first) {
   if constexpr (T < S) {
-    mma_runs<S, T, 0>(tmem_d, a0 + T * a_step, b0, b_step, first);
-    if constexpr (S % 2 == 0 && T == S / 2)  // the square pair (S/2, S/2) into accumulator S
-      mma_i8<0, 1>(tmem_d + (uint32_t)(S * QB), a0 + T * a_step, b0 + T * b_step, first ? 0u : 1u);
+    if constexpr (S % 2 == 0 && T == S / 2) {
+      // the square pair (S/2, S/2) into accumulator S, adjacent to the run's last one: after the first
+      // K-step (which must start accumulator S from zero on its own) it extends the run by one slice
+      if (first) {
+        mma_runs<S, T, 0>(tmem_d, a0 + T * a_step, b0, b_step, first);
+        mma_i8<0, 1>(tmem_d + (uint32_t)(S * QB), a0 + T * a_step, b0 + T * b_step, 0u);
+      } else {
+        mma_runs<S, T, 0, S - T + 1>(tmem_d, a0 + T * a_step, b0, b_step, first);
+      }
+    } else {
+      mma_runs<S, T, 0>(tmem_d, a0 + T * a_step, b0, b_step, first);
+    }
     mma_slices<S, T + 1>(tmem_d, a0, a_step, b0, b_step, first);
   }
 }
