@@ -208,6 +208,14 @@ double cvg_rng_uniform01(cvg_rng* rng);
 void cvg_random_dataset(cvg_rng* rng, int64_t n, int64_t k, int64_t m, double* x, double* y);
 /* random_partitioning, random.hpp:38-50 (balanced labels, Fisher-Yates). */
 void cvg_random_partitioning(cvg_rng* rng, int64_t n, int32_t p, int32_t* labels);
+/* The same two generators over a caller-owned 64-bit engine: next(state) returns its next
+ * draw.  The C++ header (cvgram/random.hpp) passes the caller's std::mt19937_64 through
+ * these, so the seeded-data contract has one implementation.  cvg_uniform01_bits maps one
+ * draw to [0, 1) (random.hpp:16-18). */
+typedef uint64_t (*cvg_next_fn)(void* state);
+double cvg_uniform01_bits(uint64_t draw);
+void cvg_random_dataset_fn(cvg_next_fn next, void* state, int64_t n, int64_t k, int64_t m, double* x, double* y);
+void cvg_random_partitioning_fn(cvg_next_fn next, void* state, int64_t n, int32_t p, int32_t* labels);
 
 /* ------------------------------------------- small vector kernels (fast.hpp) */
 /* training_mean, fast.hpp:40-47 (on the device). */

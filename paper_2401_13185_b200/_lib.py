@@ -66,6 +66,9 @@ SIGNATURES = {
     "cvg_rng_uniform01": (c_double, [c_vp]),
     "cvg_random_dataset": (None, [c_vp, c_i64, c_i64, c_i64, c_vp, c_vp]),
     "cvg_random_partitioning": (None, [c_vp, c_i64, c_i32, c_vp]),
+    "cvg_uniform01_bits": (c_double, [c_u64]),
+    "cvg_random_dataset_fn": (None, [c_vp, c_vp, c_i64, c_i64, c_i64, c_vp, c_vp]),
+    "cvg_random_partitioning_fn": (None, [c_vp, c_vp, c_i64, c_i32, c_vp]),
     "cvg_training_mean": (c_int, [c_vp, c_vp, c_vp, c_i64, c_i64, c_i64, c_vp, c_char_p, c_size_t]),
     "cvg_training_std": (c_int, [c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_vp, c_char_p, c_size_t]),
     "cvg_hadamard_outer_divide": (c_int, [c_vp, c_vp, c_i64, c_i64, c_vp, c_i64, c_vp, c_i64, c_vp, c_char_p,

@@ -146,19 +146,30 @@ struct cvg_rng {
 cvg_rng* cvg_rng_create(uint64_t seed) { return new (std::nothrow) cvg_rng{std::mt19937_64(seed)}; }
 void cvg_rng_destroy(cvg_rng* rng) { delete rng; }
 uint64_t cvg_rng_next(cvg_rng* rng) { return rng->eng(); }
-double cvg_rng_uniform01(cvg_rng* rng) { return static_cast<double>(rng->eng() >> 11) * 0x1.0p-53; }
+double cvg_uniform01_bits(uint64_t draw) { return static_cast<double>(draw >> 11) * 0x1.0p-53; }
+double cvg_rng_uniform01(cvg_rng* rng) { return cvg_uniform01_bits(rng->eng()); }
+
+void cvg_random_dataset_fn(cvg_next_fn next, void* state, int64_t n, int64_t k, int64_t m, double* x, double* y) {
+  for (int64_t i = 0; i < n * k; ++i) x[i] = cvg_uniform01_bits(next(state));
+  for (int64_t i = 0; i < n * m; ++i) y[i] = cvg_uniform01_bits(next(state));
+}
+
+void cvg_random_partitioning_fn(cvg_next_fn next, void* state, int64_t n, int32_t p, int32_t* labels) {
+  for (int64_t i = 0; i < n; ++i) labels[i] = 1 + static_cast<int32_t>(i % p);
+  for (int64_t i = n - 1; i > 0; --i) {
+    const int64_t j = static_cast<int64_t>(next(state) % static_cast<uint64_t>(i + 1));
+    std::swap(labels[i], labels[j]);
+  }
+}
+
+static uint64_t rng_next_tramp(void* st) { return static_cast<cvg_rng*>(st)->eng(); }
 
 void cvg_random_dataset(cvg_rng* rng, int64_t n, int64_t k, int64_t m, double* x, double* y) {
-  for (int64_t i = 0; i < n * k; ++i) x[i] = cvg_rng_uniform01(rng);
-  for (int64_t i = 0; i < n * m; ++i) y[i] = cvg_rng_uniform01(rng);
+  cvg_random_dataset_fn(rng_next_tramp, rng, n, k, m, x, y);
 }
 
 void cvg_random_partitioning(cvg_rng* rng, int64_t n, int32_t p, int32_t* labels) {
-  for (int64_t i = 0; i < n; ++i) labels[i] = 1 + static_cast<int32_t>(i % p);
-  for (int64_t i = n - 1; i > 0; --i) {
-    const int64_t j = static_cast<int64_t>(rng->eng() % static_cast<uint64_t>(i + 1));
-    std::swap(labels[i], labels[j]);
-  }
+  cvg_random_partitioning_fn(rng_next_tramp, rng, n, p, labels);
 }
 
 int cvg_context_create(int device, cvg_context** out, char* err, size_t errlen) {

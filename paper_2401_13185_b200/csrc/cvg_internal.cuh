@@ -41,7 +41,10 @@ constexpr int64_t kChunkRowsTf32 = 12288;
 // digits in [-128, 127] (rows < 21,845 at S = 6); the exponent is per (segment, column).
 constexpr int64_t kChunkRowsI8 = 16384;
 constexpr int kTileF32 = 128;             // tcgen05 tile edge (M = N = 128)
-constexpr int kTileRowsPerWarp = 1024; // rows per warp in the bucketing passes
+constexpr int kTileRowsPerWarp = 1024; // rows per warp in the bucketing passes (at least)
+// Bound on the bucketing's tile x fold counter table (int32): 2^26 counters = 256 MB.  Past it
+// (leave-one-out-scale P) tiles grow by powers of two, so memory stays O(N + P), not O(N P / 1024).
+constexpr int64_t kMaxTileCounters = int64_t(1) << 26;
 
 // Checked builds (make CHECKED=1 -> _build_checked/, selected with CVG_LIB_VARIANT=checked):
 // device-side bounds assertions on every index the kernels derive (row maps,
@@ -76,6 +79,7 @@ struct Status {
 
 // ------------------------------------------------------------------ kernels
 // Bucketing (build_validation_partitions, partition.hpp:61-68) on the device.
+int64_t bucket_tile_rows(int64_t n, int32_t p);  // rows per bucketing tile (>= kTileRowsPerWarp)
 void launch_tile_histogram(const int32_t* labels, int64_t n, int32_t p, int32_t* tile_counts,
                            unsigned long long* bad_row, cudaStream_t s);
 void launch_tile_scan(int32_t* tile_counts, int64_t ntiles, int32_t p, int64_t* fold_counts, cudaStream_t s);
@@ -114,6 +118,8 @@ struct PairOp {
   double* d;
 };
 void launch_pair_sums(const PairOp* ops, int nops, int64_t kp, const int2* tiles, int ntiles, cudaStream_t s);
+// g[0] = NaN when *flag has bit 0 set (non-finite input seen by K1): the flag rides in the partial.
+void launch_poison_if_flag(const int* flag, double* g, cudaStream_t s);
 
 // K5: epilogue.
 struct FoldStatsDev {

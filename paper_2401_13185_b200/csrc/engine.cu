@@ -293,7 +293,12 @@ int64_t Plan::chunk_rows() const {
     const long long r = v ? std::atoll(v) : 0;
     return (int64_t)(r > 0 ? r : 0);
   }();
-  if (env > 0) return round_up(env, row_step_);
+  if (env > 0) {
+    int64_t r = round_up(env, row_step_);
+    // int8 digits: exact int32 TMEM sums need slices * 2^14 * rows < 2^31 (21,845 rows at 6 digits)
+    if (i8_path()) r = std::min(r, ((INT32_MAX / ((int64_t)slices_ << 14)) / row_step_) * row_step_);
+    return r;
+  }
   return round_up(i8_path() ? kChunkRowsI8 : dtype_ == 0 ? kChunkRows : f16_path() ? kChunkRowsF32 : kChunkRowsTf32,
                   row_step_);
 }
@@ -453,7 +458,8 @@ void Plan::assign_rank() {
 Status Plan::bind_labels(const int32_t* d_labels, bool validate, bool require_scalable) {
   src_n_ = n_;
   cudaStream_t s = ctx_->stream;
-  const int64_t ntiles = (n_ + kTileRowsPerWarp - 1) / kTileRowsPerWarp;
+  const int64_t tile_rows = bucket_tile_rows(n_, p_);
+  const int64_t ntiles = (n_ + tile_rows - 1) / tile_rows;
   CVG_TRY(tile_counts_.ensure(sizeof(int32_t) * ntiles * p_));
   CVG_TRY(fold_counts_.ensure(sizeof(int64_t) * p_));
   CVG_TRY(bad_.ensure(sizeof(unsigned long long)));
@@ -734,7 +740,8 @@ Status Plan::gram(const void* d_x, int64_t ldx, const void* d_y, int64_t ldy, co
     }
     CVG_TRY(i8_gram(tilesq_d_.as<int2>(), (int)tilesq_.size()));
     CVG_TRY(gram_trees());
-    return i8_exact_pass(d_x, ldx, d_y, ldy, rows, nsrc);
+    CVG_TRY(i8_exact_pass(d_x, ldx, d_y, ldy, rows, nsrc));
+    return poison_local();
   } else {
     // fp64: K1 builds the fold-bucketed, shifted copy Z.  (Gathering X rows
     // straight into the Gram's shared-memory stages, or overlapping K1 with K2
@@ -756,7 +763,13 @@ Status Plan::gram(const void* d_x, int64_t ldx, const void* d_y, int64_t ldy, co
       CVG_TRY(count_launch());
     }
   }
-  return gram_trees();
+  CVG_TRY(gram_trees());
+  return poison_local();
+}
+
+Status Plan::poison_local() {
+  launch_poison_if_flag(flag_.as<int>(), local_.as<double>(), ctx_->stream);
+  return count_launch();
 }
 
 // One int8-path preparation pass over Z columns [c0, c1): segment maxima (a row sample of stride
@@ -933,7 +946,8 @@ Status Plan::gram_host(const void* h_x, const void* h_y, void* d_x, void* d_y, c
     }
   }
   CVG_TRY(gram_trees());
-  return i8_path() ? i8_exact_pass(d_x, k_, d_y, m_, src_row_.as<int64_t>(), src_n_) : Status::Ok();
+  if (i8_path()) CVG_TRY(i8_exact_pass(d_x, k_, d_y, m_, src_row_.as<int64_t>(), src_n_));
+  return poison_local();
 }
 
 Status Plan::finish(const double* d_rank_partials, int32_t n_ranks, const double* total_override,

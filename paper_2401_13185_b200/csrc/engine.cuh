@@ -138,6 +138,7 @@ class Plan {
  private:
   Status plan_segments();
   Status gram_trees();
+  Status poison_local();  // non-finite flag -> NaN in the exchanged partial (launch_poison_if_flag)
   Status i8_prep(const void* d_x, int64_t ldx, const void* d_y, int64_t ldy, const int64_t* rows, int64_t nsrc,
                  int64_t c0, int64_t c1, bool exact);
   Status i8_gram(const int2* tiles, int ntiles);

@@ -6,7 +6,8 @@
 // order), so the Gram reads each fold with plain sequential tiles.
 //
 // Three passes, all integer work, bit-exact by construction:
-//   1. tile histogram: one warp per 1024-row tile counts its labels (warp
+//   1. tile histogram: one warp per tile (1024 rows, or more when P is large: the
+//      tile x fold table stays <= 2^26 counters) counts its labels (warp
 //      __match_any_sync groups equal labels; the group leader owns the update,
 //      so no atomics and no contention).  Out-of-range labels record the first
 //      offending row (validate_partitioning's first violated clause,
@@ -18,14 +19,14 @@
 namespace cvg {
 namespace {
 
-__global__ void tile_histogram_kernel(const int32_t* __restrict__ labels, int64_t n, int32_t p,
+__global__ void tile_histogram_kernel(const int32_t* __restrict__ labels, int64_t n, int32_t p, int64_t tile_rows,
                                       int32_t* __restrict__ tile_counts, unsigned long long* __restrict__ bad) {
   const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  const int64_t row0 = warp * kTileRowsPerWarp;
+  const int64_t row0 = warp * tile_rows;
   if (row0 >= n) return;
   int32_t* counts = tile_counts + warp * p;
-  const int64_t row_end = min(n, row0 + kTileRowsPerWarp);
+  const int64_t row_end = min(n, row0 + tile_rows);
   for (int64_t base = row0; base < row_end; base += 32) {
     const int64_t row = base + lane;
     const bool live = row < row_end;
@@ -80,16 +81,17 @@ __global__ void tile_scan_kernel(int32_t* __restrict__ tile_counts, int64_t ntil
 
 // Consumes tile_offsets: each warp owns its tile's row of per-fold offsets and
 // advances it as it walks the tile, so ranks stay stable without atomics.
-__global__ void scatter_kernel(const int32_t* __restrict__ labels, int64_t n, int32_t p, int32_t fold_begin,
+__global__ void scatter_kernel(const int32_t* __restrict__ labels, int64_t n, int32_t p, int64_t tile_rows,
+                               int32_t fold_begin,
                                int32_t fold_end, int32_t* __restrict__ tile_offsets,
                                const int64_t* __restrict__ fold_zbase, int64_t win_lo, int64_t win_hi,
                                int64_t* __restrict__ src_row, int64_t zrows) {
   const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  const int64_t row0 = warp * kTileRowsPerWarp;
+  const int64_t row0 = warp * tile_rows;
   if (row0 >= n) return;
   int32_t* run = tile_offsets + warp * p;
-  const int64_t row_end = min(n, row0 + kTileRowsPerWarp);
+  const int64_t row_end = min(n, row0 + tile_rows);
   for (int64_t base = row0; base < row_end; base += 32) {
     const int64_t row = base + lane;
     const bool live = row < row_end;
@@ -141,12 +143,19 @@ void launch_remap_rows(const int64_t* src_row, int64_t zrows, const int64_t* map
   remap_rows_kernel<<<(unsigned)((zrows + 255) / 256), 256, 0, s>>>(src_row, zrows, map, n_map, n_compact, out, bad);
 }
 
+int64_t bucket_tile_rows(int64_t n, int32_t p) {
+  int64_t r = kTileRowsPerWarp;
+  while (((n + r - 1) / r) * (int64_t)p > kMaxTileCounters && r < n) r *= 2;
+  return r;
+}
+
 void launch_tile_histogram(const int32_t* labels, int64_t n, int32_t p, int32_t* tile_counts,
                            unsigned long long* bad, cudaStream_t s) {
-  const int64_t ntiles = (n + kTileRowsPerWarp - 1) / kTileRowsPerWarp;
+  const int64_t tile_rows = bucket_tile_rows(n, p);
+  const int64_t ntiles = (n + tile_rows - 1) / tile_rows;
   const int threads = 256;
   const int64_t blocks = (ntiles * 32 + threads - 1) / threads;
-  tile_histogram_kernel<<<(unsigned)blocks, threads, 0, s>>>(labels, n, p, tile_counts, bad);
+  tile_histogram_kernel<<<(unsigned)blocks, threads, 0, s>>>(labels, n, p, tile_rows, tile_counts, bad);
 }
 
 void launch_tile_scan(int32_t* tile_counts, int64_t ntiles, int32_t p, int64_t* fold_counts, cudaStream_t s) {
@@ -156,10 +165,11 @@ void launch_tile_scan(int32_t* tile_counts, int64_t ntiles, int32_t p, int64_t* 
 void launch_scatter(const int32_t* labels, int64_t n, int32_t p, int32_t fold_begin, int32_t fold_end,
                     int32_t* tile_offsets, const int64_t* fold_zbase, int64_t win_lo, int64_t win_hi, int64_t* src_row,
                     int64_t zrows, cudaStream_t s) {
-  const int64_t ntiles = (n + kTileRowsPerWarp - 1) / kTileRowsPerWarp;
+  const int64_t tile_rows = bucket_tile_rows(n, p);
+  const int64_t ntiles = (n + tile_rows - 1) / tile_rows;
   const int threads = 256;
   const int64_t blocks = (ntiles * 32 + threads - 1) / threads;
-  scatter_kernel<<<(unsigned)blocks, threads, 0, s>>>(labels, n, p, fold_begin, fold_end, tile_offsets, fold_zbase,
+  scatter_kernel<<<(unsigned)blocks, threads, 0, s>>>(labels, n, p, tile_rows, fold_begin, fold_end, tile_offsets, fold_zbase,
                                                       win_lo, win_hi, src_row, zrows);
 }
 

@@ -54,7 +54,16 @@ __global__ void __launch_bounds__(256) pair_sum_kernel(const PairOp* __restrict_
   }
 }
 
+// A plan whose K1 flagged a non-finite input writes NaN into its node's (0, 0) entry, so the flag
+// travels with the partial through the cross-rank exchange and every rank's fold statistics
+// (which test the total's diagonal) report it -- not only the rank that owns the bad rows.
+__global__ void poison_if_flag_kernel(const int* __restrict__ flag, double* __restrict__ g) {
+  if (*flag & 1) g[0] = __longlong_as_double(0x7ff8000000000000ll);
+}
+
 }  // namespace
+
+void launch_poison_if_flag(const int* flag, double* g, cudaStream_t s) { poison_if_flag_kernel<<<1, 1, 0, s>>>(flag, g); }
 
 void launch_pair_sums(const PairOp* ops, int nops, int64_t kp, const int2* tiles, int ntiles, cudaStream_t s) {
   if (nops <= 0 || ntiles <= 0) return;

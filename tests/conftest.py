@@ -14,11 +14,9 @@ if HERE not in sys.path:
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a B200 (sm_100a) device")
     config.addinivalue_line("markers", "slow: long-running parity case")
-
-
-@pytest.fixture(scope="session", autouse=True)
-def _built():
-    """Build the engine and the oracle once (nvcc cross-compiles without a GPU)."""
+    # Build the engine and the oracle before collection: test modules import the
+    # package, whose import fails loudly without the sm_100a library (nvcc
+    # cross-compiles without a GPU, so a fresh clone collects cleanly).
     import __graft_entry__
 
     __graft_entry__.build()

@@ -141,3 +141,37 @@ def test_fold_range_is_a_tree_partition():
             if world & (world - 1) == 0 and p >= world:
                 sizes = [b - a for a, b in ranges]
                 assert max(sizes) - min(sizes) <= 1 + (world > 2)  # midpoint tree is near-balanced
+
+
+def test_numpy_mt19937_64_and_partitioning_match_both_libraries():
+    """workloads.py's numpy engine (used by both bench arms, no .so) draws the same stream
+    as the product's and the oracle's std::mt19937_64, and its random_partitioning the same labels."""
+    import workloads
+
+    k = KATS["mt19937_64"]
+    assert str(int(workloads.mt19937_64(k["seed"], k["index"])[-1])) == k["value"]
+    for seed in (0, 1, 20240124, 2**64 - 1):
+        o = oracle.MT64(seed)
+        ref = [o.next() for _ in range(700)]
+        assert [int(v) for v in workloads.mt19937_64(seed, 700)] == ref
+    for n, p, seed in ((1, 1, 3), (2, 2, 5), (1000, 7, 11), (20011, 100, 20240124)):
+        lab = workloads.random_partitioning(n, p, seed)
+        assert np.array_equal(lab, cv.random_partitioning(n, p, seed).labels)
+        assert np.array_equal(lab, oracle.MT64(seed).random_partitioning(n, p))
+
+
+def test_numpy_alg7_matches_r64():
+    """The numpy/OpenBLAS CPU point (oracle/numpy_alg7.py) restates the same algorithm as R64."""
+    from oracle import numpy_alg7
+
+    rng = np.random.default_rng(3)
+    n, k, m, p = 600, 9, 3, 5
+    x = rng.uniform(-5, 5, k) + rng.uniform(0.5, 2, k) * rng.standard_normal((n, k))
+    y = x @ rng.standard_normal((k, m)) + rng.uniform(-3, 3, m)
+    labels = rng.integers(1, p + 1, n).astype(np.int32)
+    labels[:p] = np.arange(1, p + 1)
+    for cfg in range(16):
+        ref = oracle.fast_all_folds(x, y, labels, p, cfg)
+        got = numpy_alg7.run_all_folds(x, y, labels, p, cfg)
+        for r, (gx, gy) in zip(ref, got):
+            assert oracle.max_rel_diff(gx, r.xtx_t) < 1e-8 and oracle.max_rel_diff(gy, r.xty_t) < 1e-8
