@@ -26,7 +26,7 @@
  * are hand-computed values inside the Catch2 sources (test_fast.cpp,
  * test_core.cpp, test_baseline.cpp, test_partition.cpp, acceptance.cpp).  They
  * are transcribed into tests/golden/reference_kats.json and checked against
- * this file by tests/test_oracle_kats.py.  The seeded generator is
+ * this file by tests/test_reference_kats.py.  The seeded generator is
  * std::mt19937_64 (standard-specified; pinned by its 10000th output).
  *
  * Eigen's GEMM summation order is unspecified, so R64/B64
@@ -713,117 +713,119 @@ int orc_baseline_all_folds(const double* x, const double* y, int64_t n, int64_t 
 /* ------------------------------------------------------------------------- */
 typedef long double ld;
 
+static inline ld load_val(const void* base, int f32, int64_t idx) {
+  return f32 ? (ld)((const float*)base)[idx] : (ld)((const double*)base)[idx];
+}
+
+#define TRUTH_PANEL 64
+#define TRUTH_IB 32 /* Gram rows per task */
+
 typedef struct {
   const void *x, *y;
   int f32;
   int64_t n, k, m, w; /* w = k + m */
   const int64_t *rows, *offsets;
   const ld* shift; /* [w] */
-  ld* gv;          /* [p][k][w] validation Gram in shifted basis */
+  ld* gv;          /* [p][k][w] validation Gram in shifted basis (upper part, c >= i) */
   ld* sv;          /* [p][w] */
   ld* qv;          /* [p][w] */
+  int64_t nib;     /* Gram row blocks per fold */
+  int64_t ntasks;
+  int64_t next;    /* dynamic task counter */
 } truth_job;
 
-static inline ld load_val(const void* base, int f32, int64_t idx) {
-  return f32 ? (ld)((const float*)base)[idx] : (ld)((const double*)base)[idx];
-}
-
-#define TRUTH_PANEL 64
-
-static void truth_fold_fn(void* ctx, int64_t f) {
-  truth_job* j = (truth_job*)ctx;
+/* One task = (fold f, Gram rows [i_lo, i_hi)): rows of g are disjoint across tasks, so the
+ * (fold, row block) tasks run in any order with a fixed per-entry summation order (row panels
+ * in ascending order, 4 interleaved partial sums per panel). */
+static void truth_task(truth_job* j, int64_t t) {
   const int64_t k = j->k, m = j->m, w = j->w;
+  const int64_t f = t / j->nib, ib = t % j->nib;
+  const int64_t i_lo = ib * TRUTH_IB, i_hi = i_lo + TRUTH_IB < k ? i_lo + TRUTH_IB : k;
   const int64_t beg = j->offsets[f], end = j->offsets[f + 1];
+  const int64_t c0 = ib == 0 ? 0 : i_lo; /* columns this task reads (row block 0 also owns the sums) */
+  const int64_t wc = w - c0;
   ld* g = j->gv + f * k * w;
   ld* s = j->sv + f * w;
   ld* q = j->qv + f * w;
-  memset(g, 0, sizeof(ld) * (size_t)(k * w));
-  memset(s, 0, sizeof(ld) * (size_t)w);
-  memset(q, 0, sizeof(ld) * (size_t)w);
-  /* panel transposed: zp[col][r] */
-  ld* zp = (ld*)malloc(sizeof(ld) * (size_t)(w * TRUTH_PANEL));
+  for (int64_t i = i_lo; i < i_hi; ++i)
+    for (int64_t c = i; c < w; ++c) g[i * w + c] = 0;
+  if (ib == 0) {
+    memset(s, 0, sizeof(ld) * (size_t)w);
+    memset(q, 0, sizeof(ld) * (size_t)w);
+  }
+  ld* zp = (ld*)malloc(sizeof(ld) * (size_t)(wc * TRUTH_PANEL)); /* panel transposed: zp[col - c0][r] */
   for (int64_t r0 = beg; r0 < end; r0 += TRUTH_PANEL) {
-    int64_t rr = end - r0 < TRUTH_PANEL ? end - r0 : TRUTH_PANEL;
+    const int64_t rr = end - r0 < TRUTH_PANEL ? end - r0 : TRUTH_PANEL;
     for (int64_t r = 0; r < rr; ++r) {
-      int64_t row = j->rows[r0 + r];
-      for (int64_t c = 0; c < k; ++c) zp[c * TRUTH_PANEL + r] = load_val(j->x, j->f32, row * k + c) - j->shift[c];
-      for (int64_t c = 0; c < m; ++c)
-        zp[(k + c) * TRUTH_PANEL + r] = load_val(j->y, j->f32, row * m + c) - j->shift[k + c];
+      const int64_t row = j->rows[r0 + r];
+      for (int64_t c = c0; c < w; ++c)
+        zp[(c - c0) * TRUTH_PANEL + r] =
+            (c < k ? load_val(j->x, j->f32, row * k + c) : load_val(j->y, j->f32, row * m + (c - k))) - j->shift[c];
     }
-    for (int64_t c = 0; c < w; ++c) {
-      ld a = 0, b = 0;
-      for (int64_t r = 0; r < rr; ++r) {
-        a += zp[c * TRUTH_PANEL + r];
-        b += zp[c * TRUTH_PANEL + r] * zp[c * TRUTH_PANEL + r];
+    if (ib == 0)
+      for (int64_t c = 0; c < w; ++c) {
+        ld a = 0, b = 0;
+        for (int64_t r = 0; r < rr; ++r) {
+          a += zp[c * TRUTH_PANEL + r];
+          b += zp[c * TRUTH_PANEL + r] * zp[c * TRUTH_PANEL + r];
+        }
+        s[c] += a;
+        q[c] += b;
       }
-      s[c] += a;
-      q[c] += b;
-    }
-    for (int64_t i = 0; i < k; ++i) {
-      const ld* zi = zp + i * TRUTH_PANEL;
+    for (int64_t i = i_lo; i < i_hi; ++i) {
+      const ld* zi = zp + (i - c0) * TRUTH_PANEL;
       for (int64_t c = i; c < w; ++c) {
-        const ld* zc = zp + c * TRUTH_PANEL;
-        ld acc = 0;
-        for (int64_t r = 0; r < rr; ++r) acc += zi[r] * zc[r];
-        g[i * w + c] += acc;
+        const ld* zc = zp + (c - c0) * TRUTH_PANEL;
+        ld a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+        int64_t r = 0;
+        for (; r + 4 <= rr; r += 4) {
+          a0 += zi[r] * zc[r];
+          a1 += zi[r + 1] * zc[r + 1];
+          a2 += zi[r + 2] * zc[r + 2];
+          a3 += zi[r + 3] * zc[r + 3];
+        }
+        for (; r < rr; ++r) a0 += zi[r] * zc[r];
+        g[i * w + c] += (a0 + a1) + (a2 + a3);
       }
     }
   }
   free(zp);
 }
 
-int orc_truth_all_folds(const void* x, const void* y, int is_f32, int64_t n, int64_t k, int64_t m,
-                        const int32_t* labels, int64_t n_labels, int32_t p, uint32_t cfg, int n_threads,
-                        double* xtx, double* xty, double* mean_x, double* mean_y, double* std_x, double* std_y,
-                        int64_t* n_train, int64_t* n_val, char* err, size_t errlen) {
-  int rc = run_checks(n, k, m, labels, n_labels, p, cfg, err, errlen);
-  if (rc) return rc;
-  const int64_t w = k + m;
-  ld* shift = (ld*)malloc(sizeof(ld) * (size_t)w);
-  for (int64_t c = 0; c < w; ++c) {
-    ld acc = 0;
-    for (int64_t r = 0; r < n; ++r)
-      acc += c < k ? load_val(x, is_f32, r * k + c) : load_val(y, is_f32, r * m + (c - k));
-    shift[c] = (ld)(double)(acc / (ld)n); /* fp64-rounded: z = x - c is exact for near-constant columns */
+static void* truth_worker(void* arg) {
+  truth_job* j = (truth_job*)arg;
+  for (;;) {
+    const int64_t t = __atomic_fetch_add(&j->next, 1, __ATOMIC_RELAXED);
+    if (t >= j->ntasks) break;
+    truth_task(j, t);
   }
-  int64_t* rows = (int64_t*)malloc(sizeof(int64_t) * (size_t)n);
-  int64_t* offsets = (int64_t*)malloc(sizeof(int64_t) * (size_t)(p + 1));
-  orc_build_validation_partitions(labels, n, p, rows, offsets);
-  ld* gv = (ld*)malloc(sizeof(ld) * (size_t)(p * k * w));
-  ld* sv = (ld*)malloc(sizeof(ld) * (size_t)(p * w));
-  ld* qv = (ld*)malloc(sizeof(ld) * (size_t)(p * w));
-  if (!shift || !rows || !offsets || !gv || !sv || !qv) return ORC_E_OOM;
-  truth_job job = {x, y, is_f32, n, k, m, w, rows, offsets, shift, gv, sv, qv};
-  orc_parallel_for(p, n_threads, truth_fold_fn, &job);
-  /* totals */
-  ld* gt = (ld*)calloc((size_t)(k * w), sizeof(ld));
-  ld* st = (ld*)calloc((size_t)w, sizeof(ld));
-  ld* qt = (ld*)calloc((size_t)w, sizeof(ld));
-  for (int32_t f = 0; f < p; ++f) {
-    for (int64_t i = 0; i < k * w; ++i) gt[i] += gv[f * k * w + i];
-    for (int64_t c = 0; c < w; ++c) {
-      st[c] += sv[f * w + c];
-      qt[c] += qv[f * w + c];
-    }
-  }
+  return NULL;
+}
+
+/* Per-configuration epilogue of RLD (fast.hpp:94-128 in long double, shifted basis). */
+static void truth_epilogue(const truth_job* j, int32_t p, const ld* gt, const ld* st, const ld* qt, uint32_t cfg,
+                           double* xtx, double* xty, double* mean_x, double* mean_y, double* std_x, double* std_y,
+                           int64_t* n_train, int64_t* n_val) {
+  const int64_t n = j->n, k = j->k, m = j->m, w = j->w;
+  const ld* shift = j->shift;
   ld* mz = (ld*)malloc(sizeof(ld) * (size_t)w);
   ld* sd = (ld*)malloc(sizeof(ld) * (size_t)w);
   ld* sT = (ld*)malloc(sizeof(ld) * (size_t)w);
   for (int32_t f = 0; f < p; ++f) {
-    const int64_t nv = offsets[f + 1] - offsets[f], nt = n - nv;
+    const int64_t nv = j->offsets[f + 1] - j->offsets[f], nt = n - nv;
     const ld ntl = (ld)nt;
     if (n_train) n_train[f] = nt;
     if (n_val) n_val[f] = nv;
     for (int64_t c = 0; c < w; ++c) {
-      sT[c] = st[c] - sv[f * w + c];
-      const ld qT = qt[c] - qv[f * w + c];
+      sT[c] = st[c] - j->sv[f * w + c];
+      const ld qT = qt[c] - j->qv[f * w + c];
       mz[c] = sT[c] / ntl;
       ld rad = (qT - sT[c] * mz[c]) / (ntl - 1);
       /* exact-zero rule of training_std (fast.hpp:66-67): a training column
        * whose variance is below long-double resolution is constant. */
       if (rad <= 64 * LDBL_EPSILON * (qT / (ntl - 1))) rad = 0;
-      ld s = sqrtl(rad);
-      sd[c] = s == 0 ? 1 : s;
+      ld sq = sqrtl(rad);
+      sd[c] = sq == 0 ? 1 : sq;
     }
     if (ANY(cfg)) {
       if (mean_x)
@@ -835,7 +837,7 @@ int orc_truth_all_folds(const void* x, const void* y, int is_f32, int64_t n, int
       for (int64_t c = 0; c < k; ++c) std_x[f * k + c] = (double)sd[c];
     if ((cfg & SY) && std_y)
       for (int64_t c = 0; c < m; ++c) std_y[f * m + c] = (double)sd[k + c];
-    const ld* g = gv + f * k * w;
+    const ld* g = j->gv + f * k * w;
     for (int64_t i = 0; i < k; ++i)
       for (int64_t c = i; c < w; ++c) {
         ld v = gt[i * w + c] - g[i * w + c];
@@ -858,6 +860,57 @@ int orc_truth_all_folds(const void* x, const void* y, int is_f32, int64_t n, int
   free(mz);
   free(sd);
   free(sT);
+}
+
+/* RLD for n_cfg configurations from ONE long-double Gram pass.  Outputs are [n_cfg][p][...]. */
+int orc_truth_all_folds_multi(const void* x, const void* y, int is_f32, int64_t n, int64_t k, int64_t m,
+                              const int32_t* labels, int64_t n_labels, int32_t p, const uint32_t* cfgs, int n_cfg,
+                              int n_threads, double* xtx, double* xty, double* mean_x, double* mean_y, double* std_x,
+                              double* std_y, int64_t* n_train, int64_t* n_val, char* err, size_t errlen) {
+  for (int c = 0; c < n_cfg; ++c) {
+    int rc = run_checks(n, k, m, labels, n_labels, p, cfgs[c], err, errlen);
+    if (rc) return rc;
+  }
+  const int64_t w = k + m;
+  ld* shift = (ld*)malloc(sizeof(ld) * (size_t)w);
+  for (int64_t c = 0; c < w; ++c) {
+    ld acc = 0;
+    for (int64_t r = 0; r < n; ++r)
+      acc += c < k ? load_val(x, is_f32, r * k + c) : load_val(y, is_f32, r * m + (c - k));
+    shift[c] = (ld)(double)(acc / (ld)n); /* fp64-rounded: z = x - c is exact for near-constant columns */
+  }
+  int64_t* rows = (int64_t*)malloc(sizeof(int64_t) * (size_t)n);
+  int64_t* offsets = (int64_t*)malloc(sizeof(int64_t) * (size_t)(p + 1));
+  orc_build_validation_partitions(labels, n, p, rows, offsets);
+  ld* gv = (ld*)malloc(sizeof(ld) * (size_t)(p * k * w));
+  ld* sv = (ld*)malloc(sizeof(ld) * (size_t)(p * w));
+  ld* qv = (ld*)malloc(sizeof(ld) * (size_t)(p * w));
+  if (!shift || !rows || !offsets || !gv || !sv || !qv) return ORC_E_OOM;
+  const int64_t nib = (k + TRUTH_IB - 1) / TRUTH_IB;
+  truth_job job = {x, y, is_f32, n, k, m, w, rows, offsets, shift, gv, sv, qv, nib, (int64_t)p * nib, 0};
+  const int workers = n_threads < 1 ? 1 : (int64_t)n_threads < job.ntasks ? n_threads : (int)job.ntasks;
+  pthread_t* th = (pthread_t*)malloc(sizeof(pthread_t) * (size_t)workers);
+  for (int t = 0; t < workers; ++t) pthread_create(&th[t], NULL, truth_worker, &job);
+  for (int t = 0; t < workers; ++t) pthread_join(th[t], NULL);
+  free(th);
+  /* totals: folds in ascending order */
+  ld* gt = (ld*)calloc((size_t)(k * w), sizeof(ld));
+  ld* st = (ld*)calloc((size_t)w, sizeof(ld));
+  ld* qt = (ld*)calloc((size_t)w, sizeof(ld));
+  for (int32_t f = 0; f < p; ++f) {
+    for (int64_t i = 0; i < k; ++i)
+      for (int64_t c = i; c < w; ++c) gt[i * w + c] += gv[f * k * w + i * w + c];
+    for (int64_t c = 0; c < w; ++c) {
+      st[c] += sv[f * w + c];
+      qt[c] += qv[f * w + c];
+    }
+  }
+  for (int c = 0; c < n_cfg; ++c) {
+    const int64_t o = (int64_t)c * p;
+    truth_epilogue(&job, p, gt, st, qt, cfgs[c], xtx + o * k * k, xty + o * k * m, mean_x ? mean_x + o * k : NULL,
+                   mean_y ? mean_y + o * m : NULL, std_x ? std_x + o * k : NULL, std_y ? std_y + o * m : NULL,
+                   n_train, n_val);
+  }
   free(gt);
   free(st);
   free(qt);
@@ -868,6 +921,14 @@ int orc_truth_all_folds(const void* x, const void* y, int is_f32, int64_t n, int
   free(sv);
   free(qv);
   return ORC_OK;
+}
+
+int orc_truth_all_folds(const void* x, const void* y, int is_f32, int64_t n, int64_t k, int64_t m,
+                        const int32_t* labels, int64_t n_labels, int32_t p, uint32_t cfg, int n_threads,
+                        double* xtx, double* xty, double* mean_x, double* mean_y, double* std_x, double* std_y,
+                        int64_t* n_train, int64_t* n_val, char* err, size_t errlen) {
+  return orc_truth_all_folds_multi(x, y, is_f32, n, k, m, labels, n_labels, p, &cfg, 1, n_threads, xtx, xty, mean_x,
+                                   mean_y, std_x, std_y, n_train, n_val, err, errlen);
 }
 
 int orc_version(void) { return 1; }

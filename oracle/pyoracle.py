@@ -76,6 +76,9 @@ def lib():
         for name in ("orc_fast_all_folds", "orc_baseline_all_folds"):
             getattr(L, name).argtypes = ([_vp, _vp, _i64, _i64, _i64, _vp, _i64, _i32, _u32, ctypes.c_int]
                                          + [_vp] * 8 + [ctypes.c_char_p, ctypes.c_size_t])
+        L.orc_truth_all_folds_multi.argtypes = ([_vp, _vp, ctypes.c_int, _i64, _i64, _i64, _vp, _i64, _i32, _vp,
+                                                 ctypes.c_int, ctypes.c_int] + [_vp] * 8
+                                                + [ctypes.c_char_p, ctypes.c_size_t])
         L.orc_truth_all_folds.argtypes = ([_vp, _vp, ctypes.c_int, _i64, _i64, _i64, _vp, _i64, _i32, _u32,
                                            ctypes.c_int] + [_vp] * 8 + [ctypes.c_char_p, ctypes.c_size_t])
         _lib = L
@@ -330,3 +333,25 @@ def baseline_all_folds(x, y, labels, p, cfg, n_threads=1):
 def truth_all_folds(x, y, labels, p, cfg, n_threads=1):
     """RLD: Algorithm 7 in long double in a globally shifted basis (the parity anchor)."""
     return _all_folds(lib().orc_truth_all_folds, x, y, labels, p, cfg, n_threads, truth=True)
+
+
+def truth_all_folds_multi(x, y, labels, p, cfgs, n_threads=1):
+    """RLD for several configurations from one long-double Gram pass: one list of folds per configuration."""
+    labels = np.ascontiguousarray(labels, np.int32)
+    f32 = 1 if np.asarray(x).dtype == np.float32 else 0
+    dt = np.float32 if f32 else np.float64
+    x = np.ascontiguousarray(x, dt)
+    y = np.ascontiguousarray(y, dt)
+    n, k = x.shape
+    m = y.shape[1]
+    nc = len(cfgs)
+    cm = np.ascontiguousarray(cfgs, np.uint32)
+    xtx, xty = np.empty((nc, p, k, k)), np.empty((nc, p, k, m))
+    mx, my, sx, sy = np.zeros((nc, p, k)), np.zeros((nc, p, m)), np.zeros((nc, p, k)), np.zeros((nc, p, m))
+    nt, nv = np.zeros(p, np.int64), np.zeros(p, np.int64)
+    err = ctypes.create_string_buffer(512)
+    _check(lib().orc_truth_all_folds_multi(_p(x), _p(y), f32, n, k, m, _p(labels), labels.size, p, _p(cm), nc,
+                                           n_threads, _p(xtx), _p(xty), _p(mx), _p(my), _p(sx), _p(sy), _p(nt),
+                                           _p(nv), err, 512), err)
+    return [[_fold_result(f + 1, cfg, xtx[c, f], xty[c, f], mx[c, f], my[c, f], sx[c, f], sy[c, f], nt[f], nv[f])
+             for f in range(p)] for c, cfg in enumerate(cfgs)]
