@@ -229,6 +229,13 @@ int cvg_hadamard_outer_divide(cvg_context* ctx, const double* mat, int64_t rows,
                               int64_t n_left, const double* right, int64_t n_right, double* out, char* err,
                               size_t errlen);
 
+/* ------------------------------------------------------------- self-tests */
+/* The epilogue's branch-free fp64 division (the scaled outputs' one division by the product,
+ * core.hpp:128) against the hardware-correct div.rn.f64 over n hashed operand pairs (NaN/inf/subnormal
+ * patterns, quotients near 1, underflow/overflow edges).  *mismatches = fast-path quotients whose bits
+ * differ (must be 0), *fast = quotients the fast path accepted. */
+int cvg_selftest_division(cvg_context* ctx, int64_t n, uint64_t seed, int64_t* mismatches, int64_t* fast);
+
 #ifdef __cplusplus
 }
 #endif

@@ -73,6 +73,7 @@ SIGNATURES = {
     "cvg_training_std": (c_int, [c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_vp, c_char_p, c_size_t]),
     "cvg_hadamard_outer_divide": (c_int, [c_vp, c_vp, c_i64, c_i64, c_vp, c_i64, c_vp, c_i64, c_vp, c_char_p,
                                           c_size_t]),
+    "cvg_selftest_division": (c_int, [c_vp, c_i64, c_u64, c_vp, c_vp]),
 }
 
 _lib = None

@@ -841,6 +841,27 @@ int cvg_global_fold_products(cvg_global* g, const int64_t* v_rows, int64_t n_val
   });
 }
 
+int cvg_selftest_division(cvg_context* ctx, int64_t n, uint64_t seed, int64_t* mismatches, int64_t* fast) {
+  return guarded(nullptr, 0, [&]() -> Status {
+    if (!ctx || n < 0) return Status::Err(CVG_E_INVALID_ARG, "bad arguments");
+    Status s = cvg::cuda_status(cudaSetDevice(ctx->device), "cudaSetDevice");
+    if (!s.ok()) return s;
+    cvg::DevBuf counts;
+    if (!(s = counts.ensure(2 * sizeof(unsigned long long))).ok()) return s;
+    if (!(s = cvg::cuda_status(cudaMemsetAsync(counts.as<void>(), 0, 2 * sizeof(unsigned long long), ctx->stream),
+                               "memset")).ok())
+      return s;
+    cvg::launch_selftest_division(seed, n, counts.as<unsigned long long>(), ctx->stream);
+    ctx->launches += 1;
+    unsigned long long h[2] = {0, 0};
+    if (!(s = d2h(h, counts.as<void>(), sizeof h, ctx->stream)).ok()) return s;
+    if (!(s = cvg::cuda_status(cudaStreamSynchronize(ctx->stream), "stream synchronize")).ok()) return s;
+    if (mismatches) *mismatches = (int64_t)h[0];
+    if (fast) *fast = (int64_t)h[1];
+    return Status::Ok();
+  });
+}
+
 
 int cvg_training_mean(cvg_context* ctx, const double* global_mean, const double* val_mean, int64_t len, int64_t n,
                       int64_t n_val, double* out, char* err, size_t errlen) {

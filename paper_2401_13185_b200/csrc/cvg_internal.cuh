@@ -123,10 +123,10 @@ void launch_poison_if_flag(const int* flag, double* g, cudaStream_t s);
 
 // K5: epilogue.
 struct FoldStatsDev {
-  double* mz;   // [nfold][w] training mean in the shifted basis
-  double* sT;   // [nfold][w] training column sums (shifted)
-  double* sd;   // [nfold][w] training std (zero -> 1)
-};
+  double* mz;   // [nfold][kp] training mean in the shifted basis (padding columns: 0)
+  double* sT;   // [nfold][kp] training column sums (shifted; padding: 0)
+  double* sd;   // [nfold][kp] training std (zero -> 1; padding: 1)
+};  // rows of kp (a multiple of 64): every 64-column slice is a whole, 16-byte aligned 512 B copy
 // Small-fold mode (every fold <= kSmallFoldRows rows, e.g. leave-one-out): no per-fold Gram partials; a fold's
 // Gram entries are formed in the epilogue from its rows of Z (z: zrows x kp, rows zbase[f] .. + n_val[f]).
 constexpr int kSmallFoldRows = 32;
@@ -142,6 +142,8 @@ void launch_products(const double* total, const double* const* foldG, const int6
                      int64_t k, int64_t m, int64_t kp, const double* shift, FoldStatsDev st, const int2* tiles,
                      int ntiles, const uint32_t* cfgs, int ncfg, double* xtx, double* xty, cudaStream_t s,
                      SmallFolds sf = SmallFolds());
+// div_rn_fast vs __ddiv_rn over n hashed operand pairs: counts[0] += mismatches, counts[1] += fast-path quotients.
+void launch_selftest_division(uint64_t seed, int64_t n, unsigned long long* counts, cudaStream_t s);
 void launch_unshift_global(const double* total, int64_t n, int64_t k, int64_t m, int64_t kp, const double* shift,
                            double* xtx, double* xty, double* sum, double* sumsq, double* mean, cudaStream_t s);
 void launch_training_mean(const double* g, const double* v, int64_t len, int64_t n, int64_t nv, double* out,

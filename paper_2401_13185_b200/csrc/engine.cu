@@ -519,10 +519,11 @@ Status Plan::bind_labels(const int32_t* d_labels, bool validate, bool require_sc
   return Status::Ok();
 }
 
-// CVG_I8_FUSED=0 runs K1Q and the int8 Gram as two launches (A/B; bit-identical).
+// CVG_I8_FUSED=1 runs K1Q's cut inside the int8 Gram's persistent launch (K2f; bit-identical).  Opt-in:
+// measured slower than the two launches (c1 4.63 vs 4.24 ms, c4 22.9 vs 20.5 ms).
 bool Plan::i8_fused() {
   const char* v = std::getenv("CVG_I8_FUSED");  // read per call: tests A/B both paths in one process
-  return !(v && v[0] == '0');
+  return v && v[0] == '1';
 }
 
 // CVG_SMALL_FOLDS=0 keeps per-fold Gram partials even when every fold is tiny (A/B tests).
@@ -1020,9 +1021,9 @@ Status Plan::finish(const double* d_rank_partials, int32_t n_ranks, const double
     CVG_CK(cudaStreamSynchronize(s));
     return Status::Ok();
   }
-  CVG_TRY(st_mz_.ensure(sizeof(double) * nown * w_));
-  CVG_TRY(st_sT_.ensure(sizeof(double) * nown * w_));
-  CVG_TRY(st_sd_.ensure(sizeof(double) * nown * w_));
+  CVG_TRY(st_mz_.ensure(sizeof(double) * nown * kp_));
+  CVG_TRY(st_sT_.ensure(sizeof(double) * nown * kp_));
+  CVG_TRY(st_sd_.ensure(sizeof(double) * nown * kp_));
   FoldStatsDev st{st_mz_.as<double>(), st_sT_.as<double>(), st_sd_.as<double>()};
   const double* const* fptr = foldptr_d_.as<const double*>() + lo;
   const int64_t* nval = nval_d_.as<int64_t>() + lo;
@@ -1066,9 +1067,9 @@ Status Plan::finish_direct(const uint32_t* cfgs, int32_t ncfg, double* d_xtx, do
   CVG_CK(cudaMemcpyAsync(zero_ptr_.as<void>(), &zp, sizeof(void*), cudaMemcpyHostToDevice, s));
   const int64_t n_saved = n_;
   n_ = counts_[0];  // the training set is exactly the bound rows
-  CVG_TRY(st_mz_.ensure(sizeof(double) * w_));
-  CVG_TRY(st_sT_.ensure(sizeof(double) * w_));
-  CVG_TRY(st_sd_.ensure(sizeof(double) * w_));
+  CVG_TRY(st_mz_.ensure(sizeof(double) * kp_));
+  CVG_TRY(st_sT_.ensure(sizeof(double) * kp_));
+  CVG_TRY(st_sd_.ensure(sizeof(double) * kp_));
   FoldStatsDev st{st_mz_.as<double>(), st_sT_.as<double>(), st_sd_.as<double>()};
   {
     Timed t(ctx_, kStats);
