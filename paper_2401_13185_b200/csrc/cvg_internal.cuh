@@ -208,16 +208,6 @@ bool launch_gram_i8(int slices, const int8_t* zq, const unsigned long long* segm
                     int64_t kp, const GramTask* segs, int64_t nseg, const int2* tiles, int ntiles, double* part,
                     cudaStream_t s);
 
-// K2f (default fp64 int8 path): K1Q's cut and the Gram in ONE persistent launch (one CTA per SM; the
-// drain warps cut 64-row blocks between drains; the TMA producer waits for its segment's blocks).
-// counters: (1 + nseg) zeroed uint32 -- [0] the next block to claim, [1 + s] blocks of segment s done.
-// Same digits and partials as launch_reorder_q + launch_gram_i8 (bit-identical).
-bool launch_gram_i8_fused(int dtype, int slices, const void* x, int64_t ldx, const void* y, int64_t ldy, int64_t k,
-                          int64_t m, const int64_t* src_row, int64_t zrows, int64_t kp, int64_t nsrc,
-                          const double* shift, const int* blkseg, const unsigned long long* segmax, int headroom,
-                          int* ovf, int* nonfinite, int8_t* zq, const GramTask* segs, int64_t nseg, const int2* tiles,
-                          int ntiles, double* part, unsigned* counters, cudaStream_t s);
-
 inline int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
 inline int64_t padded_cols(int64_t k, int64_t m, int dtype = 0) {
   return round_up(k + m + 1, dtype == 1 ? kTileF32 : kTile);

@@ -519,13 +519,6 @@ Status Plan::bind_labels(const int32_t* d_labels, bool validate, bool require_sc
   return Status::Ok();
 }
 
-// CVG_I8_FUSED=1 runs K1Q's cut inside the int8 Gram's persistent launch (K2f; bit-identical).  Opt-in:
-// measured slower than the two launches (c1 4.63 vs 4.24 ms, c4 22.9 vs 20.5 ms).
-bool Plan::i8_fused() {
-  const char* v = std::getenv("CVG_I8_FUSED");  // read per call: tests A/B both paths in one process
-  return v && v[0] == '1';
-}
-
 // CVG_SMALL_FOLDS=0 keeps per-fold Gram partials even when every fold is tiny (A/B tests).
 bool Plan::small_folds_enabled() {
   static const bool on = [] {
@@ -744,33 +737,8 @@ Status Plan::gram(const void* d_x, int64_t ldx, const void* d_y, int64_t ldy, co
       CVG_CK(cudaMemsetAsync(segmax_.as<void>(), 0, sizeof(unsigned long long) * segs_.size() * kp_, s));
       if (sample_ > 1) CVG_CK(cudaMemsetAsync(ovf_.as<void>(), 0, sizeof(int) * segs_.size(), s));
     }
-    if (zrows_ > 0 && !segs_.empty() && i8_fused()) {
-      // segment maxima, then the cut and the Gram in one persistent launch (K2f)
-      {
-        Timed t(ctx_, kReorder);
-        launch_segmax(dtype_, d_x, ldx, d_y, ldy, k_, m_, rows, segs_d_.as<GramTask>(), (int64_t)segs_.size(),
-                      max_seg_rows(), kp_, 0, kp_, nsrc, shift_.as<double>(), sample_, nullptr,
-                      segmax_.as<unsigned long long>(), s);
-      }
-      CVG_TRY(count_launch());
-      CVG_TRY(counters_.ensure(sizeof(unsigned) * (1 + segs_.size())));
-      CVG_CK(cudaMemsetAsync(counters_.as<void>(), 0, sizeof(unsigned) * (1 + segs_.size()), s));
-      bool ok;
-      {
-        Timed t(ctx_, kGram);
-        ok = launch_gram_i8_fused(dtype_, slices_, d_x, ldx, d_y, ldy, k_, m_, rows, zrows_, kp_, nsrc,
-                                  shift_.as<double>(), blkseg_.as<int>(), segmax_.as<unsigned long long>(),
-                                  sample_ > 1 ? 1 : 0, sample_ > 1 ? ovf_.as<int>() : nullptr, flag_.as<int>(),
-                                  zq_.as<int8_t>(), segs_d_.as<GramTask>(), (int64_t)segs_.size(),
-                                  tilesq_d_.as<int2>(), (int)tilesq_.size(), part_.as<double>(),
-                                  counters_.as<unsigned>(), s);
-      }
-      if (!ok) return Status::Err(5, "cuTensorMapEncodeTiled unavailable or rejected the operand layout");
-      CVG_TRY(count_launch());
-    } else {
-      if (zrows_ > 0) CVG_TRY(i8_prep(d_x, ldx, d_y, ldy, rows, nsrc, 0, kp_, false));
-      CVG_TRY(i8_gram(tilesq_d_.as<int2>(), (int)tilesq_.size()));
-    }
+    if (zrows_ > 0) CVG_TRY(i8_prep(d_x, ldx, d_y, ldy, rows, nsrc, 0, kp_, false));
+    CVG_TRY(i8_gram(tilesq_d_.as<int2>(), (int)tilesq_.size()));
     CVG_TRY(gram_trees());
     CVG_TRY(i8_exact_pass(d_x, ldx, d_y, ldy, rows, nsrc));
     return poison_local();

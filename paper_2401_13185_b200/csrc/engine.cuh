@@ -144,7 +144,6 @@ class Plan {
   Status i8_gram(const int2* tiles, int ntiles);
   Status i8_exact_pass(const void* d_x, int64_t ldx, const void* d_y, int64_t ldy, const int64_t* rows, int64_t nsrc);
   static bool small_folds_enabled();
-  static bool i8_fused();
   SmallFolds small_folds() const {
     SmallFolds sf;
     if (small_) {
@@ -198,7 +197,6 @@ class Plan {
   TreeProgram group_tree_;
   DevBuf zero_g_, zero_nval_, zero_ptr_;
 
-  DevBuf counters_;  // K2f: next block to claim + per-segment blocks done
   DevBuf zq_, segmax_, ovf_, blkseg_, tilesq_d_, tiles_d_, out_tiles_d_, tiles128_d_, zt_hi_, zt_lo_, unscale_, tile_counts_, fold_counts_, bad_, zbase_d_, src_row_, z_, part_, foldbuf_, local_,
       total_, shift_, flag_, tiles_bycol_d_, src_map_, segs_d_, foldptr_d_, nval_d_, st_mz_, st_sT_, st_sd_, cfg_d_;
   TreeProgram fold_tree_, local_tree_, rank_tree_;

@@ -50,12 +50,12 @@ constexpr int kQThreads = 64 + 32 * kQEpiWarps;
 
 // KS rows per pipeline stage: 64 (one SW64 atom row of a 64-row block) or 32 (half of it, SW32):
 // S = 7 fits 2 stages of 64 rows (84 KB each) or 5 of 32 rows (42 KB).
-template <int S, int KS>
+template <int S, int KS, int kMaxSt = 8>
 struct QCfg {
   static constexpr int kA = QA * KS;                      // per slice
   static constexpr int kB = QB * KS;
   static constexpr int kStage = S * (kA + kB);
-  static constexpr int kNst = (227 * 1024 - 2048) / kStage;
+  static constexpr int kNst = (227 * 1024 - 2048) / kStage < kMaxSt ? (227 * 1024 - 2048) / kStage : kMaxSt;
   static constexpr int kSmem = kNst * kStage + 1024;
 };
 
@@ -169,8 +169,15 @@ __device__ __forceinline__ double pow2(int e) {  // 2^e for e in [-1022, 1023]
 // [-1018, 1080], so the cut scales in two power-of-two steps (cut_scales) and the drain
 // unscales through unscale() -- no 2^e ever has to be a normal double.
 __device__ __forceinline__ int seg_exponent(double mx, int headroom) {
+  const uint64_t bits = (uint64_t)__double_as_longlong(mx);
+  const int ex = (int)(bits >> 52);  // sign + biased exponent: 1 .. 2046 for a positive normal max
+  if (ex >= 1 && ex <= 2046) {
+    // normal: ilogb = ex - 1023 and scalbn(mx, e) = 1.f * 2^(5 | 6), which reaches 63.5 (127) iff
+    // 1.f >= 1 + 63/64, i.e. the top 6 fraction bits are all ones -- no libm calls on the hot path
+    return (headroom ? 5 : 6) - (ex - 1023) - (int)(((bits >> 46) & 63) == 63);
+  }
   if (!(mx > 0.0) || !isfinite(mx)) return 0;
-  int e = (headroom ? 5 : 6) - ilogb(mx);
+  int e = (headroom ? 5 : 6) - ilogb(mx);  // subnormal max
   if (scalbn(mx, e) >= (headroom ? 63.5 : 127.0)) --e;
   return e;
 }
@@ -194,13 +201,13 @@ __device__ __forceinline__ double unscale(double f, int E) {
 
 // tiles[i] = {I, J | wmask << 16}: rows 128I .. +128 (Z columns), columns 64J .. +64; wmask bit h:
 // the 64 x 64 sub-tile of rows 128I + 64h is needed downstream (an upper 64-tile of the plan).
-template <int S, int KS>
+template <int S, int KS, int kMaxSt = 8>
 __global__ void __launch_bounds__(kQThreads, 1)
     gram_i8_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                    const unsigned long long* __restrict__ segmax, const GramTask* __restrict__ segs,
                    const int2* __restrict__ tiles,
                    int ntiles, int64_t kp, double* __restrict__ part, int headroom) {
-  using C = QCfg<S, KS>;
+  using C = QCfg<S, KS, kMaxSt>;
   constexpr int NST = C::kNst;
   constexpr int kPer = QK / KS;  // stages per 64-row block
   extern __shared__ uint8_t smem_raw[];
@@ -589,354 +596,6 @@ __global__ void __launch_bounds__(kQ1Threads, CVG_K1Q_MIN_BLOCKS)
   if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
 }
 
-// ---------------------------------------------------------------------------
-// K2f: the fused cut + Gram (default fp64 path).  K1Q alone ran at ~88% of HBM and took a
-// third of the c1 step while the Gram -- tensor-bound -- left HBM mostly idle, and the Gram's
-// 8 drain warps sat idle except at tile ends.  Here ONE persistent launch does both: one CTA
-// per SM walks its (segment, tile) items round-robin (item = blockIdx.x + i * gridDim.x,
-// segment-major), and its 8 drain warps, between drains, cut 64-row blocks of Z into the int8
-// digit slices (the same arithmetic as K1Q, so the digits -- and every partial -- are bit-identical
-// to the two-kernel path).  Blocks are claimed from a global counter in Z order (so segments
-// complete in order); when a group finishes a block it publishes it with a release increment of
-// its segment's counter, and the TMA producer of a Gram item waits (acquire) for its segment's
-// count before loading.  Digits leave by plain 16-byte stores: a thread holds 16 consecutive rows
-// of one column, so a warp's store covers 8 columns x 64 rows = 512 contiguous bytes (whole
-// sectors, no read-for-ownership) -- no shared-memory staging beside the Gram's 3 stages.
-//
-// Drain warps step in lock-step (named barrier 1, 256 threads): at each step thread 0 decides
-// DRAIN (this tile's accumulators are full), CUT (one 64 x 64 chunk), or EXIT.  Claimed blocks sit
-// in a 4-deep ring (s_blk / s_src) so the next block's source rows and first chunk's values are in
-// flight while the current chunk is cut.  A finished block's slot is refilled in two steps (claim
-// after the next barrier, source rows after the one after), so no shared slot is ever written in
-// the step that last read it, and a slot's rows are published two barriers before their first use.  The MMA warp waits for the drain (tmem_empty)
-// before the next tile's first MMA.  No step ever waits on another CTA except the producer's
-// segment wait, and a claimed block is always finished by its claimer, so there is no deadlock.
-constexpr int kFusedRing = 4;
-enum : int { kStepCut = 0, kStepDrain = 1, kStepExit = 2 };
-
-__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
-  uint32_t ok;
-  asm volatile(
-      "{\n"
-      ".reg .pred P;\n"
-      "mbarrier.test_wait.parity.shared::cta.b64 P, [%1], %2;\n"
-      "selp.b32 %0, 1, 0, P;\n"
-      "}\n"
-      : "=r"(ok)
-      : "r"(smem_u32(bar)), "r"(parity)
-      : "memory");
-  return ok != 0;
-}
-
-__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
-  unsigned v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-
-__device__ __forceinline__ void named_bar(int id, int threads) {
-  asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(threads) : "memory");
-}
-
-template <typename T, int S>
-__global__ void __launch_bounds__(kQThreads, 1)
-    gram_i8_fused_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
-                         const T* __restrict__ x, int64_t ldx, const T* __restrict__ y, int64_t ldy, int64_t k,
-                         int64_t m, const int64_t* __restrict__ src_row, int64_t zrows, int64_t kp, int64_t nsrc,
-                         const double* __restrict__ shift, const int* __restrict__ blkseg,
-                         const unsigned long long* __restrict__ segmax, int headroom, int* __restrict__ ovf,
-                         int* __restrict__ nonfinite, int8_t* __restrict__ zq, const GramTask* __restrict__ segs,
-                         const int2* __restrict__ tiles, int ntiles, int64_t nitems, double* __restrict__ part,
-                         unsigned* __restrict__ counters) {
-  using C = QCfg<S, QK>;
-  constexpr int NST = C::kNst;
-  static_assert(8 * S <= 48, "digits must fit the 52-bit window");
-  constexpr uint32_t kHiMask = 8 * S >= 32 ? (0xfff00000u | (0x000fffffu & ~((1u << (8 * S - 32)) - 1u))) : 0xffffffffu;
-  constexpr uint32_t kLoMask = 8 * S >= 32 ? 0u : ~((1u << (8 * S)) - 1u);
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  __shared__ __align__(8) uint64_t full_bar[NST], empty_bar[NST], acc_full, tmem_empty;
-  __shared__ uint32_t tmem_base;
-  __shared__ int64_t s_src[kFusedRing][QK];
-  __shared__ int64_t s_blk[kFusedRing];
-  __shared__ int s_dec;
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t G = gridDim.x;
-  const int64_t nblk = zrows / QK;
-  unsigned* next_blk = counters;
-  unsigned* seg_done = counters + 1;
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < NST; ++s) {
-      mbar_init(&full_bar[s], 1);
-      mbar_init(&empty_bar[s], 1);
-    }
-    mbar_init(&acc_full, 1);
-    mbar_init(&tmem_empty, kQEpiWarps);
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-  }
-  if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(&tmem_base)),
-                 "r"(512));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-  __syncthreads();
-  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-  const uint32_t tmem_d = uniform(tmem_base);
-  auto opA = [&](int s) { return smem + s * C::kStage; };
-  auto opB = [&](int s) { return smem + s * C::kStage + S * C::kA; };
-
-  if (warp == 0) {  // ---- TMA producer: wait for the item's segment, then stream its digits
-    const uint32_t bytes = (uint32_t)(S * (C::kA + C::kB));
-    int64_t g = 0;
-    for (int64_t it = blockIdx.x; it < nitems; it += G) {
-      const int seg = (int)(it / ntiles);
-      const int2 tile0 = tiles[it - (int64_t)seg * ntiles];
-      const int ti = uniform(tile0.x), tj = uniform(tile0.y & 0xffff);
-      const GramTask task0 = segs[seg];
-      const GramTask task{uniform(task0.zrow), uniform(task0.rows)};
-      const unsigned need = (unsigned)(task.rows / QK);
-      while (ld_acquire_u32(seg_done + seg) < need) __nanosleep(128);
-      asm volatile("fence.proxy.async.global;\n" ::: "memory");  // generic-proxy digits -> TMA reads
-      __syncwarp();
-      const int nsteps = (int)(task.rows / QK);
-      for (int st = 0; st < nsteps; ++st, ++g) {
-        const int s = (int)(g % NST);
-        mbar_wait(&empty_bar[s], ((uint32_t)(g / NST) & 1u) ^ 1u);
-        const int blk = (int)(task.zrow / QK) + st;
-        if (elect_one()) {
-          mbar_expect_tx(&full_bar[s], bytes);
-          tma_load_4d(opA(s), &map_a, &full_bar[s], 0, ti * QA, blk, 0);
-          tma_load_4d(opB(s), &map_b, &full_bar[s], 0, tj * QB, blk, 0);
-        }
-        __syncwarp();
-      }
-    }
-  } else if (warp == 1) {  // ---- MMA issuer
-    int64_t g = 0;
-    int t = 0;
-    for (int64_t it = blockIdx.x; it < nitems; it += G, ++t) {
-      const int seg = (int)(it / ntiles);
-      const int nsteps = (int)(segs[seg].rows / QK);
-      if (t > 0) {  // the previous tile's accumulators have been drained
-        mbar_wait(&tmem_empty, (uint32_t)(t - 1) & 1u);
-        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-      }
-      for (int st = 0; st < nsteps; ++st, ++g) {
-        const int s = (int)(g % NST);
-        mbar_wait(&full_bar[s], (uint32_t)(g / NST) & 1u);
-        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-        const uint64_t a0 = kmajor_sw_desc<QK>(opA(s));
-        const uint64_t b0 = kmajor_sw_desc<QK>(opB(s));
-        const uint64_t a_step = (uint64_t)(C::kA >> 4), b_step = (uint64_t)(C::kB >> 4);
-        if (elect_one()) {
-#pragma unroll
-          for (int kk = 0; kk < QK / 32; ++kk)
-            mma_slices<S, 0>(tmem_d, a0 + 2ull * kk, a_step, b0 + 2ull * kk, b_step, st == 0 && kk == 0);
-          mma_commit(&empty_bar[s]);
-          if (st == nsteps - 1) mma_commit(&acc_full);
-        }
-        __syncwarp();
-      }
-    }
-  } else {  // ---- drain + cut warps (256 threads in lock-step on named barrier 1)
-    const int dw = warp - 2;
-    const int tid = threadIdx.x - 64;
-    // cut mapping: warp dw owns columns 8 dw .. 8 dw + 7 of a chunk; lane (j, qq) holds column 8 dw + j,
-    // rows 16 qq .. 16 qq + 15 of the 64-row block
-    const int j = lane >> 2, qq = lane & 3;
-    const int col = 8 * dw + j;
-    const int64_t wd = k + m;
-    const int64_t nchunk = kp / 64;
-    const double Cof = 0x1p52 + (double)DigitOffset<S>::v;
-    const int64_t slice = zrows * kp;  // bytes per digit slice
-    // ring of claimed blocks: h = current; a block claimed into buffer b is first read two steps later
-    if (tid == 0)
-      for (int b = 0; b < kFusedRing; ++b) {
-        const int64_t nb = (int64_t)atomicAdd(next_blk, 1u);
-        s_blk[b] = nb < nblk ? nb : -1;
-      }
-    named_bar(1, 256);
-    if (tid < QK)
-      for (int b = 0; b < kFusedRing; ++b)
-        if (s_blk[b] >= 0) s_src[b][tid] = src_row[s_blk[b] * QK + tid];
-    named_bar(1, 256);
-    int h = 0, cch = 0;
-    int claim_buf = -1;    // slot to refill: thread 0 claims a block into it after the next barrier
-    int load_buf = -1;     // slot whose claimed block's source rows are loaded after the next barrier
-    int done_seg = -1;     // segment whose block finished last step (thread 0 publishes after the barrier)
-    uint32_t oor = 0;
-    double v[16];
-    auto load_vals = [&](int b, int64_t ch) {
-      const int64_t c = ch * 64 + col;
-      const int kind = c < k ? 0 : c < wd ? 1 : c == wd ? 2 : 3;  // x, y, ones, padding
-      const T* base = kind == 0 ? x + c : y + (c - k);
-      const int64_t ld = kind == 0 ? ldx : ldy;
-#pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        const int64_t src = s_src[b][16 * qq + i];
-        CVG_DCHECK(src < nsrc && src >= -1);
-        v[i] = src < 0 ? 0.0 : kind <= 1 ? (double)__ldg(base + src * ld) : kind == 2 ? 1.0 : 0.0;
-      }
-    };
-    if (s_blk[0] >= 0) load_vals(0, 0);
-    int t = 0;
-    int64_t my_it = blockIdx.x;
-    for (;;) {
-      if (tid == 0) {
-        const bool tile_left = my_it < nitems;
-        const bool cut_left = s_blk[h] >= 0;
-        int dec;
-        if (tile_left && (mbar_test(&acc_full, (uint32_t)t & 1u) || !cut_left))
-          dec = kStepDrain;
-        else
-          dec = cut_left ? kStepCut : kStepExit;
-        s_dec = dec;
-      }
-      named_bar(1, 256);
-      const int dec = s_dec;
-      if (tid == 0 && done_seg >= 0) {  // every thread's stores of that block precede the barrier
-        __threadfence();
-        atomicAdd(seg_done + done_seg, 1u);
-      }
-      done_seg = -1;
-      if (load_buf >= 0) {  // claimed one step ago (published by this step's barrier)
-        const int64_t b = s_blk[load_buf];
-        if (tid < QK && b >= 0) s_src[load_buf][tid] = src_row[b * QK + tid];
-        load_buf = -1;
-      }
-      if (claim_buf >= 0) {  // last read in the previous step, before this barrier
-        if (tid == 0) {
-          const int64_t nb = (int64_t)atomicAdd(next_blk, 1u);
-          s_blk[claim_buf] = nb < nblk ? nb : -1;
-        }
-        load_buf = claim_buf;
-        claim_buf = -1;
-      }
-      if (dec == kStepExit) break;
-      if (dec == kStepDrain) {
-        // ---- drain this CTA's tile t: Horner over the diagonal accumulators, exact unscale
-        const int seg = (int)(my_it / ntiles);
-        const int2 tile0 = tiles[my_it - (int64_t)seg * ntiles];
-        const int ti = tile0.x, tj = tile0.y & 0xffff, wmask = tile0.y >> 16;
-        const int q = warp & 3;  // TMEM lanes [32q, 32q + 32) (hardware: warp id mod 4)
-        const int hh = dw >> 2;  // columns [32hh, 32hh + 32) of the 64-wide tile
-        const int64_t row = (int64_t)ti * QA + 32 * q + lane;
-        const int64_t col0 = (int64_t)tj * QB + 32 * hh;
-        const bool write = row < kp && ((wmask >> (q >> 1)) & 1);
-        const unsigned long long* mx = segmax + (int64_t)seg * kp;
-        const int erow = seg_exponent(__longlong_as_double((long long)mx[row < kp ? row : 0]), headroom);
-        const int ecol = seg_exponent(__longlong_as_double((long long)mx[col0 + lane]), headroom);
-        mbar_wait(&acc_full, (uint32_t)t & 1u);
-        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-        double* out = part + (int64_t)seg * kp * kp + row * kp + col0;
-#pragma unroll
-        for (int c0 = 0; c0 < 32; c0 += 16) {
-          double f[16];
-          {
-            uint32_t r[16];
-            tmem_ld16(tmem_d + ((uint32_t)(32 * q) << 16) + (uint32_t)((kNAcc<S> - 1) * QB + 32 * hh + c0), r);
-#pragma unroll
-            for (int jj = 0; jj < 16; ++jj) f[jj] = i2d_exact(r[jj]);
-          }
-#pragma unroll
-          for (int d = kNAcc<S> - 2; d >= 0; --d) {
-            uint32_t r[16];
-            tmem_ld16(tmem_d + ((uint32_t)(32 * q) << 16) + (uint32_t)(d * QB + 32 * hh + c0), r);
-#pragma unroll
-            for (int jj = 0; jj < 16; ++jj) f[jj] = fma(f[jj], 0x1p-8, i2d_exact(r[jj]));
-          }
-#pragma unroll
-          for (int jj = 0; jj < 16; jj += 2) {
-            const int e0 = __shfl_sync(0xffffffffu, ecol, c0 + jj), e1 = __shfl_sync(0xffffffffu, ecol, c0 + jj + 1);
-            if (write)
-              *reinterpret_cast<double2*>(out + c0 + jj) =
-                  make_double2(unscale(f[jj], erow + e0), unscale(f[jj + 1], erow + e1));
-          }
-        }
-        asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&tmem_empty);
-        ++t;
-        my_it += G;
-        continue;
-      }
-      // ---- cut chunk cch of block s_blk[h]: shift, scale by the segment exponent, S int8 digits
-      const int64_t blk = s_blk[h];
-      const int seg = blkseg[blk];
-      const int64_t c = cch * 64 + col;
-      const double sh = c < wd ? shift[c] : 0.0;
-      const unsigned long long mxb = segmax[(int64_t)seg * kp + c];
-      const CutScale cs = cut_scales(seg_exponent(__longlong_as_double((long long)mxb), headroom) + 8 * (S - 1));
-      const bool zero_col = ovf && mxb == 0ull;
-      uint32_t lo[16], hi[16];
-#pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        const bool real = s_src[h][16 * qq + i] >= 0 && c < wd;
-        double z = real ? __dsub_rn(v[i], sh) : v[i];
-        if (cs.pre != 1.0) z = __dmul_rn(z, cs.pre);
-        const double tt = fma(z, cs.sc, Cof);
-        lo[i] = (uint32_t)__double2loint(tt);
-        hi[i] = (uint32_t)__double2hiint(tt);
-        oor |= ((hi[i] ^ 0x43300000u) & kHiMask) | (lo[i] & kLoMask);
-        if (zero_col) oor |= z != 0.0;
-      }
-      const bool last = cch + 1 == nchunk;
-      const int hn = h + 1 == kFusedRing ? 0 : h + 1;
-      // next chunk's loads in flight while this one is transposed and stored
-      if (!last)
-        load_vals(h, cch + 1);
-      else if (s_blk[hn] >= 0)
-        load_vals(hn, 0);
-      // 4 x 4 byte transposes: quad p (rows 16 qq + 4p .. + 3) gives one word per digit
-      uint32_t wd4[S][4];
-#pragma unroll
-      for (int p = 0; p < 4; ++p) {
-        const uint32_t* L = lo + 4 * p;
-        const uint32_t* H = hi + 4 * p;
-        uint32_t wb[8];
-        {
-          const uint32_t x0 = __byte_perm(L[0], L[1], 0x5140), x1 = __byte_perm(L[0], L[1], 0x7362);
-          const uint32_t y0 = __byte_perm(L[2], L[3], 0x5140), y1 = __byte_perm(L[2], L[3], 0x7362);
-          wb[0] = __byte_perm(x0, y0, 0x5410);
-          wb[1] = __byte_perm(x0, y0, 0x7632);
-          wb[2] = __byte_perm(x1, y1, 0x5410);
-          wb[3] = __byte_perm(x1, y1, 0x7632);
-        }
-        if constexpr (S > 4) {
-          const uint32_t x0 = __byte_perm(H[0], H[1], 0x5140), y0 = __byte_perm(H[2], H[3], 0x5140);
-          wb[4] = __byte_perm(x0, y0, 0x5410);
-          wb[5] = __byte_perm(x0, y0, 0x7632);
-        }
-#pragma unroll
-        for (int d = 0; d < S; ++d) wd4[d][p] = wb[S - 1 - d] ^ 0x80808080u;
-      }
-      int8_t* dst = zq + blk * (kp * QK) + c * QK + 16 * qq;
-#pragma unroll
-      for (int d = 0; d < S; ++d)
-        *reinterpret_cast<uint4*>(dst + d * slice) = make_uint4(wd4[d][0], wd4[d][1], wd4[d][2], wd4[d][3]);
-      if (last) {
-        if (__any_sync(0xffffffffu, oor != 0u) && lane == 0) atomicOr(ovf ? ovf + seg : nonfinite, 1);
-        oor = 0;
-        asm volatile("fence.proxy.async.global;\n" ::: "memory");  // these digits will be read by TMA
-        done_seg = seg;
-        claim_buf = h;
-        h = hn;
-        cch = 0;
-      } else {
-        ++cch;
-      }
-    }
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-  __syncthreads();
-  if (warp == 1) {
-    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem_d), "r"(512));
-  }
-}
-
 // 4-D map over Zq: {64 rows, kp, zrows / 64, S} bytes, box {64, box_cols, 1, S}, SWIZZLE_64B.
 inline bool make_zq_map(CUtensorMap* map, const int8_t* zq, int64_t zrows, int64_t kp, int slices, int box_cols,
                         int box_rows = QK) {
@@ -951,17 +610,17 @@ inline bool make_zq_map(CUtensorMap* map, const int8_t* zq, int64_t zrows, int64
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int S, int KS>
+template <int S, int KS, int kMaxSt = 8>
 bool launch_gram_i8_s(const int8_t* zq, const unsigned long long* segmax, int headroom, int64_t zrows, int64_t kp,
                       const GramTask* segs, int64_t nseg, const int2* tiles, int ntiles, double* part, cudaStream_t s) {
   CUtensorMap ma, mb;
   if (!make_zq_map(&ma, zq, zrows, kp, S, QA, KS) || !make_zq_map(&mb, zq, zrows, kp, S, QB, KS)) return false;
-  using C = QCfg<S, KS>;
-  cudaFuncSetAttribute(gram_i8_kernel<S, KS>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
+  using C = QCfg<S, KS, kMaxSt>;
+  cudaFuncSetAttribute(gram_i8_kernel<S, KS, kMaxSt>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
   const int64_t blocks = nseg * (int64_t)ntiles;
   if (blocks > 0)
-    gram_i8_kernel<S, KS><<<(unsigned)blocks, kQThreads, C::kSmem, s>>>(ma, mb, segmax, segs, tiles, ntiles, kp, part,
-                                                                                 headroom);
+    gram_i8_kernel<S, KS, kMaxSt><<<(unsigned)blocks, kQThreads, C::kSmem, s>>>(ma, mb, segmax, segs, tiles, ntiles,
+                                                                                kp, part, headroom);
   return true;
 }
 
@@ -986,30 +645,6 @@ bool launch_k1q(const void* x, int64_t ldx, const void* y, int64_t ldy, int64_t 
   reorder_q_kernel<T, S><<<(unsigned)blocks, kQ1Threads, smem, s>>>(mo, (const T*)x, ldx, (const T*)y, ldy, k, m,
                                                                     src_row, zrows, kp, c_begin, c_end, nsrc, shift,
                                                                     blkseg, segmax, headroom, ovf, nonfinite);
-  return true;
-}
-
-template <typename T, int S>
-bool launch_fused_s(const void* x, int64_t ldx, const void* y, int64_t ldy, int64_t k, int64_t m,
-                    const int64_t* src_row, int64_t zrows, int64_t kp, int64_t nsrc, const double* shift,
-                    const int* blkseg, const unsigned long long* segmax, int headroom, int* ovf, int* nonfinite,
-                    int8_t* zq, const GramTask* segs, int64_t nseg, const int2* tiles, int ntiles, double* part,
-                    unsigned* counters, cudaStream_t s) {
-  CUtensorMap ma, mb;
-  if (!make_zq_map(&ma, zq, zrows, kp, S, QA) || !make_zq_map(&mb, zq, zrows, kp, S, QB)) return false;
-  using C = QCfg<S, QK>;
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaFuncSetAttribute(gram_i8_fused_kernel<T, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
-  }
-  const int64_t nitems = nseg * (int64_t)ntiles;
-  // one CTA per SM: every CTA cuts, so the grid never shrinks below the SM count
-  gram_i8_fused_kernel<T, S><<<(unsigned)sms, kQThreads, C::kSmem, s>>>(
-      ma, mb, (const T*)x, ldx, (const T*)y, ldy, k, m, src_row, zrows, kp, nsrc, shift, blkseg, segmax, headroom, ovf,
-      nonfinite, zq, segs, tiles, ntiles, nitems, part, counters);
   return true;
 }
 
@@ -1076,24 +711,6 @@ bool launch_gram_i8(int slices, const int8_t* zq, const unsigned long long* segm
     default: CVG_GRAM_I8(6);
   }
 #undef CVG_GRAM_I8
-}
-
-bool launch_gram_i8_fused(int dtype, int slices, const void* x, int64_t ldx, const void* y, int64_t ldy, int64_t k,
-                          int64_t m, const int64_t* src_row, int64_t zrows, int64_t kp, int64_t nsrc,
-                          const double* shift, const int* blkseg, const unsigned long long* segmax, int headroom,
-                          int* ovf, int* nonfinite, int8_t* zq, const GramTask* segs, int64_t nseg, const int2* tiles,
-                          int ntiles, double* part, unsigned* counters, cudaStream_t s) {
-  if (zrows <= 0 || nseg <= 0) return true;
-#define CVG_FUSED(T, S)                                                                                          \
-  return launch_fused_s<T, S>(x, ldx, y, ldy, k, m, src_row, zrows, kp, nsrc, shift, blkseg, segmax, headroom, ovf, \
-                              nonfinite, zq, segs, nseg, tiles, ntiles, part, counters, s)
-  if (dtype == 0) {
-    if (slices == 5) CVG_FUSED(double, 5);
-    CVG_FUSED(double, 6);
-  }
-  if (slices == 3) CVG_FUSED(float, 3);
-  CVG_FUSED(float, 4);
-#undef CVG_FUSED
 }
 
 }  // namespace cvg
