@@ -3,6 +3,7 @@
 // include/cvgram_b200.h): per-thread default context, status -> exception
 // translation, and the device-backed core/fast.hpp functions.
 
+#include <cstdlib>
 #include <memory>
 #include <string>
 #include <vector>
@@ -34,7 +35,10 @@ inline void check(int rc, const char* err) {
 }
 
 /// One context per thread (contexts are not internally thread-safe), bound to
-/// device CVG_DEVICE / LOCAL_RANK / 0.
+/// device CVG_DEVICE / LOCAL_RANK / 0 -- or, with CVG_DEVICES="0,1,2,3", to several
+/// devices (cvg_context_create_multi): run_all_folds then shards the folds across
+/// them with the same results, bit for bit (threading.hpp:8-10's n_threads contract,
+/// as GPUs).
 class Context {
  public:
   static cvg_context* get() {
@@ -47,9 +51,23 @@ class Context {
 
  private:
   Context() {
+    char err[512] = {0};
+    if (const char* list = std::getenv("CVG_DEVICES")) {
+      std::vector<int> ids;
+      for (const char* p = list; *p;) {
+        char* end = nullptr;
+        const long v = std::strtol(p, &end, 10);
+        if (end == p) break;
+        ids.push_back(static_cast<int>(v));
+        p = *end == ',' ? end + 1 : end;
+      }
+      if (!ids.empty()) {
+        check(cvg_context_create_multi(static_cast<int>(ids.size()), ids.data(), &h_, err, sizeof err), err);
+        return;
+      }
+    }
     const char* d = std::getenv("CVG_DEVICE");
     if (!d) d = std::getenv("LOCAL_RANK");
-    char err[512] = {0};
     check(cvg_context_create(d ? std::atoi(d) : 0, &h_, err, sizeof err), err);
   }
   cvg_context* h_ = nullptr;

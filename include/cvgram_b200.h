@@ -33,6 +33,7 @@ extern "C" {
 #define CVG_E_INVALID_ARG 4 /* std::invalid_argument (fast.hpp:43,78-79; core.hpp:122,125) */
 #define CVG_E_CUDA 5        /* device missing / kernel or copy failure       */
 #define CVG_E_OOM 6         /* device allocation failure                     */
+#define CVG_E_NCCL 7        /* NCCL unavailable or a collective failed (multi-device contexts) */
 
 #define CVG_DTYPE_F64 0 /* fp64 inputs, fp64 DMMA Gram (BASELINE configs 0,1,2,4) */
 #define CVG_DTYPE_F32 1 /* fp32 inputs (BASELINE config 3)                          */
@@ -51,6 +52,20 @@ int cvg_version(void);
 /* Binds `device` (CUDA ordinal).  Fails with CVG_E_CUDA if it is not sm_100. */
 int cvg_context_create(int device, cvg_context** out, char* err, size_t errlen);
 void cvg_context_destroy(cvg_context* ctx);
+/* A context over n_gpus devices of this node (the reference's run_all_folds(..., n_threads) knob,
+ * threading.hpp:12-26, as GPUs).  cvg_run_all_folds on it shards the folds across the devices: each rank owns
+ * a node of the canonical fold tree (cvg_fold_range), copies only its row shard over its own PCIe link when
+ * p >= n_gpus (rows then move to their fold's owner over NVLink), and the ranks exchange one partial Gram
+ * (all-gather); outputs are bit-identical to one device for power-of-two n_gpus.  One host thread per device;
+ * the exchanges use NCCL (loaded at run time; CVG_E_NCCL if it cannot be) over distinct devices, or device
+ * copies when dev_ids repeats a device (a one-GPU emulation) or CVG_EXCHANGE=peer.  A run whose folds all hold
+ * <= 32 rows (leave-one-out scale) stays on dev_ids[0]: one device forms such folds' Grams in its epilogue, a
+ * summation order rank plans do not share.  Every other entry point runs on dev_ids[0]. */
+int cvg_context_create_multi(int n_gpus, const int* dev_ids, cvg_context** out, char* err, size_t errlen);
+/* Devices of a context (1 for cvg_context_create). */
+int cvg_context_device_count(const cvg_context* ctx);
+/* Exchange backend of a multi-device context: 1 NCCL, 2 device copies, 0 single device. */
+int cvg_context_exchange(const cvg_context* ctx);
 /* Subsequent work is issued on `stream` (a cudaStream_t; NULL = the context's
  * own non-blocking stream; cudaStreamLegacy = the legacy default stream). */
 int cvg_context_set_stream(cvg_context* ctx, void* stream);

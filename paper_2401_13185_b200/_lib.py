@@ -16,7 +16,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _VARIANT = os.environ.get("CVG_LIB_VARIANT", "")
 LIB_PATH = os.path.join(_HERE, f"_build_{_VARIANT}" if _VARIANT else "_build", "libcvgram_b200.so")
 
-OK, E_DIMENSION, E_PARTITION, E_SCALABILITY, E_INVALID_ARG, E_CUDA, E_OOM = 0, 1, 2, 3, 4, 5, 6
+OK, E_DIMENSION, E_PARTITION, E_SCALABILITY, E_INVALID_ARG, E_CUDA, E_OOM, E_NCCL = 0, 1, 2, 3, 4, 5, 6, 7
 DTYPE_F64, DTYPE_F32 = 0, 1
 
 c_i64, c_i32, c_u32, c_u64 = ctypes.c_int64, ctypes.c_int32, ctypes.c_uint32, ctypes.c_uint64
@@ -74,6 +74,9 @@ SIGNATURES = {
     "cvg_hadamard_outer_divide": (c_int, [c_vp, c_vp, c_i64, c_i64, c_vp, c_i64, c_vp, c_i64, c_vp, c_char_p,
                                           c_size_t]),
     "cvg_selftest_division": (c_int, [c_vp, c_i64, c_u64, c_vp, c_vp]),
+    "cvg_context_create_multi": (c_int, [c_int, c_vp, c_vp, c_char_p, c_size_t]),
+    "cvg_context_device_count": (c_int, [c_vp]),
+    "cvg_context_exchange": (c_int, [c_vp]),
 }
 
 _lib = None

@@ -15,6 +15,7 @@
 
 #include "../../include/cvgram_b200.h"
 #include "engine.cuh"
+#include "multi.cuh"
 
 using cvg::Status;
 
@@ -204,8 +205,38 @@ int cvg_context_create(int device, cvg_context** out, char* err, size_t errlen) 
   });
 }
 
+int cvg_context_create_multi(int n_gpus, const int* dev_ids, cvg_context** out, char* err, size_t errlen) {
+  return guarded(err, errlen, [&]() -> Status {
+    if (!out) return Status::Err(CVG_E_INVALID_ARG, "null output pointer");
+    *out = nullptr;
+    if (n_gpus < 1 || !dev_ids) return Status::Err(CVG_E_INVALID_ARG, "need at least one device id");
+    cvg_context* ctx = nullptr;
+    char e2[256] = {0};
+    const int rc = cvg_context_create(dev_ids[0], &ctx, e2, sizeof e2);
+    if (rc != CVG_OK) return Status::Err(rc, e2);
+    Status s = cvg::multi_init(ctx, dev_ids, n_gpus);
+    if (!s.ok()) {
+      cvg_context_destroy(ctx);
+      return s;
+    }
+    *out = ctx;
+    return Status::Ok();
+  });
+}
+
+int cvg_context_device_count(const cvg_context* ctx) {
+  if (!ctx) return 0;
+  return ctx->ranks.empty() ? 1 : (int)ctx->ranks.size();
+}
+
+int cvg_context_exchange(const cvg_context* ctx) {
+  if (!ctx || ctx->ranks.empty()) return 0;
+  return ctx->nccl ? 1 : 2;
+}
+
 void cvg_context_destroy(cvg_context* ctx) {
   if (!ctx) return;
+  cvg::multi_destroy(ctx);
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
   ctx->clear_recs();
@@ -224,7 +255,12 @@ int cvg_context_set_stream(cvg_context* ctx, void* stream) {
   return CVG_OK;
 }
 
-int64_t cvg_context_launch_count(const cvg_context* ctx) { return ctx ? ctx->launches : 0; }
+int64_t cvg_context_launch_count(const cvg_context* ctx) {
+  if (!ctx) return 0;
+  int64_t n = ctx->launches;
+  for (const cvg_context* r : ctx->ranks) n += r->launches;
+  return n;
+}
 
 int cvg_context_enable_timing(cvg_context* ctx, int enable) {
   if (!ctx) return CVG_E_INVALID_ARG;
@@ -316,6 +352,19 @@ int cvg_run_all_folds(cvg_context* ctx, int dtype, const void* x, const void* y,
     if (scal) {
       s = check_scalable(counts, n);
       if (!s.ok()) return s;
+    }
+    // several devices (cvg_context_create_multi) -- except when every fold is tiny (<= 32 rows, e.g. leave-one-out):
+    // one device's small-fold mode forms the fold Grams in the epilogue, a summation order rank plans do not share,
+    // so such runs stay on the first device and keep returning one device's bits
+    if (!ctx->ranks.empty() && !cvg::Plan::small_fold_mode(dtype, counts)) {
+      s = cvg::run_all_folds_multi(ctx, dtype, x, y, n, k, m, labels, p, cfg_masks, n_cfg, counts, scal, xtx, xty,
+                                   mean_x, mean_y, std_x, std_y);
+      if (!s.ok()) return s;
+      for (int32_t f = 0; f < p; ++f) {
+        if (n_train) n_train[f] = n - counts[f];
+        if (n_val) n_val[f] = counts[f];
+      }
+      return Status::Ok();
     }
     s = cvg::cuda_status(cudaSetDevice(ctx->device), "cudaSetDevice");
     if (!s.ok()) return s;

@@ -520,6 +520,13 @@ Status Plan::bind_labels(const int32_t* d_labels, bool validate, bool require_sc
 }
 
 // CVG_SMALL_FOLDS=0 keeps per-fold Gram partials even when every fold is tiny (A/B tests).
+bool Plan::small_fold_mode(int dtype, const std::vector<int64_t>& counts) {
+  if (dtype != 0 || !small_folds_enabled()) return false;
+  int64_t mx = 0;
+  for (int64_t c : counts) mx = std::max(mx, c);
+  return mx <= kSmallFoldRows;
+}
+
 bool Plan::small_folds_enabled() {
   static const bool on = [] {
     const char* v = std::getenv("CVG_SMALL_FOLDS");

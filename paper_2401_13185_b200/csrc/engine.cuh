@@ -144,6 +144,13 @@ class Plan {
   Status i8_gram(const int2* tiles, int ntiles);
   Status i8_exact_pass(const void* d_x, int64_t ldx, const void* d_y, int64_t ldy, const int64_t* rows, int64_t nsrc);
   static bool small_folds_enabled();
+
+ public:
+  // A single full-range plan over these fold sizes runs small-fold mode (a different fixed summation order than
+  // rank-mode plans, which keep per-fold partials).
+  static bool small_fold_mode(int dtype, const std::vector<int64_t>& counts);
+
+ private:
   SmallFolds small_folds() const {
     SmallFolds sf;
     if (small_) {
@@ -218,6 +225,11 @@ struct cvg_context {
   cudaStream_t stream = nullptr;
   int64_t launches = 0;
   std::unique_ptr<cvg::HostScratch> scratch;
+  // cvg_context_create_multi: one sub-context per rank (device) and, for distinct devices, one NCCL
+  // communicator per rank (multi.cu); empty for a single-device context
+  std::vector<cvg_context*> ranks;
+  std::vector<void*> comms;  // ncclComm_t
+  bool nccl = false;
   // optional per-class kernel timing (cvg_context_enable_timing)
   bool timing = false;
   struct Rec {

@@ -32,6 +32,7 @@
 //               pair (t, u) into accumulator t + u (S x 64 int32 TMEM columns); the pairs of
 //               one A slice with adjacent B slices are one MMA of N = 64 .. 256
 //   warps 2..9  drain once per tile: Horner over the S accumulators, exact unscale
+#include <atomic>
 #include <cstdlib>
 
 #include "cvg_internal.cuh"
@@ -632,16 +633,21 @@ bool launch_k1q(const void* x, int64_t ldx, const void* y, int64_t ldy, int64_t 
   CUtensorMap mo;
   if (!make_zq_map(&mo, zq, zrows, kp, S, 64)) return false;
   constexpr int smem = k1q_smem_bytes<S>();
-  static int per_sm = 0, sms = 0;  // grid-stride over one wave of resident CTAs
-  if (!per_sm) {
-    int dev = 0;
-    cudaGetDevice(&dev);
+  // grid-stride over one wave of resident CTAs.  Function attributes are per device (one process may drive
+  // several: cvg_context_create_multi), so they are set on every launch; the occupancy query is cached per device.
+  static std::atomic<int> wave_cache[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaFuncSetAttribute(reorder_q_kernel<T, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  int wave = wave_cache[dev & 63].load(std::memory_order_relaxed);
+  if (!wave) {
+    int sms = 0, per_sm = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaFuncSetAttribute(reorder_q_kernel<T, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, reorder_q_kernel<T, S>, kQ1Threads, smem);
-    per_sm = per_sm > 0 ? per_sm : 1;
+    wave = (per_sm > 0 ? per_sm : 1) * sms;
+    wave_cache[dev & 63].store(wave, std::memory_order_relaxed);
   }
-  const int64_t blocks = std::min<int64_t>(zrows / QK, (int64_t)per_sm * sms);
+  const int64_t blocks = std::min<int64_t>(zrows / QK, (int64_t)wave);
   reorder_q_kernel<T, S><<<(unsigned)blocks, kQ1Threads, smem, s>>>(mo, (const T*)x, ldx, (const T*)y, ldy, k, m,
                                                                     src_row, zrows, kp, c_begin, c_end, nsrc, shift,
                                                                     blkseg, segmax, headroom, ovf, nonfinite);

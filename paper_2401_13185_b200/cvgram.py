@@ -45,7 +45,7 @@ class DeviceError(RuntimeError):
 
 
 _ERRORS = {L.E_DIMENSION: DimensionError, L.E_PARTITION: PartitionError, L.E_SCALABILITY: ScalabilityError,
-           L.E_INVALID_ARG: InvalidArgument, L.E_CUDA: DeviceError, L.E_OOM: DeviceError}
+           L.E_INVALID_ARG: InvalidArgument, L.E_CUDA: DeviceError, L.E_OOM: DeviceError, L.E_NCCL: DeviceError}
 
 
 def _check(rc: int, buf) -> None:
@@ -89,6 +89,30 @@ class Context:
 
     def close(self) -> None:
         self._fin()
+
+
+class MultiContext(Context):
+    """Several devices behind one context (cvg_context_create_multi): run_all_folds on it shards the folds
+    across the devices (per-device host threads; NCCL exchanges over distinct devices, device copies when a
+    device repeats -- a one-GPU emulation), bit-identical to one device.  Other calls run on devices[0]."""
+
+    def __init__(self, devices):
+        self.devices = [int(d) for d in devices]
+        self.device = self.devices[0]
+        ids = (ctypes.c_int * len(self.devices))(*self.devices)
+        h = ctypes.c_void_p()
+        buf = L.err_buf()
+        _check(L.lib().cvg_context_create_multi(len(self.devices), ids, ctypes.byref(h), buf, len(buf)), buf)
+        self._h = h
+        self._fin = weakref.finalize(self, L.lib().cvg_context_destroy, h)
+
+    @property
+    def device_count(self) -> int:
+        return int(L.lib().cvg_context_device_count(self._h))
+
+    @property
+    def exchange(self) -> str:
+        return {1: "nccl", 2: "copy"}.get(int(L.lib().cvg_context_exchange(self._h)), "single")
 
 
 CUDA_STREAM_LEGACY = 1  # cudaStreamLegacy

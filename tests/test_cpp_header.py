@@ -25,3 +25,14 @@ def test_cpp_header_all_cases_on_device():
     r = _run()
     assert r.returncode == 0, r.stdout + r.stderr
     assert "0 failing tests" in r.stdout
+
+
+@pytest.mark.gpu
+def test_cpp_header_all_cases_on_a_multi_device_context():
+    """The same C++ cases with CVG_DEVICES naming a repeated device: every cvgram::run_all_folds call goes
+    through cvg_context_create_multi's sharded path (rank plans on host threads, device-copy exchanges)."""
+    env = dict(os.environ, CVG_DEVICES="0,0")
+    r = subprocess.run([BIN], capture_output=True, text=True, timeout=600, env=env)
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "0 failing tests" in r.stdout

@@ -221,3 +221,55 @@ def test_shard_rows_partition():
             spans = [P.shard_rows(n, r, world) for r in range(world)]
             assert spans[0][0] == 0 and spans[-1][1] == n
             assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
+
+
+# ------------------------------------------------------------ the real CUDA rank plans, world 2 on one GPU
+def _worker_cuda(rank, world, port, outdir, data):
+    """A real DevicePlan per process (all on cuda:0); the partial Gram exchanged through host gloo -- no kernel
+    waits on another process's kernel."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2401_13185_b200 import plan as P
+
+    x, y, labels, p = data
+    dev = torch.device("cuda", 0)
+    pl = P.DevicePlan(x.shape[0], x.shape[1], y.shape[1], p, rank=rank, world=world)
+    pl.bind_labels(torch.from_numpy(labels).to(dev), True)
+    pl.gram(torch.from_numpy(x).to(dev), torch.from_numpy(y).to(dev))
+    mine = torch.empty(pl.partial_count, dtype=torch.float64, device=dev)
+    pl.partial_into(mine)
+    parts = [torch.empty(pl.partial_count, dtype=torch.float64) for _ in range(world)]
+    dist.all_gather(parts, mine.cpu())
+    out = pl.finish([15, 0], torch.cat(parts).to(dev), world)
+    np.savez(os.path.join(outdir, f"rank{rank}.npz"), fb=pl.fold_begin, fe=pl.fold_end,
+             xtx=out["xtx"].cpu().numpy(), xty=out["xty"].cpu().numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 4])
+def test_cuda_rank_plans_over_gloo_match_single_gpu_bitwise(world):
+    from paper_2401_13185_b200 import plan as P
+
+    rng = np.random.default_rng(5)
+    n, k, m, p = 30000, 70, 5, 6
+    x = rng.normal(rng.uniform(-5, 5, k), rng.uniform(0.5, 2, k), (n, k))
+    y = rng.normal(1, 1, (n, m))
+    labels = (rng.permutation(n) % p + 1).astype(np.int32)
+    dev = torch.device("cuda", 0)
+    one = P.DevicePlan(n, k, m, p)
+    one.bind_labels(torch.from_numpy(labels).to(dev), True)
+    one.gram(torch.from_numpy(x).to(dev), torch.from_numpy(y).to(dev))
+    ref = one.finish([15, 0])
+    rxx, rxy = ref["xtx"].cpu().numpy(), ref["xty"].cpu().numpy()
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_worker_cuda, args=(world, _free_port(), d, (x, y, labels, p)), nprocs=world, join=True)
+        covered = []
+        for r in range(world):
+            q = np.load(os.path.join(d, f"rank{r}.npz"))
+            fb, fe = int(q["fb"]), int(q["fe"])
+            covered += list(range(fb, fe))
+            assert np.array_equal(q["xtx"], rxx[:, fb:fe]) and np.array_equal(q["xty"], rxy[:, fb:fe])
+        assert sorted(covered) == list(range(p))
