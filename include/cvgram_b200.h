@@ -244,6 +244,13 @@ int cvg_hadamard_outer_divide(cvg_context* ctx, const double* mat, int64_t rows,
                               int64_t n_left, const double* right, int64_t n_right, double* out, char* err,
                               size_t errlen);
 
+/* ------------------------------------------------- pinned host output buffers */
+/* Page-locked host memory from a process-wide pool (64 KB granularity): output arrays allocated here receive
+ * cvg_run_all_folds' device-to-host copies at full PCIe speed, and a freed block is reused by the next
+ * allocation of a similar size (no cudaHostAlloc, no first-touch page faults).  CVG_E_OOM if no block. */
+int cvg_host_alloc(size_t bytes, void** out);
+void cvg_host_free(void* p);
+
 /* ------------------------------------------------------------- self-tests */
 /* The epilogue's branch-free fp64 division (the scaled outputs' one division by the product,
  * core.hpp:128) against the hardware-correct div.rn.f64 over n hashed operand pairs (NaN/inf/subnormal

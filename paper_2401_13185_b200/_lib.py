@@ -77,6 +77,8 @@ SIGNATURES = {
     "cvg_context_create_multi": (c_int, [c_int, c_vp, c_vp, c_char_p, c_size_t]),
     "cvg_context_device_count": (c_int, [c_vp]),
     "cvg_context_exchange": (c_int, [c_vp]),
+    "cvg_host_alloc": (c_int, [c_size_t, c_vp]),
+    "cvg_host_free": (None, [c_vp]),
 }
 
 _lib = None

@@ -215,6 +215,13 @@ class Plan {
 struct HostScratch {
   DevBuf x, y, labels, xtx, xty, mx, my, sx, sy;
   Plan plan;
+  void* stage = nullptr;  // 2 x 32 MB pinned staging for large D2H into pageable memory (capi.cu d2h_large)
+  cudaEvent_t stage_ev[2] = {nullptr, nullptr};
+  ~HostScratch() {
+    if (stage) cudaFreeHost(stage);
+    for (cudaEvent_t e : stage_ev)
+      if (e) cudaEventDestroy(e);
+  }
 };
 
 }  // namespace cvg

@@ -202,31 +202,28 @@ __device__ __forceinline__ double unscale(double f, int E) {
 
 // tiles[i] = {I, J | wmask << 16}: rows 128I .. +128 (Z columns), columns 64J .. +64; wmask bit h:
 // the 64 x 64 sub-tile of rows 128I + 64h is needed downstream (an upper 64-tile of the plan).
+//
+// Persistent: one CTA per SM walks the (segment, tile) items round-robin (item = blockIdx.x + i gridDim.x,
+// segment-major, so the CTAs running at once share a segment's digits in L2).  The TMA ring runs on across
+// items -- the next item's first stages load while this one drains -- and TMEM is allocated once; the MMA warp
+// starts an item once the drain warps have read the previous item's accumulators (tmem_empty).  A launch per
+// item paid its TMEM allocation, barrier setup and pipeline fill every time: ~9 us per item, which dominated
+// short folds (the paper's P = 1000 at N = 1e5: 20,000 items of 2 K-steps).
 template <int S, int KS, int kMaxSt = 8>
 __global__ void __launch_bounds__(kQThreads, 1)
     gram_i8_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                    const unsigned long long* __restrict__ segmax, const GramTask* __restrict__ segs,
-                   const int2* __restrict__ tiles,
-                   int ntiles, int64_t kp, double* __restrict__ part, int headroom) {
+                   const int2* __restrict__ tiles, int ntiles, int64_t nitems, int64_t kp, double* __restrict__ part,
+                   int headroom) {
   using C = QCfg<S, KS, kMaxSt>;
   constexpr int NST = C::kNst;
   constexpr int kPer = QK / KS;  // stages per 64-row block
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  __shared__ __align__(8) uint64_t full_bar[NST], empty_bar[NST], acc_full;
+  __shared__ __align__(8) uint64_t full_bar[NST], empty_bar[NST], acc_full, tmem_empty;
   __shared__ uint32_t tmem_base;
-
-  const int seg = blockIdx.x / ntiles;
-  const int2 tile0 = tiles[blockIdx.x - seg * ntiles];
-  const int ti = uniform(tile0.x), tj = uniform(tile0.y & 0xffff), wmask = uniform(tile0.y >> 16);
-  // B is always loaded into its own stage slices (even when it lies inside A's 128 columns): the
-  // merged-N MMAs need the S B slices side by side
-  const GramTask task0 = segs[seg];
-  const GramTask task{uniform(task0.zrow), uniform(task0.rows)};
-  CVG_DCHECK(task.zrow % QK == 0 && task.rows % QK == 0 && task.rows > 0);
-  CVG_DCHECK(ti >= 0 && 2 * ti <= tj && (int64_t)tj * QB < kp);
-  const int nsteps = (int)(task.rows / KS);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t G = gridDim.x;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < NST; ++s) {
@@ -234,6 +231,7 @@ __global__ void __launch_bounds__(kQThreads, 1)
       mbar_init(&empty_bar[s], 1);
     }
     mbar_init(&acc_full, 1);
+    mbar_init(&tmem_empty, kQEpiWarps);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   if (warp == 1) {
@@ -248,77 +246,118 @@ __global__ void __launch_bounds__(kQThreads, 1)
 
   auto opA = [&](int s) { return smem + s * C::kStage; };
   auto opB = [&](int s) { return smem + s * C::kStage + S * C::kA; };
+  // item -> (segment, tile)
+  auto item = [&](int64_t it, int& seg, int& ti, int& tj, int& wmask, GramTask& task) {
+    seg = (int)(it / ntiles);
+    const int2 tile0 = tiles[it - (int64_t)seg * ntiles];
+    ti = uniform(tile0.x);
+    tj = uniform(tile0.y & 0xffff);
+    wmask = uniform(tile0.y >> 16);
+    const GramTask task0 = segs[seg];
+    task = GramTask{uniform(task0.zrow), uniform(task0.rows)};
+    CVG_DCHECK(task.zrow % QK == 0 && task.rows % QK == 0 && task.rows > 0);
+    CVG_DCHECK(ti >= 0 && 2 * ti <= tj && (int64_t)tj * QB < kp);
+  };
 
   if (warp == 0) {  // ---- TMA producer (whole warp waits; one elected lane issues)
     const uint32_t bytes = (uint32_t)(S * (C::kA + C::kB));
-    for (int it = 0; it < nsteps; ++it) {
-      const int s = it % NST;
-      mbar_wait(&empty_bar[s], ((uint32_t)(it / NST) & 1u) ^ 1u);
-      const int blk = (int)(task.zrow / QK) + it / kPer, r0 = (it % kPer) * KS;
-      if (elect_one()) {
-        mbar_expect_tx(&full_bar[s], bytes);
-        tma_load_4d(opA(s), &map_a, &full_bar[s], r0, ti * QA, blk, 0);
-        tma_load_4d(opB(s), &map_b, &full_bar[s], r0, tj * QB, blk, 0);
+    int64_t g = 0;  // stage-ring position, continuous across items
+    for (int64_t it = blockIdx.x; it < nitems; it += G) {
+      int seg, ti, tj, wmask;
+      GramTask task;
+      item(it, seg, ti, tj, wmask, task);
+      const int nsteps = (int)(task.rows / KS);
+      for (int st = 0; st < nsteps; ++st, ++g) {
+        const int s = (int)(g % NST);
+        mbar_wait(&empty_bar[s], ((uint32_t)(g / NST) & 1u) ^ 1u);
+        const int blk = (int)(task.zrow / QK) + st / kPer, r0 = (st % kPer) * KS;
+        if (elect_one()) {
+          mbar_expect_tx(&full_bar[s], bytes);
+          tma_load_4d(opA(s), &map_a, &full_bar[s], r0, ti * QA, blk, 0);
+          tma_load_4d(opB(s), &map_b, &full_bar[s], r0, tj * QB, blk, 0);
+        }
+        __syncwarp();
       }
-      __syncwarp();
     }
   } else if (warp == 1) {  // ---- MMA issuer
-    for (int it = 0; it < nsteps; ++it) {
-      const int s = it % NST;
-      mbar_wait(&full_bar[s], (uint32_t)(it / NST) & 1u);
-      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-      const uint64_t a0 = kmajor_sw_desc<KS>(opA(s));
-      const uint64_t b0 = kmajor_sw_desc<KS>(opB(s));
-      const uint64_t a_step = (uint64_t)(C::kA >> 4), b_step = (uint64_t)(C::kB >> 4);
-      if (elect_one()) {
-#pragma unroll
-        for (int k = 0; k < KS / 32; ++k)  // K = 32 int8 = 32 B per MMA: +2 in 16-byte descriptor units
-          mma_slices<S, 0>(tmem_d, a0 + 2ull * k, a_step, b0 + 2ull * k, b_step, it == 0 && k == 0);
-        mma_commit(&empty_bar[s]);  // frees the stage once these MMAs have read it
-        if (it == nsteps - 1) mma_commit(&acc_full);
+    int64_t g = 0;
+    int t = 0;  // items of this CTA
+    for (int64_t it = blockIdx.x; it < nitems; it += G, ++t) {
+      int seg, ti, tj, wmask;
+      GramTask task;
+      item(it, seg, ti, tj, wmask, task);
+      const int nsteps = (int)(task.rows / KS);
+      if (t > 0) {  // the drain warps have read the previous item's accumulators
+        mbar_wait(&tmem_empty, (uint32_t)(t - 1) & 1u);
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
       }
-      __syncwarp();
+      for (int st = 0; st < nsteps; ++st, ++g) {
+        const int s = (int)(g % NST);
+        mbar_wait(&full_bar[s], (uint32_t)(g / NST) & 1u);
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+        const uint64_t a0 = kmajor_sw_desc<KS>(opA(s));
+        const uint64_t b0 = kmajor_sw_desc<KS>(opB(s));
+        const uint64_t a_step = (uint64_t)(C::kA >> 4), b_step = (uint64_t)(C::kB >> 4);
+        if (elect_one()) {
+#pragma unroll
+          for (int k = 0; k < KS / 32; ++k)  // K = 32 int8 = 32 B per MMA: +2 in 16-byte descriptor units
+            mma_slices<S, 0>(tmem_d, a0 + 2ull * k, a_step, b0 + 2ull * k, b_step, st == 0 && k == 0);
+          mma_commit(&empty_bar[s]);  // frees the stage once these MMAs have read it
+          if (st == nsteps - 1) mma_commit(&acc_full);
+        }
+        __syncwarp();
+      }
     }
   } else {  // ---- drain: Horner over the diagonal accumulators, exact unscale, fp64 partial
     const int dw = warp - 2;
     const int q = warp & 3;  // TMEM lanes [32q, 32q + 32) (hardware: warp id mod 4)
     const int h = dw >> 2;   // columns [32h, 32h + 32) of the 64-wide tile
-    const int64_t row = (int64_t)ti * QA + 32 * q + lane;  // this thread's Gram row (a Z column)
-    const int64_t col0 = (int64_t)tj * QB + 32 * h;
-    const bool write = row < kp && ((wmask >> (q >> 1)) & 1);
-    const unsigned long long* mx = segmax + (int64_t)seg * kp;
-    const int erow = seg_exponent(__longlong_as_double((long long)mx[row < kp ? row : 0]), headroom);
-    const int ecol = seg_exponent(__longlong_as_double((long long)mx[col0 + lane]), headroom);  // lane j: column col0 + j
-    mbar_wait(&acc_full, 0);
-    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-    double* out = part + (int64_t)seg * kp * kp + row * kp + col0;
+    int t = 0;
+    for (int64_t it = blockIdx.x; it < nitems; it += G, ++t) {
+      int seg, ti, tj, wmask;
+      GramTask task;
+      item(it, seg, ti, tj, wmask, task);
+      const int64_t row = (int64_t)ti * QA + 32 * q + lane;  // this thread's Gram row (a Z column)
+      const int64_t col0 = (int64_t)tj * QB + 32 * h;
+      const bool write = row < kp && ((wmask >> (q >> 1)) & 1);
+      const unsigned long long* mx = segmax + (int64_t)seg * kp;
+      const int erow = seg_exponent(__longlong_as_double((long long)mx[row < kp ? row : 0]), headroom);
+      const int ecol = seg_exponent(__longlong_as_double((long long)mx[col0 + lane]), headroom);  // lane j: column col0 + j
+      mbar_wait(&acc_full, (uint32_t)t & 1u);
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+      double* out = part + (int64_t)seg * kp * kp + row * kp + col0;
 #pragma unroll
-    for (int c0 = 0; c0 < 32; c0 += 16) {
-      double f[16];
-      {
-        uint32_t r[16];
-        tmem_ld16(tmem_d + ((uint32_t)(32 * q) << 16) + (uint32_t)((kNAcc<S> - 1) * QB + 32 * h + c0), r);
+      for (int c0 = 0; c0 < 32; c0 += 16) {
+        // all accumulators' 16 columns in one batch of TMEM loads (one wait: the item's MMAs restart sooner)
+        uint32_t r[kNAcc<S>][16];
 #pragma unroll
-        for (int j = 0; j < 16; ++j) f[j] = i2d_exact(r[j]);
-      }
+        for (int d = 0; d < kNAcc<S>; ++d)
+          tmem_ld16_nowait(tmem_d + ((uint32_t)(32 * q) << 16) + (uint32_t)(d * QB + 32 * h + c0), r[d]);
+        tmem_ld_wait();
+        double f[16];
 #pragma unroll
-      for (int d = kNAcc<S> - 2; d >= 0; --d) {
-        uint32_t r[16];
-        tmem_ld16(tmem_d + ((uint32_t)(32 * q) << 16) + (uint32_t)(d * QB + 32 * h + c0), r);
+        for (int j = 0; j < 16; ++j) f[j] = i2d_exact(r[kNAcc<S> - 1][j]);
 #pragma unroll
-        for (int j = 0; j < 16; ++j) f[j] = fma(f[j], 0x1p-8, i2d_exact(r[j]));  // f * 2^-8 exact
-      }
-      if (write) {
+        for (int d = kNAcc<S> - 2; d >= 0; --d)
 #pragma unroll
-        for (int j = 0; j < 16; j += 2) {
-          const int e0 = __shfl_sync(0xffffffffu, ecol, c0 + j), e1 = __shfl_sync(0xffffffffu, ecol, c0 + j + 1);
-          *reinterpret_cast<double2*>(out + c0 + j) = make_double2(unscale(f[j], erow + e0), unscale(f[j + 1], erow + e1));
+          for (int j = 0; j < 16; ++j) f[j] = fma(f[j], 0x1p-8, i2d_exact(r[d][j]));  // f * 2^-8 exact
+        if (c0 == 16) {  // every accumulator column of this thread has been read: the MMA warp may go on
+          asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tmem_empty);
         }
-      } else {
+        if (write) {
 #pragma unroll
-        for (int j = 0; j < 16; j += 2) {  // keep the shuffles converged
-          __shfl_sync(0xffffffffu, ecol, c0 + j);
-          __shfl_sync(0xffffffffu, ecol, c0 + j + 1);
+          for (int j = 0; j < 16; j += 2) {
+            const int e0 = __shfl_sync(0xffffffffu, ecol, c0 + j), e1 = __shfl_sync(0xffffffffu, ecol, c0 + j + 1);
+            *reinterpret_cast<double2*>(out + c0 + j) = make_double2(unscale(f[j], erow + e0), unscale(f[j + 1], erow + e1));
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 16; j += 2) {  // keep the shuffles converged
+            __shfl_sync(0xffffffffu, ecol, c0 + j);
+            __shfl_sync(0xffffffffu, ecol, c0 + j + 1);
+          }
         }
       }
     }
@@ -618,10 +657,14 @@ bool launch_gram_i8_s(const int8_t* zq, const unsigned long long* segmax, int he
   if (!make_zq_map(&ma, zq, zrows, kp, S, QA, KS) || !make_zq_map(&mb, zq, zrows, kp, S, QB, KS)) return false;
   using C = QCfg<S, KS, kMaxSt>;
   cudaFuncSetAttribute(gram_i8_kernel<S, KS, kMaxSt>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
-  const int64_t blocks = nseg * (int64_t)ntiles;
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t nitems = nseg * (int64_t)ntiles;
+  const int64_t blocks = std::min<int64_t>(nitems, sms);  // persistent: one CTA per SM (1 fits: shared memory)
   if (blocks > 0)
     gram_i8_kernel<S, KS, kMaxSt><<<(unsigned)blocks, kQThreads, C::kSmem, s>>>(ma, mb, segmax, segs, tiles, ntiles,
-                                                                                kp, part, headroom);
+                                                                                nitems, kp, part, headroom);
   return true;
 }
 

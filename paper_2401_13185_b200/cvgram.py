@@ -240,6 +240,28 @@ def _empty():
     return np.empty(0)
 
 
+_EMPTY = np.empty(0)
+_EMPTY.flags.writeable = False  # the shared "not filled" statistic (FoldStats fill rules, core.hpp:95-105)
+_PINNED_MIN_BYTES = 1 << 22
+
+
+def _output_array(shape, dtype=np.float64):
+    """An output array for the engine's device-to-host copies: large ones come from the library's pinned host
+    pool (cvg_host_alloc; the block returns to the pool when the array -- and every view of it -- is gone), so
+    results land at full PCIe speed in already-faulted pages; small ones, or no pool, are plain np.empty."""
+    shape = tuple(int(d) for d in shape)
+    nbytes = int(np.prod(shape, dtype=np.int64)) * np.dtype(dtype).itemsize
+    if nbytes < _PINNED_MIN_BYTES:
+        return np.empty(shape, dtype)
+    p = ctypes.c_void_p()
+    if L.lib().cvg_host_alloc(nbytes, ctypes.byref(p)) != L.OK or not p.value:
+        return np.empty(shape, dtype)
+    raw = (ctypes.c_char * nbytes).from_address(p.value)
+    arr = np.frombuffer(raw, dtype=dtype).reshape(shape)
+    weakref.finalize(raw, L.lib().cvg_host_free, ctypes.c_void_p(p.value))
+    return arr
+
+
 @dataclass
 class GlobalCache:
     """Whole-dataset aggregates (core.hpp:83-93); unused vectors stay empty."""
@@ -453,27 +475,25 @@ def run_all_folds_configs(data: DatasetPair, part: Partitioning, cfgs, ctx: Opti
     nc = len(cfgs)
     pp = max(p, 0)
     masks = np.array([c.mask for c in cfgs], np.uint32)
-    xtx = np.empty((nc, pp, k, k))
-    xty = np.empty((nc, pp, k, m))
-    mx, my = np.empty((nc, pp, k)), np.empty((nc, pp, m))
-    sx, sy = np.empty((nc, pp, k)), np.empty((nc, pp, m))
+    xtx = _output_array((nc, pp, k, k))
+    xty = _output_array((nc, pp, k, m))
+    mx, my = _output_array((nc, pp, k)), _output_array((nc, pp, m))
+    sx, sy = _output_array((nc, pp, k)), _output_array((nc, pp, m))
     nt, nv = np.empty(pp, np.int64), np.empty(pp, np.int64)
     buf = L.err_buf()
     _check(L.lib().cvg_run_all_folds(ctx.handle, data.dtype_code, _ptr(data.x()), _ptr(data.y()), n, k, m,
                                      _ptr(part.labels), part.labels.size, p, _ptr(masks), nc, _ptr(xtx), _ptr(xty),
                                      _ptr(mx), _ptr(my), _ptr(sx), _ptr(sy), _ptr(nt), _ptr(nv), buf, len(buf)), buf)
     out = []
+    ntl, nvl = nt.tolist(), nv.tolist()
     for ci, cfg in enumerate(cfgs):
+        anyc, scx, scy = cfg.any(), cfg.scale_x, cfg.scale_y
+        xs, ys, mxs, mys, sxs, sys_ = xtx[ci], xty[ci], mx[ci], my[ci], sx[ci], sy[ci]
         runs = []
         for f in range(p):
-            st = FoldStats(n_train=int(nt[f]), n_val=int(nv[f]))
-            if cfg.any():
-                st.mean_x_t, st.mean_y_t = mx[ci, f], my[ci, f]
-            if cfg.scale_x:
-                st.std_x_t = sx[ci, f]
-            if cfg.scale_y:
-                st.std_y_t = sy[ci, f]
-            runs.append(FoldResult(f + 1, xtx[ci, f], xty[ci, f], st))
+            st = FoldStats(mxs[f] if anyc else _EMPTY, mys[f] if anyc else _EMPTY, sxs[f] if scx else _EMPTY,
+                           sys_[f] if scy else _EMPTY, ntl[f], nvl[f])
+            runs.append(FoldResult(f + 1, xs[f], ys[f], st))
         out.append(runs)
     return out
 
@@ -604,17 +624,15 @@ def baseline_fold_products_configs(data: DatasetPair, part: Partitioning, cfgs, 
                                               _ptr(xty), _ptr(mx), _ptr(my), _ptr(sx), _ptr(sy), _ptr(nt), _ptr(nv),
                                               buf, len(buf)), buf)
     out = []
+    ntl, nvl = nt.tolist(), nv.tolist()
     for ci, cfg in enumerate(cfgs):
+        anyc, scx, scy = cfg.any(), cfg.scale_x, cfg.scale_y
+        xs, ys, mxs, mys, sxs, sys_ = xtx[ci], xty[ci], mx[ci], my[ci], sx[ci], sy[ci]
         runs = []
         for f in range(p):
-            st = FoldStats(n_train=int(nt[f]), n_val=int(nv[f]))
-            if cfg.any():
-                st.mean_x_t, st.mean_y_t = mx[ci, f], my[ci, f]
-            if cfg.scale_x:
-                st.std_x_t = sx[ci, f]
-            if cfg.scale_y:
-                st.std_y_t = sy[ci, f]
-            runs.append(FoldResult(f + 1, xtx[ci, f], xty[ci, f], st))
+            st = FoldStats(mxs[f] if anyc else _EMPTY, mys[f] if anyc else _EMPTY, sxs[f] if scx else _EMPTY,
+                           sys_[f] if scy else _EMPTY, ntl[f], nvl[f])
+            runs.append(FoldResult(f + 1, xs[f], ys[f], st))
         out.append(runs)
     return out
 
