@@ -98,7 +98,7 @@ def load_inputs(args, allow_random: bool):
     return data, part
 
 
-def cmd_verify(data, part, tol: float) -> int:
+def cmd_verify(data, part, tol: float, ctx=None) -> int:
     err = cv.validate_partitioning(part)
     if err:
         print(f"invalid partitioning: {err}", file=sys.stderr)
@@ -108,7 +108,7 @@ def cmd_verify(data, part, tol: float) -> int:
         print(f"partitioning not scalable: {err}", file=sys.stderr)
         return EXIT_NOT_SCALABLE
     configs = cv.enumerate_configs()
-    fast = cv.run_all_folds_configs(data, part, configs)  # one Gram pass, 16 epilogues
+    fast = cv.run_all_folds_configs(data, part, configs, ctx=ctx)  # one Gram pass, 16 epilogues
     base = cv.baseline_fold_products_configs(data, part, configs)
     all_ok = True
     for cfg, fr, br in zip(configs, fast, base):
@@ -123,7 +123,23 @@ def cmd_verify(data, part, tol: float) -> int:
     return 0 if all_ok else EXIT_TOLERANCE
 
 
-def cmd_run(data, part, cfg: cv.PreprocessConfig, engine: str, out_dir: str) -> int:
+def _stats_lines(r) -> list:
+    lines = [f"{r.fold_id},counts,{r.stats.n_train},{r.stats.n_val}"]
+    for name, v in (("mean_x", r.stats.mean_x_t), ("mean_y", r.stats.mean_y_t), ("std_x", r.stats.std_x_t),
+                    ("std_y", r.stats.std_y_t)):
+        if v.size:
+            lines.append(f"{r.fold_id},{name}," + ",".join(cv.format_double(x) for x in v))
+    return lines
+
+
+def cmd_run(data, part, cfg: cv.PreprocessConfig, engine: str, out_dir: str, ctx=None) -> int:
+    """Per-fold %.17g CSVs + stats.csv (cvgram_cli.cpp:90-132).  The fast engine streams folds in batches
+    (cvg_run_all_folds_stream): a writer thread formats and writes each batch while the next batch's epilogue
+    and device-to-host copy run (the C call releases the GIL).  With a multi-device context (--devices) the
+    folds come from one sharded run instead; the files are byte-identical either way."""
+    import queue
+    import threading
+
     err = cv.validate_partitioning(part)
     if err:
         print(f"invalid partitioning: {err}", file=sys.stderr)
@@ -133,25 +149,58 @@ def cmd_run(data, part, cfg: cv.PreprocessConfig, engine: str, out_dir: str) -> 
         if err:
             print(f"partitioning not scalable: {err}", file=sys.stderr)
             return EXIT_NOT_SCALABLE
-    results = (cv.baseline_fold_products(data, part, cfg) if engine == "baseline"
-               else cv.run_all_folds(data, part, cfg))
     os.makedirs(out_dir, exist_ok=True)
+    stats = {}
+    work: queue.Queue = queue.Queue(maxsize=4)
+    failure = []
+
+    def writer():
+        while True:
+            batch = work.get()
+            if batch is None:
+                return
+            try:
+                for r in batch:
+                    tag = f"fold_{r.fold_id}"
+                    write_matrix_csv(os.path.join(out_dir, tag + "_xtx.csv"), r.xtx_t)
+                    write_matrix_csv(os.path.join(out_dir, tag + "_xty.csv"), r.xty_t)
+                    stats[r.fold_id] = _stats_lines(r)
+            except OSError as e:
+                failure.append(e)
+
+    th = threading.Thread(target=writer, daemon=True)
+    th.start()
+    try:
+        if engine == "baseline":
+            work.put(cv.baseline_fold_products(data, part, cfg))
+        elif isinstance(ctx, cv.MultiContext):
+            work.put(cv.run_all_folds(data, part, cfg, ctx=ctx))
+        else:
+            pending = []
+
+            def take(ci, r):  # for_each_fold hands over arrays it has already copied out of the batch buffers
+                pending.append(r)
+                if len(pending) >= 64:
+                    work.put(list(pending))
+                    pending.clear()
+
+            cv.for_each_fold(data, part, [cfg], take, batch=64, ctx=ctx)
+            if pending:
+                work.put(list(pending))
+    finally:
+        work.put(None)
+        th.join()
+    if failure:
+        raise CliIOError(f"cannot write fold files in {out_dir}: {failure[0]}")
     stats_lines = ["fold,name,values"]
-    for r in results:
-        tag = f"fold_{r.fold_id}"
-        write_matrix_csv(os.path.join(out_dir, tag + "_xtx.csv"), r.xtx_t)
-        write_matrix_csv(os.path.join(out_dir, tag + "_xty.csv"), r.xty_t)
-        stats_lines.append(f"{r.fold_id},counts,{r.stats.n_train},{r.stats.n_val}")
-        for name, v in (("mean_x", r.stats.mean_x_t), ("mean_y", r.stats.mean_y_t), ("std_x", r.stats.std_x_t),
-                        ("std_y", r.stats.std_y_t)):
-            if v.size:
-                stats_lines.append(f"{r.fold_id},{name}," + ",".join(cv.format_double(x) for x in v))
+    for f in sorted(stats):
+        stats_lines += stats[f]
     try:
         with open(os.path.join(out_dir, "stats.csv"), "w", newline="\n") as f:
             f.write("\n".join(stats_lines) + "\n")
     except OSError:
         raise CliIOError(f"cannot write stats.csv in {out_dir}")
-    print(f"wrote {len(results)} folds to {out_dir}")
+    print(f"wrote {len(stats)} folds to {out_dir}")
     return 0
 
 
@@ -195,6 +244,8 @@ def build_parser():
     v.add_argument("--random", nargs=5, metavar=("N", "K", "M", "P", "SEED"))
     v.add_argument("--tol", type=float, default=1e-8)
     v.add_argument("--threads", type=int, default=1)
+    v.add_argument("--devices", default=None, help="comma-separated CUDA devices for the fast engine's run "
+                                                    "(cvg_context_create_multi; results are identical)")
     r = sub.add_parser("run", help="write per-fold products and statistics to disk")
     r.add_argument("--x", required=True)
     r.add_argument("--y", required=True)
@@ -203,6 +254,7 @@ def build_parser():
     r.add_argument("--engine", default="fast", choices=["fast", "baseline"])
     r.add_argument("--out-dir", required=True)
     r.add_argument("--threads", type=int, default=1)
+    r.add_argument("--devices", default=None)
     b = sub.add_parser("bench", help="time both engines over a sweep of fold counts")
     b.add_argument("--n", type=int, required=True)
     b.add_argument("--k", type=int, required=True)
@@ -222,17 +274,28 @@ def main(argv=None) -> int:
         args = ap.parse_args(argv)
     except SystemExit as e:
         return 0 if e.code == 0 else EXIT_PARSE
+    if getattr(args, "threads", 1) < 1:
+        print("--threads must be at least 1", file=sys.stderr)
+        return EXIT_PARSE
     try:
+        ctx = None
+        if getattr(args, "devices", None):
+            try:
+                devs = [int(t) for t in args.devices.split(",") if t != ""]
+            except ValueError:
+                print(f"bad --devices list: {args.devices}", file=sys.stderr)
+                return EXIT_PARSE
+            ctx = cv.MultiContext(devs)
         if args.cmd == "verify":
             if not args.random and not (args.x and args.y and args.partition):
                 print("verify needs --x/--y/--partition or --random", file=sys.stderr)
                 return EXIT_PARSE
             data, part = load_inputs(args, allow_random=True)
-            return cmd_verify(data, part, args.tol)
+            return cmd_verify(data, part, args.tol, ctx)
         if args.cmd == "run":
             cfg = cv.parse_config(args.config)
             data, part = load_inputs(args, allow_random=False)
-            return cmd_run(data, part, cfg, args.engine, args.out_dir)
+            return cmd_run(data, part, cfg, args.engine, args.out_dir, ctx)
         if args.cmd == "bench":
             if not 3 <= args.reps <= 1000:
                 print("--reps must be in [3, 1000]", file=sys.stderr)

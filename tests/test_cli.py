@@ -107,3 +107,39 @@ def test_classify_combos_on_engine_output():  # test_combos.cpp:29-74, acceptanc
     assert rep.min_xty_separation >= 1e-3 and rep.min_pair_separation >= 1e-3
     text = cv.format_combo_table(rep)
     assert "distinct XtY classes: 8" in text and "distinct pair classes: 12" in text and "warning" not in text
+
+
+@pytest.mark.gpu
+def test_acceptance_c9_byte_identical_across_runs_and_devices(tmp_path):
+    """acceptance.cpp:267-304 on the GPU engine: `verify` and `run` outputs are byte-identical across two runs
+    and across thread counts, and across device counts (--devices 0,0: the sharded multi-device run in its
+    one-GPU emulation); `run`'s files also match the long-double oracle (1e-10 normalized)."""
+    import oracle
+    from paper_2401_13185_b200 import cvgram as cv
+    from paper_2401_13185_b200.cli import read_matrix_csv
+
+    v = [cli("verify", "--random", "120", "8", "3", "6", "77", "--threads", t, *extra)
+         for t, extra in (("1", ()), ("1", ()), ("4", ()), ("1", ("--devices", "0,0")))]
+    assert all(c == 0 for c, _, _ in v), v
+    assert v[0][1] == v[1][1] == v[2][1] == v[3][1]
+    rng = cv.MT19937_64(109)
+    data = cv.random_dataset(5000, 40, 2, rng)  # folds of 1000 rows: the multi-device run is sharded
+    part = cv.random_partitioning(5000, 5, rng)
+    xp, yp, pp = write_inputs(str(tmp_path), data.x(), data.y(), part.labels)
+    outs = []
+    for name, extra in (("o1", ("--threads", "1")), ("o2", ("--threads", "1")), ("o4", ("--threads", "4")),
+                        ("od", ("--devices", "0,0"))):
+        code, out, err = cli("run", "--x", xp, "--y", yp, "--partition", pp, "--config", "1111", "--out-dir",
+                             str(tmp_path / name), *extra)
+        assert code == 0, out + err
+        outs.append(tmp_path / name)
+    files = sorted(os.listdir(outs[0]))
+    assert len(files) == 2 * 5 + 1
+    for o in outs[1:]:
+        match, mismatch, errors = filecmp.cmpfiles(outs[0], o, files, shallow=False)
+        assert not mismatch and not errors, (o, mismatch, errors)
+    truth = oracle.truth_all_folds(data.x(), data.y(), part.labels, 5, 15, n_threads=8)
+    for r in truth:
+        got = read_matrix_csv(str(outs[0] / f"fold_{r.fold_id}_xtx.csv"))
+        sc = np.sqrt(np.abs(np.diag(r.xtx_t)))
+        assert np.max(np.abs(got - r.xtx_t) / np.maximum(np.abs(r.xtx_t), np.outer(sc, sc))) <= 1e-10
