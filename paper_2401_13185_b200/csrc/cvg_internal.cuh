@@ -203,10 +203,13 @@ void launch_segmax(int dtype, const void* x, int64_t ldx, const void* y, int64_t
 bool launch_reorder_q(int dtype, int slices, const void* x, int64_t ldx, const void* y, int64_t ldy, int64_t k,
                       int64_t m, const int64_t* src_row, int64_t zrows, int64_t kp, int64_t c_begin, int64_t c_end,
                       int64_t nsrc, const double* shift, const int* blkseg, const unsigned long long* segmax,
-                      int headroom, int* ovf, int8_t* zq, int* nonfinite, cudaStream_t s);
+                      int headroom, int* ovf, int8_t* zq, int* nonfinite, cudaStream_t s, int64_t blk_lo = 0,
+                      int64_t blk_hi = -1, int max_sms = 0);
+// Segments [seg_base, seg_base + nseg) of segs (absolute indices into segs / segmax / part); max_ctas > 0 caps
+// the persistent grid.
 bool launch_gram_i8(int slices, const int8_t* zq, const unsigned long long* segmax, int headroom, int64_t zrows,
                     int64_t kp, const GramTask* segs, int64_t nseg, const int2* tiles, int ntiles, double* part,
-                    cudaStream_t s);
+                    cudaStream_t s, int64_t seg_base = 0, int max_ctas = 0);
 
 inline int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
 inline int64_t padded_cols(int64_t k, int64_t m, int dtype = 0) {

@@ -213,8 +213,8 @@ template <int S, int KS, int kMaxSt = 8>
 __global__ void __launch_bounds__(kQThreads, 1)
     gram_i8_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                    const unsigned long long* __restrict__ segmax, const GramTask* __restrict__ segs,
-                   const int2* __restrict__ tiles, int ntiles, int64_t nitems, int64_t kp, double* __restrict__ part,
-                   int headroom) {
+                   const int2* __restrict__ tiles, int ntiles, int64_t nitems, int64_t seg_base, int64_t kp,
+                   double* __restrict__ part, int headroom) {
   using C = QCfg<S, KS, kMaxSt>;
   constexpr int NST = C::kNst;
   constexpr int kPer = QK / KS;  // stages per 64-row block
@@ -248,8 +248,9 @@ __global__ void __launch_bounds__(kQThreads, 1)
   auto opB = [&](int s) { return smem + s * C::kStage + S * C::kA; };
   // item -> (segment, tile)
   auto item = [&](int64_t it, int& seg, int& ti, int& tj, int& wmask, GramTask& task) {
-    seg = (int)(it / ntiles);
-    const int2 tile0 = tiles[it - (int64_t)seg * ntiles];
+    const int64_t sl = it / ntiles;  // segment within this launch's range [seg_base, seg_base + nitems / ntiles)
+    seg = (int)(seg_base + sl);
+    const int2 tile0 = tiles[it - sl * ntiles];
     ti = uniform(tile0.x);
     tj = uniform(tile0.y & 0xffff);
     wmask = uniform(tile0.y >> 16);
@@ -506,7 +507,8 @@ __global__ void __launch_bounds__(kQ1Threads, CVG_K1Q_MIN_BLOCKS)
                      int64_t zrows, int64_t kp, int64_t c_begin, int64_t c_end, int64_t nsrc,
                      const double* __restrict__ shift, const int* __restrict__ blkseg,
                      const unsigned long long* __restrict__ segmax, int headroom, int* __restrict__ ovf,
-                     int* __restrict__ nonfinite) {
+                     int* __restrict__ nonfinite, int64_t blk_lo, int64_t blk_hi) {
+  // Blocks [blk_lo, blk_hi) of Z.
   // Out of range: tt outside [2^52, 2^53) (a non-finite z, or w below the digits' range) or V >= 2^(7S)
   // (w above it).  With sampled exponents (ovf != null) that marks the block's segment for the exact
   // pass; otherwise (exact exponents, where only a non-finite z can get there) it is the
@@ -525,7 +527,8 @@ __global__ void __launch_bounds__(kQ1Threads, CVG_K1Q_MIN_BLOCKS)
   const int64_t wd = k + m;
   CVG_DCHECK(c_begin >= 0 && c_end <= kp && c_begin % 64 == 0 && zrows % QK == 0);
   const int64_t nchunk = (c_end - c_begin) / 64;
-  const int64_t nblk = zrows / QK;
+  const int64_t nblk = blk_hi;
+  CVG_DCHECK(blk_lo >= 0 && blk_hi <= zrows / QK);
   const int64_t grid = gridDim.x;
   const double C = 0x1p52 + (double)DigitOffset<S>::v;
   uint32_t oor = 0;  // out-of-range bits of this block's values
@@ -551,7 +554,7 @@ __global__ void __launch_bounds__(kQ1Threads, CVG_K1Q_MIN_BLOCKS)
         v[4 * pp + i] = src < 0 ? 0.0 : kind <= 1 ? (double)__ldg(base + src * ld) : kind == 2 ? 1.0 : 0.0;
       }
   };
-  int64_t blk = blockIdx.x;
+  int64_t blk = blk_lo + blockIdx.x;
   load_src(blk, 0);
   load_src(blk + grid, 1);
   __syncthreads();
@@ -652,7 +655,8 @@ inline bool make_zq_map(CUtensorMap* map, const int8_t* zq, int64_t zrows, int64
 
 template <int S, int KS, int kMaxSt = 8>
 bool launch_gram_i8_s(const int8_t* zq, const unsigned long long* segmax, int headroom, int64_t zrows, int64_t kp,
-                      const GramTask* segs, int64_t nseg, const int2* tiles, int ntiles, double* part, cudaStream_t s) {
+                      const GramTask* segs, int64_t seg_base, int64_t nseg, const int2* tiles, int ntiles, double* part,
+                      int max_ctas, cudaStream_t s) {
   CUtensorMap ma, mb;
   if (!make_zq_map(&ma, zq, zrows, kp, S, QA, KS) || !make_zq_map(&mb, zq, zrows, kp, S, QB, KS)) return false;
   using C = QCfg<S, KS, kMaxSt>;
@@ -661,10 +665,11 @@ bool launch_gram_i8_s(const int8_t* zq, const unsigned long long* segmax, int he
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int64_t nitems = nseg * (int64_t)ntiles;
-  const int64_t blocks = std::min<int64_t>(nitems, sms);  // persistent: one CTA per SM (1 fits: shared memory)
+  // persistent: one CTA per SM (1 fits: shared memory), or max_ctas to leave SMs to a concurrent K1Q
+  const int64_t blocks = std::min<int64_t>(nitems, max_ctas > 0 ? std::min(max_ctas, sms) : sms);
   if (blocks > 0)
     gram_i8_kernel<S, KS, kMaxSt><<<(unsigned)blocks, kQThreads, C::kSmem, s>>>(ma, mb, segmax, segs, tiles, ntiles,
-                                                                                nitems, kp, part, headroom);
+                                                                                nitems, seg_base, kp, part, headroom);
   return true;
 }
 
@@ -672,7 +677,7 @@ template <typename T, int S>
 bool launch_k1q(const void* x, int64_t ldx, const void* y, int64_t ldy, int64_t k, int64_t m, const int64_t* src_row,
                 int64_t zrows, int64_t kp, int64_t c_begin, int64_t c_end, int64_t nsrc, const double* shift,
                 const int* blkseg, const unsigned long long* segmax, int headroom, int* ovf, int8_t* zq, int* nonfinite,
-                cudaStream_t s) {
+                int64_t blk_lo, int64_t blk_hi, int max_sms, cudaStream_t s) {
   CUtensorMap mo;
   if (!make_zq_map(&mo, zq, zrows, kp, S, 64)) return false;
   constexpr int smem = k1q_smem_bytes<S>();
@@ -690,10 +695,15 @@ bool launch_k1q(const void* x, int64_t ldx, const void* y, int64_t ldy, int64_t 
     wave = (per_sm > 0 ? per_sm : 1) * sms;
     wave_cache[dev & 63].store(wave, std::memory_order_relaxed);
   }
-  const int64_t blocks = std::min<int64_t>(zrows / QK, (int64_t)wave);
+  int sms_all = 0;
+  cudaDeviceGetAttribute(&sms_all, cudaDevAttrMultiProcessorCount, dev);
+  if (max_sms > 0 && max_sms < sms_all) wave = wave / sms_all * max_sms;  // confine to max_sms SMs' worth
+  const int64_t blocks = std::min<int64_t>(blk_hi - blk_lo, (int64_t)std::max(wave, 1));
+  if (blocks <= 0) return true;
   reorder_q_kernel<T, S><<<(unsigned)blocks, kQ1Threads, smem, s>>>(mo, (const T*)x, ldx, (const T*)y, ldy, k, m,
                                                                     src_row, zrows, kp, c_begin, c_end, nsrc, shift,
-                                                                    blkseg, segmax, headroom, ovf, nonfinite);
+                                                                    blkseg, segmax, headroom, ovf, nonfinite, blk_lo,
+                                                                    blk_hi);
   return true;
 }
 
@@ -723,10 +733,13 @@ void launch_segmax(int dtype, const void* x, int64_t ldx, const void* y, int64_t
 bool launch_reorder_q(int dtype, int slices, const void* x, int64_t ldx, const void* y, int64_t ldy, int64_t k,
                       int64_t m, const int64_t* src_row, int64_t zrows, int64_t kp, int64_t c_begin, int64_t c_end,
                       int64_t nsrc, const double* shift, const int* blkseg, const unsigned long long* segmax,
-                      int headroom, int* ovf, int8_t* zq, int* nonfinite, cudaStream_t s) {
+                      int headroom, int* ovf, int8_t* zq, int* nonfinite, cudaStream_t s, int64_t blk_lo,
+                      int64_t blk_hi, int max_sms) {
   if (zrows <= 0 || c_end <= c_begin) return true;
-#define CVG_K1Q(T, S) \
-  return launch_k1q<T, S>(x, ldx, y, ldy, k, m, src_row, zrows, kp, c_begin, c_end, nsrc, shift, blkseg, segmax, headroom, ovf, zq, nonfinite, s)
+  if (blk_hi < 0) blk_hi = zrows / QK;
+#define CVG_K1Q(T, S)                                                                                              \
+  return launch_k1q<T, S>(x, ldx, y, ldy, k, m, src_row, zrows, kp, c_begin, c_end, nsrc, shift, blkseg, segmax, \
+                          headroom, ovf, zq, nonfinite, blk_lo, blk_hi, max_sms, s)
   if (dtype == 0) {
     if (slices == 5) CVG_K1Q(double, 5);
     else CVG_K1Q(double, 6);
@@ -749,10 +762,13 @@ static int i8_stage_rows() {
 
 bool launch_gram_i8(int slices, const int8_t* zq, const unsigned long long* segmax, int headroom, int64_t zrows,
                     int64_t kp, const GramTask* segs, int64_t nseg, const int2* tiles, int ntiles, double* part,
-                    cudaStream_t s) {
-#define CVG_GRAM_I8(S)                                                                                       \
-  return i8_stage_rows() == 64 ? launch_gram_i8_s<S, 64>(zq, segmax, headroom, zrows, kp, segs, nseg, tiles, ntiles, part, s) \
-                               : launch_gram_i8_s<S, 32>(zq, segmax, headroom, zrows, kp, segs, nseg, tiles, ntiles, part, s)
+                    cudaStream_t s, int64_t seg_base, int max_ctas) {
+#define CVG_GRAM_I8(S)                                                                                             \
+  return i8_stage_rows() == 64                                                                                     \
+             ? launch_gram_i8_s<S, 64>(zq, segmax, headroom, zrows, kp, segs, seg_base, nseg, tiles, ntiles, part, \
+                                       max_ctas, s)                                                                \
+             : launch_gram_i8_s<S, 32>(zq, segmax, headroom, zrows, kp, segs, seg_base, nseg, tiles, ntiles, part, \
+                                       max_ctas, s)
   switch (slices) {
     case 3: CVG_GRAM_I8(3);
     case 4: CVG_GRAM_I8(4);
