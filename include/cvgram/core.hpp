@@ -1,10 +1,15 @@
 #pragma once
 // Core types of the B200 cvgram engine, source-compatible with the reference
 // header /root/reference/proj/include/cvgram/core.hpp (same names, fields,
-// exception types and messages) but without Eigen: Matrix / Vector are a small
-// dense row-major fp64 type providing the subset of Eigen the reference API and
-// its tests use.  Computation happens in the sm_100a engine
-// behind include/cvgram_b200.h; these headers only validate and marshal.
+// exception types and messages).  Matrix / Vector / Index are the reference's
+// own Eigen typedefs (core.hpp:16-18) whenever <Eigen/Dense> is on the include
+// path, so callers that run Eigen operations on a FoldResult (.block, .ldlt,
+// ...) compile unchanged; without Eigen (define CVGRAM_NO_EIGEN to force it)
+// they are a small dense row-major fp64 type with the subset of Eigen the
+// reference API and its tests use.  Computation happens in
+// the sm_100a engine behind include/cvgram_b200.h; these headers only validate
+// and marshal, touching matrices only through rows() / cols() / size() /
+// data() / (i, j) / allFinite() / norm() -- the members both types share.
 
 #include <algorithm>
 #include <cmath>
@@ -16,8 +21,20 @@
 #include <string>
 #include <vector>
 
+#if !defined(CVGRAM_NO_EIGEN) && defined(__has_include)
+#if __has_include(<Eigen/Dense>)
+#include <Eigen/Dense>
+#define CVGRAM_WITH_EIGEN 1
+#endif
+#endif
+
 namespace cvgram {
 
+#ifdef CVGRAM_WITH_EIGEN
+using Matrix = Eigen::Matrix<double, Eigen::Dynamic, Eigen::Dynamic, Eigen::RowMajor>;  // core.hpp:16
+using Vector = Eigen::RowVectorXd;                                                       // core.hpp:17
+using Index = Eigen::Index;                                                              // core.hpp:18
+#else
 using Index = std::ptrdiff_t;  // Eigen::Index (core.hpp:18)
 
 class Matrix;
@@ -149,6 +166,8 @@ class Vector : public Matrix {
   static Vector Zero(Index n) { return Vector(n); }
 };
 
+#endif  // CVGRAM_WITH_EIGEN
+
 struct dimension_error : std::invalid_argument {
   using std::invalid_argument::invalid_argument;
 };
@@ -242,9 +261,11 @@ struct FoldResult {
 inline double max_rel_diff(const Matrix& a, const Matrix& b, double floor = 1e-30) {
   if (a.rows() != b.rows() || a.cols() != b.cols()) throw dimension_error("max_rel_diff: shape mismatch");
   double worst = 0.0;
+  const double* pa = a.data();
+  const double* pb = b.data();
   for (Index i = 0; i < a.size(); ++i) {
-    const double den = std::max({std::abs(a(i)), std::abs(b(i)), floor});
-    worst = std::max(worst, std::abs(a(i) - b(i)) / den);
+    const double den = std::max({std::abs(pa[i]), std::abs(pb[i]), floor});
+    worst = std::max(worst, std::abs(pa[i] - pb[i]) / den);
   }
   return worst;
 }

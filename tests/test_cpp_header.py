@@ -36,3 +36,15 @@ def test_cpp_header_all_cases_on_a_multi_device_context():
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "0 failing tests" in r.stdout
+
+
+def test_headers_compile_against_eigen_typedefs():
+    """With <Eigen/Dense> on the include path the headers take the reference's own Matrix / Vector / Index
+    typedefs (core.hpp:16-18), so callers' Eigen code on a FoldResult compiles unchanged.  Eigen is absent from
+    this image: tests/cpp/eigen_shape stands in with Eigen's spelling of the members the headers may use."""
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run(["g++", "-std=c++20", "-fsyntax-only", "-Wall", "-Wextra", "-I" + os.path.join(root, "include"),
+                        "-I" + os.path.join(root, "tests", "cpp", "eigen_shape"),
+                        os.path.join(root, "tests", "cpp", "eigen_shape_check.cpp")],
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr
