@@ -174,17 +174,8 @@ void launch_reorder_split_h(int dtype, const void* x, int64_t ldx, const void* y
 bool launch_gram_f16s(const void* zh_hi, const void* zh_lo, const float* unscale, int group_rows, int64_t zrows,
                       int64_t kp, const GramTask* segs, int64_t nseg, const int2* tiles128, int ntiles, double* part,
                       cudaStream_t s);
-// The same on CTA pairs (cta_group::2, M = 256 split across the pair, B halves): pairs as for
-// launch_gram_tf32_2sm.
-bool launch_gram_f16s_2sm(const void* zh_hi, const void* zh_lo, const float* unscale, int group_rows, int64_t zrows,
-                          int64_t kp, const GramTask* segs, int64_t nseg, const int4* pairs, int npairs, double* part,
-                          cudaStream_t s);
 bool launch_gram_tf32(const float* zt_hi, const float* zt_lo, int64_t zrows, int64_t kp, const GramTask* segs,
                       int64_t nseg, const int2* tiles128, int ntiles, double* part, int nterms, cudaStream_t s);
-// The same on CTA pairs (cta_group::2, cluster of 2): pairs[i] = {a, j, write0, write1}
-// covers row blocks 2a, 2a+1 (128 wide) x column block j; writeN: that CTA's tile is needed.
-bool launch_gram_tf32_2sm(const float* zt_hi, const float* zt_lo, int64_t zrows, int64_t kp, const GramTask* segs,
-                          int64_t nseg, const int4* pairs, int npairs, double* part, cudaStream_t s);
 
 // K1Q + K2q (fp64, CVG_FP64_KIND=i8; k_gram_i8.cu): per-(segment, column) exponents from the
 // segment's max |z| (segmax), then bucket/shift/scale/cut into `slices` int8 digits laid out

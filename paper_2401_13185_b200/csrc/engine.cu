@@ -209,23 +209,6 @@ Status TreeProgram::run(cvg_context* ctx, const int2* tiles, int ntiles, int64_t
 // Rows per segment: a fixed constant per dtype (never a function of the GPU
 // count, so sums stay bit-identical across world sizes).  CVG_CHUNK_ROWS
 // overrides it for tuning experiments (rounded to the plan's row step).
-// fp32 Gram on CTA pairs (tcgen05 cta_group::2): CVG_TF32_2SM=1 (A/B against the single-CTA kernel).
-static bool tf32_2sm() {
-  static const bool v = [] {
-    const char* e = std::getenv("CVG_TF32_2SM");
-    return e && e[0] == '1';
-  }();
-  return v;
-}
-
-// fp16 Gram on CTA pairs (cta_group::2): CVG_F16_2SM=1.
-static bool f16_2sm() {
-  static const bool v = [] {
-    const char* e = std::getenv("CVG_F16_2SM");
-    return e && e[0] == '1';
-  }();
-  return v;
-}
 
 // fp32 operand kind: the scaled fp16 split on kind::f16 (default) or, with
 // CVG_FP32_KIND=tf32, the 3xTF32 split on kind::tf32 (k_gram_tf32.cu; A/B tests).
@@ -374,23 +357,6 @@ Status Plan::create(cvg_context* ctx, int dtype, int64_t n, int64_t k, int64_t m
                          ctx->stream));
   CVG_CK(cudaMemcpyAsync(out_tiles_d_.as<int2>(), out_tiles_.data(), out_tiles_.size() * sizeof(int2),
                          cudaMemcpyHostToDevice, ctx->stream));
-  pairs128_.clear();
-  for (const int2& t : tiles128_) {
-    const int a = t.x / 2, half = t.x & 1;
-    int4* hit = nullptr;
-    for (int4& q : pairs128_)
-      if (q.x == a && q.y == t.y) hit = &q;
-    if (!hit) {
-      pairs128_.push_back(make_int4(a, t.y, 0, 0));
-      hit = &pairs128_.back();
-    }
-    (half ? hit->w : hit->z) = 1;
-  }
-  if (!pairs128_.empty()) {
-    CVG_TRY(pairs128_d_.ensure(pairs128_.size() * sizeof(int4)));
-    CVG_CK(cudaMemcpyAsync(pairs128_d_.as<int4>(), pairs128_.data(), pairs128_.size() * sizeof(int4),
-                           cudaMemcpyHostToDevice, ctx->stream));
-  }
   if (!tiles128_.empty()) {
     CVG_TRY(tiles128_d_.ensure(tiles128_.size() * sizeof(int2)));
     CVG_CK(cudaMemcpyAsync(tiles128_d_.as<int2>(), tiles128_.data(), tiles128_.size() * sizeof(int2),
@@ -719,18 +685,10 @@ Status Plan::gram(const void* d_x, int64_t ldx, const void* d_y, int64_t ldy, co
       bool ok;
       {
         Timed t(ctx_, kGram);
-        ok = f16_path() && f16_2sm()
-                 ? launch_gram_f16s_2sm(zt_hi_.as<void>(), zt_lo_.as<void>(), unscale_.as<float>(), (int)row_step_,
-                                        zrows_, kp_, segs_d_.as<GramTask>(), (int64_t)segs_.size(),
-                                        pairs128_d_.as<int4>(), (int)pairs128_.size(), part_.as<double>(), s)
-             : f16_path()
+        ok = f16_path()
                  ? launch_gram_f16s(zt_hi_.as<void>(), zt_lo_.as<void>(), unscale_.as<float>(), (int)row_step_,
                                     zrows_, kp_, segs_d_.as<GramTask>(), (int64_t)segs_.size(),
                                     tiles128_d_.as<int2>(), (int)tiles128_.size(), part_.as<double>(), s)
-             : tf32_2sm()
-                 ? launch_gram_tf32_2sm(zt_hi_.as<float>(), zt_lo_.as<float>(), zrows_, kp_, segs_d_.as<GramTask>(),
-                                        (int64_t)segs_.size(), pairs128_d_.as<int4>(), (int)pairs128_.size(),
-                                        part_.as<double>(), s)
                  : launch_gram_tf32(zt_hi_.as<float>(), zt_lo_.as<float>(), zrows_, kp_, segs_d_.as<GramTask>(),
                                     (int64_t)segs_.size(), tiles128_d_.as<int2>(), (int)tiles128_.size(),
                                     part_.as<double>(), 3, s);

@@ -180,14 +180,12 @@ class Plan {
   int64_t n_ = 0, k_ = 0, m_ = 0, w_ = 0, kp_ = 0;
   int32_t p_ = 0, fb_ = 0, fe_ = 0;
   std::vector<int2> tiles_, out_tiles_, tiles128_;
-  std::vector<int4> pairs128_;  // CTA-pair tiles for the cta_group::2 fp32 Gram
   std::vector<int2> tilesq_;    // int8 Gram tiles {I (128 rows), J (64 columns) | write mask << 16}
   bool i8_ = false;             // int8 digit slices: fp64 default (CVG_FP64_KIND=dmma: DMMA); fp32 with CVG_FP32_KIND=i8
   int sample_ = 16;             // int8 path: segment maxima over every sample_-th row (CVG_I8_SAMPLE; 1 = exact)
   int64_t exact_segments_ = 0;  // segments the last gram redid from their exact max
   std::vector<int> ovf_host_;
   int slices_ = 6;              // base-256 int8 digits per value (fp64: CVG_I8_SLICES = 5 | 6; fp32: CVG_I8_SLICES_F32 = 3 | 4)
-  DevBuf pairs128_d_;
   std::vector<int64_t> counts_;  // per fold (all p) validation sizes
   std::vector<GramTask> segs_;
   std::vector<int32_t> fold_seg_begin_;

@@ -185,190 +185,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
-// ---------------------------------------------------------------------------
-// K2'' (cta_group::2): the same contraction on a CTA pair (cluster of 2 on one
-// TPC).  A pair owns a 256 x 128 output tile: rows = Z columns of the 128-blocks
-// 2a and 2a+1 (one per CTA, the M = 256 MMA split), columns = Z columns of block
-// j, whose B operand is split in halves of 64 columns (one per CTA).  Per CTA and
-// 32-row stage that is 48 KB of operands instead of 64 KB for the same 128 x 128
-// outputs, so L2 and shared-memory traffic per flop drop by a quarter.  The leader
-// (rank 0) issues tcgen05.mma.cta_group::2; both CTAs TMA their own halves into
-// their own shared memory, signalling the leader's full barrier; the leader's
-// commits multicast to both CTAs' stage-free and accumulator-full barriers; each
-// CTA drains its own TMEM (same layout as K2') and arrives on the leader's
-// accumulator-empty barrier.  Bit-identical to K2' (same products, same order).
-constexpr int kB2 = TT / 2;                       // B half: 64 columns per CTA
-constexpr int kOpB2 = kB2 * KS * 4;               // 8 KB
-constexpr int kStage2 = 2 * kOpBytes + 2 * kOpB2;  // A_hi, A_lo (16 KB each), B_hi, B_lo (8 KB each)
-constexpr int NST2 = 4;
-constexpr int kSmemTf32x2 = NST2 * kStage2 + 1024;
-constexpr uint32_t kIdescTf32x2 = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(TT >> 3) << 17) |
-                                  ((uint32_t)(2 * TT >> 4) << 24);  // M = 256, N = 128
-
-__device__ __forceinline__ uint32_t cluster_rank() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
-  return r;
-}
-__device__ __forceinline__ void cluster_sync_all() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
-}
-// shared::cluster address of `p` in CTA `rank` of the cluster
-__device__ __forceinline__ uint32_t mapa(const void* p, uint32_t rank) {
-  uint32_t r;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
-  return r;
-}
-__device__ __forceinline__ void tma_load_3d_2sm(void* dst, const CUtensorMap* map, uint32_t leader_bar, int c0, int c1,
-                                                int c2) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, "
-      "%5}], [%2];\n" ::"r"(smem_u32(dst)),
-      "l"(map), "r"(leader_bar), "r"(c0), "r"(c1), "r"(c2)
-      : "memory");
-}
-__device__ __forceinline__ void mma_tf32_x2(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t accumulate) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "setp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n"
-      "}\n" ::"r"(tmem_d),
-      "l"(a), "l"(b), "r"(kIdescTf32x2), "r"(accumulate));
-}
-__device__ __forceinline__ void mma_commit_x2(uint64_t* bar) {  // arrive on `bar` in both CTAs of the pair
-  asm volatile(
-      "{\n.reg .b16 m;\nmov.b16 m, 3;\n"
-      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], m;\n}\n" ::"r"(
-          smem_u32(bar))
-      : "memory");
-}
-
-// pairs[i] = {a, j, write0, write1}: row blocks 2a (CTA 0) and 2a+1 (CTA 1), column block j.
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
-    gram_tf32_2sm_kernel(const __grid_constant__ CUtensorMap map_a_hi, const __grid_constant__ CUtensorMap map_a_lo,
-                         const __grid_constant__ CUtensorMap map_b_hi, const __grid_constant__ CUtensorMap map_b_lo,
-                         const GramTask* __restrict__ segs, const int4* __restrict__ pairs, int npairs, int64_t kp,
-                         double* __restrict__ part) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  __shared__ __align__(8) uint64_t full_bar[NST2], empty_bar[NST2], acc_full[2], acc_empty[2];
-  __shared__ uint32_t tmem_base;
-  const uint32_t rank = cluster_rank();
-  const int64_t pid = blockIdx.x >> 1;
-  const int seg = (int)(pid / npairs);
-  const int4 pt = pairs[pid - (int64_t)seg * npairs];
-  const int rblk = 2 * pt.x + (int)rank;  // this CTA's 128-row block of the output
-  const bool write_out = rank == 0 ? pt.z != 0 : pt.w != 0;
-  const GramTask task = segs[seg];
-  CVG_DCHECK(task.zrow % KS == 0 && task.rows % KS == 0 && task.rows > 0);
-  const int nsteps = (int)(task.rows / KS);
-  const int nchunks = (nsteps + kDrainSteps - 1) / kDrainSteps;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < NST2; ++s) {
-      mbar_init(&full_bar[s], 1);
-      mbar_init(&empty_bar[s], 1);
-    }
-    for (int b = 0; b < 2; ++b) {
-      mbar_init(&acc_full[b], 1);
-      mbar_init(&acc_empty[b], 2 * kEpiWarps);  // both CTAs' drain warps (leader's copy is the one used)
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-  }
-  if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(&tmem_base)),
-                 "r"(2 * TT));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;\n");
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-  cluster_sync_all();
-  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-  const uint32_t tmem_d = tmem_base;
-
-  auto op = [&](int s, int which) {  // 0 A_hi 1 A_lo 2 B_hi 3 B_lo
-    return smem + s * kStage2 + (which < 2 ? which * kOpBytes : 2 * kOpBytes + (which - 2) * kOpB2);
-  };
-
-  if (warp == 0) {
-    if (lane == 0) {  // ---- TMA producer (both CTAs): this CTA's A block and B half
-      const uint32_t leader_full0 = mapa(&full_bar[0], 0) ;
-      for (int it = 0; it < nsteps; ++it) {
-        const int s = it % NST2;
-        const uint32_t ph = (uint32_t)(it / NST2) & 1u;
-        mbar_wait(&empty_bar[s], ph ^ 1u);
-        if (rank == 0) mbar_expect_tx(&full_bar[s], (uint32_t)(2 * kStage2));  // both CTAs' bytes
-        const uint32_t lb = leader_full0 + (uint32_t)(s * sizeof(uint64_t));
-        const int blk = (int)(task.zrow / KS) + it;
-        tma_load_3d_2sm(op(s, 0), &map_a_hi, lb, 0, rblk * TT, blk);
-        tma_load_3d_2sm(op(s, 1), &map_a_lo, lb, 0, rblk * TT, blk);
-        tma_load_3d_2sm(op(s, 2), &map_b_hi, lb, 0, pt.y * TT + (int)rank * kB2, blk);
-        tma_load_3d_2sm(op(s, 3), &map_b_lo, lb, 0, pt.y * TT + (int)rank * kB2, blk);
-      }
-    }
-  } else if (warp == 1) {
-    if (lane == 0 && rank == 0) {  // ---- MMA issuer (leader only)
-      for (int it = 0; it < nsteps; ++it) {
-        const int chunk = it / kDrainSteps, b = chunk & 1;
-        const bool first = it % kDrainSteps == 0;
-        if (first && chunk >= 2) mbar_wait(&acc_empty[b], (uint32_t)((chunk >> 1) - 1) & 1u);
-        const int s = it % NST2;
-        mbar_wait(&full_bar[s], (uint32_t)(it / NST2) & 1u);
-        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-        const uint32_t acc = tmem_d + (uint32_t)(b * TT);
-        const uint64_t a_hi = kmajor_sw128_desc(op(s, 0)), a_lo = kmajor_sw128_desc(op(s, 1));
-        const uint64_t b_hi = kmajor_sw128_desc(op(s, 2)), b_lo = kmajor_sw128_desc(op(s, 3));
-#pragma unroll
-        for (int k = 0; k < KS / 8; ++k) {
-          const uint64_t dk = 2ull * k;
-          mma_tf32_x2(acc, a_hi + dk, b_hi + dk, (first && k == 0) ? 0u : 1u);
-          mma_tf32_x2(acc, a_hi + dk, b_lo + dk, 1u);
-          mma_tf32_x2(acc, a_lo + dk, b_hi + dk, 1u);
-        }
-        mma_commit_x2(&empty_bar[s]);
-        if (it % kDrainSteps == kDrainSteps - 1 || it == nsteps - 1) mma_commit_x2(&acc_full[b]);
-      }
-    }
-  } else {  // ---- drain warps (both CTAs): own TMEM rows, 64 columns each
-    const int q = warp & 3;
-    const int h = (warp - 2) >> 2;
-    const uint32_t leader_empty0 = mapa(&acc_empty[0], 0);
-    double acc64[64];
-#pragma unroll
-    for (int j = 0; j < 64; ++j) acc64[j] = 0.0;
-    for (int chunk = 0; chunk < nchunks; ++chunk) {
-      const int b = chunk & 1;
-      mbar_wait(&acc_full[b], (uint32_t)(chunk >> 1) & 1u);
-      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-#pragma unroll
-      for (int c0 = 0; c0 < 64; c0 += 32) {
-        uint32_t r[32];
-        tmem_ld32(tmem_d + ((uint32_t)(32 * q) << 16) + (uint32_t)(b * TT + 64 * h + c0), r);
-#pragma unroll
-        for (int j = 0; j < 32; ++j) acc64[c0 + j] += (double)__uint_as_float(r[j]);
-      }
-      asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-      __syncwarp();
-      if (lane == 0)
-        asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(
-                         leader_empty0 + (uint32_t)(b * sizeof(uint64_t)))
-                     : "memory");
-    }
-    if (write_out) {
-      const int64_t row = (int64_t)rblk * TT + 32 * q + lane;
-      double* out = part + (int64_t)seg * kp * kp + row * kp + (int64_t)pt.y * TT + 64 * h;
-#pragma unroll
-      for (int j = 0; j < 64; j += 2) *reinterpret_cast<double2*>(out + j) = make_double2(acc64[j], acc64[j + 1]);
-    }
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-  cluster_sync_all();  // the leader's MMAs and both drains are done before TMEM is released
-  if (warp == 1) {
-    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;\n" ::"r"(tmem_d), "r"(2 * TT));
-  }
-}
 
 // TF32 round-to-nearest of an fp32 value (low 13 mantissa bits cleared).
 __device__ __forceinline__ float tf32_rn(float v) {
@@ -500,19 +316,3 @@ bool launch_gram_tf32(const float* zt_hi, const float* zt_lo, int64_t zrows, int
 
 }  // namespace cvg
 
-namespace cvg {
-
-bool launch_gram_tf32_2sm(const float* zt_hi, const float* zt_lo, int64_t zrows, int64_t kp, const GramTask* segs,
-                          int64_t nseg, const int4* pairs, int npairs, double* part, cudaStream_t s) {
-  CUtensorMap ah, al, bh, bl;
-  if (!make_map(&ah, zt_hi, zrows, kp) || !make_map(&al, zt_lo, zrows, kp) || !make_map(&bh, zt_hi, zrows, kp, kB2) ||
-      !make_map(&bl, zt_lo, zrows, kp, kB2))
-    return false;
-  cudaFuncSetAttribute(gram_tf32_2sm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemTf32x2);
-  const int64_t blocks = 2 * nseg * (int64_t)npairs;
-  if (blocks > 0)
-    gram_tf32_2sm_kernel<<<(unsigned)blocks, kThreads, kSmemTf32x2, s>>>(ah, al, bh, bl, segs, pairs, npairs, kp, part);
-  return true;
-}
-
-}  // namespace cvg
