@@ -530,10 +530,9 @@ def rooflines(cid, n, k, m, p, masks, world, flops, kms, kcnt, steps, x_elt):
     f32 = not x_dtype_is_f64(cid)
     executed = executed_gram_flops(n, k, m, p, f32) / max(world, 1) / (gram_ms * 1e-3) / 1e12
     tf32_kind = os.environ.get("CVG_FP32_KIND") == "tf32"
-    f32_i8 = f32 and os.environ.get("CVG_FP32_KIND") == "i8"
-    i8_kind = (not f32 and executed_fp64_kind() == "i8") or f32_i8
+    i8_kind = not f32 and executed_fp64_kind() == "i8"
     if i8_kind:
-        s_ = i8_slices(f32)
+        s_ = i8_slices()
         gram_kernel = (f"gram_i8_kernel<{s_}, 64> (tcgen05.mma kind::i8: exact base-256 int8 digit slices, "
                        f"{i8_pairs(s_)} slice-pair products into int32 TMEM, exact fp64 drain)")
         peak, unit = INT8_PEAK_TOPS, "TOPS (int8)"
@@ -568,7 +567,7 @@ def rooflines(cid, n, k, m, p, masks, world, flops, kms, kcnt, steps, x_elt):
     kp = -(-(k + m + 1) // tile) * tile
     if i8_kind:  # segment maxima over a 1/16 row sample + K1Q (read x | y, write S int8 digit slices)
         sample = max(1, int(os.environ.get("CVG_I8_SAMPLE", "16") or 16))
-        reorder_bytes = int(n * (k + m) * x_elt * (1 + 1 / sample)) + n * kp * i8_slices(f32)
+        reorder_bytes = int(n * (k + m) * x_elt * (1 + 1 / sample)) + n * kp * i8_slices()
     else:
         z_elem = 4 if (f32 and not tf32_kind) else 8  # Z: fp64 | fp16 hi + lo | tf32 hi + lo
         reorder_bytes = n * (k + m) * x_elt + n * kp * z_elem

@@ -231,21 +231,11 @@ static int i8_slices_env() {  // base-256 digits: 6 (48 bits, default) or 5 (40 
   const char* e = std::getenv("CVG_I8_SLICES");
   return e && std::atoi(e) == 5 ? 5 : 6;
 }
-// fp32 inputs on the int8 digit path (CVG_FP32_KIND=i8): 4 base-256 digits (32 bits below each segment
-// column's max, fp32 carries 24) or, with CVG_I8_SLICES_F32=3, 3 digits (24 bits).
 // Row-sample stride of the int8 path's segment maxima (CVG_I8_SAMPLE; 1 = every row, one exact pass).
 static int i8_sample_env() {
   const char* e = std::getenv("CVG_I8_SAMPLE");
   const int v = e ? std::atoi(e) : 16;
   return v >= 1 ? v : 16;
-}
-static bool fp32_i8_env() {
-  const char* e = std::getenv("CVG_FP32_KIND");
-  return e && std::string(e) == "i8";
-}
-static int i8_slices_f32_env() {
-  const char* e = std::getenv("CVG_I8_SLICES_F32");
-  return e && std::atoi(e) == 3 ? 3 : 4;
 }
 
 // The fp16 path's row group G (one exponent per group and column, one fp32 TMEM
@@ -328,8 +318,8 @@ Status Plan::create(cvg_context* ctx, int dtype, int64_t n, int64_t k, int64_t m
   kp_ = padded_cols(k, m, dtype);
   tiles_ = gram_tiles(k, m, kp_);
   tiles128_ = dtype == 1 ? gram_tiles(k, m, kp_, kTileF32) : std::vector<int2>{};
-  i8_ = dtype == 0 ? fp64_i8_env() : fp32_i8_env();
-  slices_ = dtype == 0 ? i8_slices_env() : i8_slices_f32_env();
+  i8_ = dtype == 0 && fp64_i8_env();  // fp32 inputs: the scaled fp16 split (or 3xTF32), never int8 digits
+  slices_ = i8_slices_env();
   sample_ = i8_sample_env();
   tilesq_.clear();
   if (i8_) {  // 128 x 64 int8-Gram tiles covering the needed upper 64-tiles (i, j): I = i / 2, J = j

@@ -740,13 +740,9 @@ bool launch_reorder_q(int dtype, int slices, const void* x, int64_t ldx, const v
 #define CVG_K1Q(T, S)                                                                                              \
   return launch_k1q<T, S>(x, ldx, y, ldy, k, m, src_row, zrows, kp, c_begin, c_end, nsrc, shift, blkseg, segmax, \
                           headroom, ovf, zq, nonfinite, blk_lo, blk_hi, max_sms, s)
-  if (dtype == 0) {
-    if (slices == 5) CVG_K1Q(double, 5);
-    else CVG_K1Q(double, 6);
-  } else {
-    if (slices == 3) CVG_K1Q(float, 3);
-    else CVG_K1Q(float, 4);
-  }
+  (void)dtype;  // fp64 inputs only (fp32 inputs take the fp16-split Gram)
+  if (slices == 5) CVG_K1Q(double, 5);
+  CVG_K1Q(double, 6);
 #undef CVG_K1Q
 }
 
@@ -769,12 +765,8 @@ bool launch_gram_i8(int slices, const int8_t* zq, const unsigned long long* segm
                                        max_ctas, s)                                                                \
              : launch_gram_i8_s<S, 32>(zq, segmax, headroom, zrows, kp, segs, seg_base, nseg, tiles, ntiles, part, \
                                        max_ctas, s)
-  switch (slices) {
-    case 3: CVG_GRAM_I8(3);
-    case 4: CVG_GRAM_I8(4);
-    case 5: CVG_GRAM_I8(5);
-    default: CVG_GRAM_I8(6);
-  }
+  if (slices == 5) CVG_GRAM_I8(5);
+  CVG_GRAM_I8(6);
 #undef CVG_GRAM_I8
 }
 

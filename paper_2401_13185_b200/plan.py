@@ -370,9 +370,7 @@ def fp64_kind() -> str:
     return "dmma" if os.environ.get("CVG_FP64_KIND") == "dmma" else "i8"
 
 
-def i8_slices(f32: bool = False) -> int:
-    if f32:
-        return 3 if os.environ.get("CVG_I8_SLICES_F32") == "3" else 4
+def i8_slices() -> int:
     return 5 if os.environ.get("CVG_I8_SLICES") == "5" else 6
 
 
@@ -382,20 +380,19 @@ def i8_pairs(s: int) -> int:
 
 
 def fp32_kind() -> str:
-    """The fp32 Gram kind: "f16" (scaled fp16 hi/lo on kind::f16, default), "tf32" or "i8" (CVG_FP32_KIND)."""
-    v = os.environ.get("CVG_FP32_KIND")
-    return v if v in ("tf32", "i8") else "f16"
+    """The fp32 Gram kind: "f16" (scaled fp16 hi/lo on kind::f16, default) or "tf32" (CVG_FP32_KIND=tf32)."""
+    return "tf32" if os.environ.get("CVG_FP32_KIND") == "tf32" else "f16"
 
 
 def executed_gram_flops(n: int, k: int, m: int, p: int, f32: bool = False) -> float:
     """Tensor-core flops the Gram kernel issues for n rows (fold padding ignored):
     fp64: 64x64 DMMA tiles, diagonal tiles only their 36 upper 8x8 blocks;
     fp32: 128x128 tcgen05 tiles x 3 products (fp16 hi/lo split by default, TF32 with CVG_FP32_KIND=tf32)."""
-    if f32 and fp32_kind() != "i8":
+    if f32:
         return 3 * 2.0 * len(gram_tiles(k, m, 128)) * 128 * 128 * n
     tiles = gram_tiles(k, m)
-    if f32 or fp64_kind() == "i8":  # int8 ops: 128x64 tiles x slice pairs
+    if fp64_kind() == "i8":  # int8 ops: 128x64 tiles x slice pairs
         tq = {(i // 2, j) for i, j in tiles}
-        return 2.0 * len(tq) * 128 * 64 * n * i8_pairs(i8_slices(f32))
+        return 2.0 * len(tq) * 128 * 64 * n * i8_pairs(i8_slices())
     n_diag = sum(1 for i, j in tiles if i == j)
     return 2.0 * ((len(tiles) - n_diag) * 64 * 64 + n_diag * 36 * 64) * n
