@@ -68,12 +68,12 @@ __device__ __forceinline__ void mma_f16(uint32_t tmem_d, uint64_t a, uint64_t b,
 //
 // fp32 -> fp64 without F2F: F2F.F64.F32 issues at ~4 per clock per SM (XU), which made
 // the drain the kernel's bottleneck.  For t = f * 2^-e_j (fp32 bits u), the fp64 whose
-// bits are ((u & 0x7fffffff) >> 3, u << 29) is exactly |t| * 2^-896 (normal and
-// subnormal t alike, zero stays zero), so with M = 2^-e_i * 2^896 carrying t's sign,
+// bits are (sign(u) | ((u & 0x7fffffff) >> 3), u << 29) is exactly t * 2^-896 (normal and
+// subnormal t alike, +-0 stays +-0), so with M = 2^-e_i * 2^896,
 //     acc = fma(D, M, acc)  ==  fma((double)t, 2^-e_i, acc)    (bit for bit)
-// at 4 integer ops per element.
-__device__ __forceinline__ double fp32_bits_scaled(uint32_t u) {  // |t| * 2^-896, t = __uint_as_float(u)
-  return __hiloint2double((int)((u & 0x7fffffffu) >> 3), (int)(u << 29));
+// at 3 integer ops per element.
+__device__ __forceinline__ double fp32_bits_scaled_signed(uint32_t u) {
+  return __hiloint2double((int)((u & 0x80000000u) | ((u >> 3) & 0x0fffffffu)), (int)(u << 29));
 }
 
 template <typename Release>
@@ -94,8 +94,7 @@ __device__ __forceinline__ void drain_groups(uint32_t tmem_d, int q, int h, int 
     const int b = chunk & 1;
     __syncwarp();
     *reinterpret_cast<float2*>(tab + 2 * lane) = cs;
-    const double srow = (double)rs * 0x1p+896;  // 2^-e_i * 2^896 (e_i in [-64, 64]: a normal double)
-    const int m_hi = __double2hiint(srow), m_lo = __double2loint(srow);
+    const double mrow = (double)rs * 0x1p+896;  // 2^-e_i * 2^896 (e_i in [-64, 64]: a normal double)
     if (chunk + 1 < nchunks) {  // next group's factors, in flight during this drain
       uc += kp;
       ur += kp;
@@ -116,8 +115,7 @@ __device__ __forceinline__ void drain_groups(uint32_t tmem_d, int q, int h, int 
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           const uint32_t u = __float_as_uint(__uint_as_float(r[j + i]) * sc[i]);
-          const double msign = __hiloint2double(m_hi ^ (int)(u & 0x80000000u), m_lo);
-          acc64[c0 + j + i] = fma(fp32_bits_scaled(u), msign, acc64[c0 + j + i]);
+          acc64[c0 + j + i] = fma(fp32_bits_scaled_signed(u), mrow, acc64[c0 + j + i]);
         }
       }
     }
