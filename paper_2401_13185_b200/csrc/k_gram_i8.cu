@@ -33,6 +33,7 @@
 //               one A slice with adjacent B slices are one MMA of N = 64 .. 256
 //   warps 2..9  drain once per tile: Horner over the S accumulators, exact unscale
 #include <atomic>
+#include <type_traits>
 #include <cstdlib>
 
 #include "cvg_internal.cuh"
@@ -457,13 +458,14 @@ __global__ void __launch_bounds__(kSmThreads) segmax_kernel(const T* __restrict_
 
 // ---------------------------------------------------------------------------
 // K1Q: bucket, shift, scale by the segment exponent, cut into S int8 digits, write
-// Zq[t][blk][col][64].  A CTA item is one 64-row block x 64 columns; its S x 4 KB of
-// digits are assembled in shared memory in the operand's own SWIZZLE_64B layout and
-// leave by one TMA tensor store (full, contiguous 4 KB lines; double-buffered so the
-// next item's loads and cuts overlap the store).  Warp w owns columns 8w .. 8w + 7; lane
-// (j, qq) = (lane >> 2, lane & 3) holds column 8w + j of the row quads qq, qq + 4, qq + 8,
-// qq + 12 (16 rows; a warp load reads 64 contiguous bytes of 4 rows).  Each thread packs
-// a quad's 4 digits of one position into one word; with the SW64 XOR the 32 lanes' words
+// Zq[t][blk][col][64].  A CTA item is one 64-row block x 64 columns.  Warp w owns columns 8w .. 8w + 7 and
+// runs on its own: it assembles its S x 8 columns x 64 rows of digits (S x 512 B) in its own shared-memory
+// region in the operand's SWIZZLE_64B layout and sends them with its own TMA tensor store (8 contiguous 64 B
+// lines per slice; double-buffered so the next chunk's loads and cuts overlap the store).  The only CTA
+// barrier is one per 64-row block, publishing the row pointers of the block two ahead (triple-buffered), so
+// the warps drift past one another's load latencies.  Lane (j, qq) = (lane >> 2, lane & 3) holds column 8w + j
+// of the row quads qq, qq + 4, qq + 8, qq + 12 (16 rows; a warp load reads 64 contiguous bytes of 4 rows).
+// Each thread packs a quad's 4 digits of one position into one word; with the SW64 XOR the 32 lanes' words
 // land in 32 distinct banks.
 //
 // Digits: one fma gives V = round(z 2^(e + 8(S-1))) + O in the low 52 bits of
@@ -472,13 +474,11 @@ __global__ void __launch_bounds__(kSmThreads) segmax_kernel(const T* __restrict_
 // byte XOR 0x80 -- so sum_t d_t 2^-8t = round(w 2^8(S-1)) 2^-8(S-1) exactly (|w| < 127, while the
 // digits reach 128 - 128/255).  Four rows' digits of one byte position are one word of a 4 x 4
 // byte transpose (8 byte permutes for bytes 0-3, 4 for bytes 4-5).
-// PQ row quads per thread: 4 (256 threads, 16 rows per thread) or 2 (512 threads, 8 rows: twice the warps
-// to interleave loads with the cut).
-#ifndef CVG_K1Q_PQ
-#define CVG_K1Q_PQ 4
-#endif
-constexpr int kQ1PQ = CVG_K1Q_PQ;
-constexpr int kQ1Threads = 256 * 4 / kQ1PQ;
+//
+// Padding rows (src < 0) read through a row pointer aimed at the shift vector itself, so z = c_j - c_j = +0
+// with no per-value select; the ones column takes the block's padding mask.
+constexpr int kQ1Threads = 256;
+constexpr int kQ1PQ = 4;  // row quads per thread
 #ifndef CVG_K1Q_MIN_BLOCKS
 #define CVG_K1Q_MIN_BLOCKS 2
 #endif
@@ -489,8 +489,12 @@ struct DigitOffset {  // 128 * (256^S - 1) / 255: 0x80 in every byte of V
 };
 
 template <int S>
+constexpr int k1q_region_bytes() {  // one warp's S x 512 B of digits, 1 KB aligned
+  return (S * 512 + 1023) / 1024 * 1024;
+}
+template <int S>
 constexpr int k1q_smem_bytes() {
-  return 2 * S * 4096 + 1024;
+  return 2 * 8 * k1q_region_bytes<S>() + 1024;
 }
 
 __device__ __forceinline__ void tma_store_4d(const CUtensorMap* map, const void* src, int c0, int c1, int c2, int c3) {
@@ -508,22 +512,25 @@ __global__ void __launch_bounds__(kQ1Threads, CVG_K1Q_MIN_BLOCKS)
                      const double* __restrict__ shift, const int* __restrict__ blkseg,
                      const unsigned long long* __restrict__ segmax, int headroom, int* __restrict__ ovf,
                      int* __restrict__ nonfinite, int64_t blk_lo, int64_t blk_hi) {
-  // Blocks [blk_lo, blk_hi) of Z.
+  // Blocks [blk_lo, blk_hi) of Z.  map_out's box is {64, 8, 1, S}: one warp's columns.
   // Out of range: tt outside [2^52, 2^53) (a non-finite z, or w below the digits' range) or V >= 2^(7S)
   // (w above it).  With sampled exponents (ovf != null) that marks the block's segment for the exact
   // pass; otherwise (exact exponents, where only a non-finite z can get there) it is the
   // non-finite-input flag (DatasetPair's allFinite, core.hpp:43-44).
+  static_assert(std::is_same<T, double>::value, "padding rows read the (double) shift through the row pointers");
   static_assert(8 * S <= 48, "digits must fit the 52-bit window");
   constexpr uint32_t kHiMask = 8 * S >= 32 ? (0xfff00000u | (0x000fffffu & ~((1u << (8 * S - 32)) - 1u))) : 0xffffffffu;
   constexpr uint32_t kLoMask = 8 * S >= 32 ? 0u : ~((1u << (8 * S)) - 1u);
+  constexpr int kRegion = k1q_region_bytes<S>();
+  constexpr int NV = 4 * kQ1PQ;
   extern __shared__ uint8_t k1q_raw[];
   uint8_t* tiles = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(k1q_raw) + 1023) & ~uintptr_t(1023));
-  __shared__ int64_t s_src[2][QK];  // this block's and the next block's source rows
+  __shared__ const double* s_row[3][2][QK];  // per block: X and Y row pointers (padding: the shift)
+  __shared__ uint32_t s_pad[3][2];           // per block: padding-row mask
+  __shared__ int s_seg[3];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int j = lane >> 2, qq = lane & 3;
-  const int col = 8 * (w & 7) + j;  // column within the 64-column chunk
-  const int p0 = (w >> 3) * kQ1PQ;  // this thread's row quads: qq + 4p, p = p0 .. p0 + PQ - 1
-  constexpr int NV = 4 * kQ1PQ;
+  const int col = 8 * w + j;  // column within the 64-column chunk
   const int64_t wd = k + m;
   CVG_DCHECK(c_begin >= 0 && c_end <= kp && c_begin % 64 == 0 && zrows % QK == 0);
   const int64_t nchunk = (c_end - c_begin) / 64;
@@ -531,75 +538,93 @@ __global__ void __launch_bounds__(kQ1Threads, CVG_K1Q_MIN_BLOCKS)
   CVG_DCHECK(blk_lo >= 0 && blk_hi <= zrows / QK);
   const int64_t grid = gridDim.x;
   const double C = 0x1p52 + (double)DigitOffset<S>::v;
-  uint32_t oor = 0;  // out-of-range bits of this block's values
-  auto load_src = [&](int64_t b, int sb) {
-    if (threadIdx.x < QK && b < nblk) {
+  auto load_src = [&](int64_t b, int rb) {
+    if (threadIdx.x < QK && b < nblk) {  // warps 0 and 1, whole
       const int64_t src = src_row[b * QK + threadIdx.x];
       CVG_DCHECK(src < nsrc && src >= -1);
-      s_src[sb][threadIdx.x] = src;
+      s_row[rb][0][threadIdx.x] = src < 0 ? shift : x + src * ldx;
+      s_row[rb][1][threadIdx.x] = src < 0 || m == 0 ? shift + k : y + src * ldy;
+      const uint32_t pm = __ballot_sync(0xffffffffu, src < 0);
+      if (lane == 0) s_pad[rb][w] = pm;
+      if (threadIdx.x == 0) s_seg[rb] = blkseg[b];
     }
   };
-  // this thread's NV values of column c0 + col in block b (raw: the shift is applied at the cut)
-  double v[NV];
-  auto load_vals = [&](int sb, int64_t c0) {
+  // the next chunk's NV values, shift and sampled column max, loaded while the current chunk is cut and stored
+  double v[NV], shn = 0.0;
+  unsigned long long mxn = 0ull;
+  auto load_chunk = [&](int rb, int64_t c0) {
     const int64_t c = c0 + col;
-    const int kind = c < k ? 0 : c < wd ? 1 : c == wd ? 2 : 3;  // x, y, ones, padding
-    const T* base = kind == 0 ? x + c : y + (c - k);
-    const int64_t ld = kind == 0 ? ldx : ldy;
+    mxn = __ldg(segmax + (int64_t)s_seg[rb] * kp + c);
+    if (c < wd) {
+      shn = __ldg(shift + c);
+      const int h = c < k ? 0 : 1;
+      const int64_t cc = c < k ? c : c - k;
 #pragma unroll
-    for (int pp = 0; pp < kQ1PQ; ++pp)
+      for (int pp = 0; pp < kQ1PQ; ++pp)
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int64_t src = s_src[sb][4 * (qq + 4 * (p0 + pp)) + i];
-        v[4 * pp + i] = src < 0 ? 0.0 : kind <= 1 ? (double)__ldg(base + src * ld) : kind == 2 ? 1.0 : 0.0;
-      }
+        for (int i = 0; i < 4; ++i) v[4 * pp + i] = __ldg(s_row[rb][h][4 * (qq + 4 * pp) + i] + cc);
+    } else {
+      shn = 0.0;
+      const uint64_t pad = s_pad[rb][0] | (uint64_t)s_pad[rb][1] << 32;
+#pragma unroll
+      for (int pp = 0; pp < kQ1PQ; ++pp)
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          v[4 * pp + i] = c == wd && !((pad >> (4 * (qq + 4 * pp) + i)) & 1) ? 1.0 : 0.0;  // ones / padding
+    }
   };
   int64_t blk = blk_lo + blockIdx.x;
   load_src(blk, 0);
   load_src(blk + grid, 1);
   __syncthreads();
-  if (blk < nblk) load_vals(0, c_begin);
-  int buf = 0, sb = 0;
-  for (; blk < nblk; blk += grid, sb ^= 1) {
-    const int seg = blkseg[blk];
-    const unsigned long long* smx = segmax + (int64_t)seg * kp;
+  if (blk < nblk) load_chunk(0, c_begin);
+  int buf = 0, rb = 0;
+  uint32_t oor_hi = 0, oor_lo = 0;  // out-of-range bits of this block's values
+  for (; blk < nblk; blk += grid, rb = rb == 2 ? 0 : rb + 1) {
+    const int rn = rb == 2 ? 0 : rb + 1;
+    const int seg = s_seg[rb];
     for (int64_t ch = 0; ch < nchunk; ++ch, buf ^= 1) {
       const int64_t c0 = c_begin + 64 * ch;
-      const int64_t c = c0 + col;
-      const double sh = c < wd ? shift[c] : 0.0;
-      const unsigned long long mxb = smx[c];
+      const double sh = shn;
+      const unsigned long long mxb = mxn;
       const CutScale cs = cut_scales(seg_exponent(__longlong_as_double((long long)mxb), headroom) + 8 * (S - 1));
       // a sampled max of 0 cannot scale the column: any nonzero value sends the segment to the exact pass
       const bool zero_col = ovf && mxb == 0ull;
       uint32_t lo[NV], hi[NV];
+      if (cs.pre == 1.0 && !zero_col) {
 #pragma unroll
-      for (int pp = 0; pp < kQ1PQ; ++pp)
+        for (int e = 0; e < NV; ++e) {
+          const double tt = fma(__dsub_rn(v[e], sh), cs.sc, C);
+          lo[e] = (uint32_t)__double2loint(tt);
+          hi[e] = (uint32_t)__double2hiint(tt);
+          oor_hi |= hi[e] ^ 0x43300000u;
+          oor_lo |= lo[e];
+        }
+      } else {
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int e = 4 * pp + i;
-          const bool real = s_src[sb][4 * (qq + 4 * (p0 + pp)) + i] >= 0 && c < wd;
-          double z = real ? __dsub_rn(v[e], sh) : v[e];
+        for (int e = 0; e < NV; ++e) {
+          double z = __dsub_rn(v[e], sh);
           if (cs.pre != 1.0) z = __dmul_rn(z, cs.pre);
           const double tt = fma(z, cs.sc, C);
           lo[e] = (uint32_t)__double2loint(tt);
           hi[e] = (uint32_t)__double2hiint(tt);
-          oor |= ((hi[e] ^ 0x43300000u) & kHiMask) | (lo[e] & kLoMask);
-          if (zero_col) oor |= z != 0.0;
+          oor_hi |= (hi[e] ^ 0x43300000u) | (zero_col && z != 0.0 ? 0x80000000u : 0u);
+          oor_lo |= lo[e];
         }
+      }
       // next chunk's loads in flight while this one is cut and stored
       if (ch + 1 < nchunk)
-        load_vals(sb, c0 + 64);
+        load_chunk(rb, c0 + 64);
       else if (blk + grid < nblk)
-        load_vals(sb ^ 1, c_begin);
-      // this buffer's previous TMA store has finished reading shared memory
-      if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");
-      __syncthreads();
-      uint8_t* tile = tiles + buf * (S * 4096);
+        load_chunk(rn, c_begin);
+      uint8_t* region = tiles + buf * (8 * kRegion) + w * kRegion;
+      // this warp's previous TMA store from this buffer has finished reading shared memory
+      if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");
+      __syncwarp();
 #pragma unroll
       for (int pp = 0; pp < kQ1PQ; ++pp) {
-        const int p = p0 + pp;
-        // quad q = qq + 4p of column col, SWIZZLE_64B: 16-byte chunk (q >> 2) ^ ((col >> 1) & 3)
-        const int off = col * 64 + ((p ^ ((col >> 1) & 3)) << 4) + (qq << 2);
+        // quad q = qq + 4 pp of line j, SWIZZLE_64B: 16-byte chunk (q >> 2) ^ ((j >> 1) & 3)
+        const int off = j * 64 + ((pp ^ ((j >> 1) & 3)) << 4) + (qq << 2);
         // 4 x 4 byte transposes: word b = byte b of the 4 rows' V (low word: bytes 0-3, high word: 4-5)
         const uint32_t* L = lo + 4 * pp;
         const uint32_t* H = hi + 4 * pp;
@@ -619,24 +644,23 @@ __global__ void __launch_bounds__(kQ1Threads, CVG_K1Q_MIN_BLOCKS)
         }
 #pragma unroll
         for (int d = 0; d < S; ++d)  // digit d = byte S-1-d; offset binary -> two's complement: ^ 0x80
-          *reinterpret_cast<uint32_t*>(tile + d * 4096 + off) = wb[S - 1 - d] ^ 0x80808080u;
+          *reinterpret_cast<uint32_t*>(region + d * 512 + off) = wb[S - 1 - d] ^ 0x80808080u;
       }
       asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        tma_store_4d(&map_out, tile, 0, (int)c0, (int)blk, 0);
+      __syncwarp();
+      if (lane == 0) {
+        tma_store_4d(&map_out, region, 0, (int)c0 + 8 * w, (int)blk, 0);
         asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
       }
     }
+    const uint32_t oor = (oor_hi & kHiMask) | (oor_lo & kLoMask);
     if (__any_sync(0xffffffffu, oor != 0u) && lane == 0) atomicOr(ovf ? ovf + seg : nonfinite, 1);
-    oor = 0;
-    // s_src[sb] is free (the next block's prefetch used sb ^ 1): fill it for block + 2 grid; the
-    // second barrier publishes it before a one-chunk block's prefetch reads it
-    __syncthreads();
-    load_src(blk + 2 * grid, sb);
+    oor_hi = oor_lo = 0;
+    // every warp is past its reads of the block before this one: its buffer takes the block two ahead
+    load_src(blk + 2 * grid, rb == 0 ? 2 : rb - 1);
     __syncthreads();
   }
-  if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
+  if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
 }
 
 // 4-D map over Zq: {64 rows, kp, zrows / 64, S} bytes, box {64, box_cols, 1, S}, SWIZZLE_64B.
@@ -679,7 +703,7 @@ bool launch_k1q(const void* x, int64_t ldx, const void* y, int64_t ldy, int64_t 
                 const int* blkseg, const unsigned long long* segmax, int headroom, int* ovf, int8_t* zq, int* nonfinite,
                 int64_t blk_lo, int64_t blk_hi, int max_sms, cudaStream_t s) {
   CUtensorMap mo;
-  if (!make_zq_map(&mo, zq, zrows, kp, S, 64)) return false;
+  if (!make_zq_map(&mo, zq, zrows, kp, S, 8)) return false;
   constexpr int smem = k1q_smem_bytes<S>();
   // grid-stride over one wave of resident CTAs.  Function attributes are per device (one process may drive
   // several: cvg_context_create_multi), so they are set on every launch; the occupancy query is cached per device.
