@@ -167,7 +167,7 @@ void launch_reorder_split_t(int dtype, const void* x, int64_t ldx, const void* y
 // K1H + K2h (fp32 inputs, default): bucket/shift, per-(G-row group, column) power-of-two
 // scaling, fp16 hi + lo split into Zh[row / 64][col][64]; then the tcgen05 kind::f16 Gram
 // (3 products, fp32 TMEM chunks of one row group, exact unscale into fp64).  k_gram_f16.cu.
-void launch_reorder_split_h(int dtype, const void* x, int64_t ldx, const void* y, int64_t ldy, int64_t k, int64_t m,
+bool launch_reorder_split_h(int dtype, const void* x, int64_t ldx, const void* y, int64_t ldy, int64_t k, int64_t m,
                             const int64_t* src_row, int64_t zrows, int64_t kp, int64_t c_begin, int64_t c_end,
                             int64_t nsrc, const double* shift, int group_rows, void* zh_hi, void* zh_lo,
                             float* unscale, int* nonfinite, cudaStream_t s);

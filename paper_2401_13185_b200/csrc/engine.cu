@@ -661,11 +661,12 @@ Status Plan::gram(const void* d_x, int64_t ldx, const void* d_y, int64_t ldy, co
     if (zrows_ > 0) {
       {
         Timed t(ctx_, kReorder);
-        if (f16_path())
-          launch_reorder_split_h(dtype_, d_x, ldx, d_y, ldy, k_, m_, rows, zrows_, kp_, 0, kp_, nsrc, shift,
-                                 (int)row_step_, zt_hi_.as<void>(), zt_lo_.as<void>(), unscale_.as<float>(),
-                                 flag_.as<int>(), s);
-        else
+        if (f16_path()) {
+          if (!launch_reorder_split_h(dtype_, d_x, ldx, d_y, ldy, k_, m_, rows, zrows_, kp_, 0, kp_, nsrc, shift,
+                                      (int)row_step_, zt_hi_.as<void>(), zt_lo_.as<void>(), unscale_.as<float>(),
+                                      flag_.as<int>(), s))
+            return Status::Err(5, "cuTensorMapEncodeTiled unavailable or rejected the operand layout");
+        } else
           launch_reorder_split_t(dtype_, d_x, ldx, d_y, ldy, k_, m_, rows, zrows_, kp_, 0, kp_, shift,
                                  zt_hi_.as<float>(), zt_lo_.as<float>(), flag_.as<int>(), s);
       }
@@ -863,9 +864,10 @@ Status Plan::gram_host(const void* h_x, const void* h_y, void* d_x, void* d_y, c
       {
         Timed t(ctx_, kReorder);
         if (f16_path()) {
-          launch_reorder_split_h(dtype_, d_x, k_, d_y, m_, k_, m_, src_row_.as<int64_t>(), zrows_, kp_, z0, z1, src_n_,
-                                 shift, (int)row_step_, zt_hi_.as<void>(), zt_lo_.as<void>(), unscale_.as<float>(),
-                                 flag_.as<int>(), s);
+          if (!launch_reorder_split_h(dtype_, d_x, k_, d_y, m_, k_, m_, src_row_.as<int64_t>(), zrows_, kp_, z0, z1,
+                                      src_n_, shift, (int)row_step_, zt_hi_.as<void>(), zt_lo_.as<void>(),
+                                      unscale_.as<float>(), flag_.as<int>(), s))
+            return Status::Err(5, "cuTensorMapEncodeTiled unavailable or rejected the operand layout");
         }
         else if (dtype_ == 1)
           launch_reorder_split_t(dtype_, d_x, k_, d_y, m_, k_, m_, src_row_.as<int64_t>(), zrows_, kp_, z0, z1, shift,

@@ -236,23 +236,19 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 // K1H: bucket, shift, scale, fp16-split, transpose into Zh[block][col][64] (HBM-bound).
-// One CTA per G bucketed rows, two CTAs per SM (one loads while the other
-// computes); 64-column chunks.  Lane (h, cq) = (lane >> 4, lane & 15) holds the 4
-// adjacent columns c0 + 4cq .. + 3 (one 16-byte load per row: a warp reads two
-// 256-byte row segments) of the row pairs rp = 2w + h + 32j of warp w.  A column's
-// group max is a 32-way reduction in shared memory; each (hi, lo) row pair is one
-// 32-bit word of a column-major shared tile whose row-pair index is XOR-swizzled
-// by the column quad (word = col * G/2 + (rp ^ 2(col >> 2))): the transposed
-// writes hit 32 distinct banks and the write-out reads 16-byte blocks
-// conflict-free, so the output leaves as 16-byte stores (a warp: 4 columns x 128 B
-// contiguous).
-constexpr int kK1hThreads = 512;
-constexpr int kK1hWarps = kK1hThreads / 32;
+// One CTA per G bucketed rows; warp w owns the 8 columns c0 + 8w .. + 7 of every 64-column chunk over all G rows
+// and runs on its own (the group's per-column exponent is a reduction within the warp), so the warps drift past
+// one another's load latencies with no CTA barrier after the row indices are in.  Lane (rq, h) = (lane >> 1,
+// lane & 1) holds columns 4h .. 4h + 3 of the row pairs rp = 16 i + rq (rows 2 rp, 2 rp + 1): a warp load reads
+// 16 rows' 32-byte segments (whole sectors).  Each (hi, lo) row pair is one 32-bit word of the warp's shared
+// tile [block][col][64 rows] in the SWIZZLE_128B layout (16-byte chunk (word >> 2) ^ col): the 32 lanes' words
+// land in 32 distinct banks, and the tile leaves by one TMA tensor store per plane (4 KB at G = 256).
+constexpr int kK1hThreads = 256;
 constexpr int kK1hCols = 64;
 
 template <int G>
-constexpr int k1h_smem_bytes() {
-  return 2 * kK1hCols * (G / 2) * 4 + 2 * kK1hWarps * kK1hCols * 4 + kK1hCols * 4 + G * 8;
+constexpr int k1h_smem_bytes() {  // per warp: hi and lo planes of (G / 64) x 8 columns x 128 B
+  return 8 * 2 * (G / 64) * 1024 + 1024;
 }
 
 template <typename T>
@@ -266,102 +262,95 @@ __device__ __forceinline__ void load4(const T* p, float (&v)[4]) {
   }
 }
 
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void* src, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];\n" ::"l"(map),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2)
+               : "memory");
+}
+
 template <typename T, int G>
 __global__ void __launch_bounds__(kK1hThreads, 2) reorder_split_h_kernel(
-    const T* __restrict__ x, int64_t ldx, const T* __restrict__ y, int64_t ldy, int64_t k, int64_t m,
-    const int64_t* __restrict__ src_row, int64_t zrows, int64_t kp, int64_t c_begin, int64_t c_end, int64_t nsrc,
-    const double* __restrict__ shift, __half* __restrict__ zh_hi, __half* __restrict__ zh_lo,
+    const __grid_constant__ CUtensorMap map_hi, const __grid_constant__ CUtensorMap map_lo, const T* __restrict__ x,
+    int64_t ldx, const T* __restrict__ y, int64_t ldy, int64_t k, int64_t m, const int64_t* __restrict__ src_row,
+    int64_t zrows, int64_t kp, int64_t c_begin, int64_t c_end, int64_t nsrc, const double* __restrict__ shift,
     float* __restrict__ unscale, int* __restrict__ nonfinite) {
-  constexpr int S = G / 2;    // words (row pairs) per column
-  constexpr int NJ = G / 64;  // row pairs per thread
-  constexpr int kSlots = 2 * kK1hWarps;  // row-pair slots per 32 row pairs (= 32)
-  extern __shared__ __align__(16) uint8_t k1h_smem[];
-  uint32_t* s_hi = reinterpret_cast<uint32_t*>(k1h_smem);
-  uint32_t* s_lo = s_hi + kK1hCols * S;
-  float* s_max = reinterpret_cast<float*>(s_lo + kK1hCols * S);  // [slot][cols]
-  float* s_scale = s_max + kSlots * kK1hCols;                     // [cols] 2^e
-  int64_t* s_src = reinterpret_cast<int64_t*>(s_scale + kK1hCols);
+  // map_hi / map_lo: Zh planes as {64 rows, kp, zrows / 64} halves, box {64, 8, G / 64}, SWIZZLE_128B.
+  constexpr int NB = G / 64;  // 64-row blocks per group
+  constexpr int NI = G / 32;  // row-pair batches per thread
+  extern __shared__ uint8_t k1h_raw[];
+  uint8_t* tiles = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(k1h_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ int64_t s_src[G];
   const int64_t grp = blockIdx.x;
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
-  const int h = lane >> 4, cq = lane & 15;
-  const int slot = 2 * w + h;  // this thread's row pairs: slot + 32j
+  const int h = lane & 1, rq = lane >> 1;
   const int64_t wd = k + m;
   CVG_DCHECK(c_begin >= 0 && c_end <= kp && c_begin % kK1hCols == 0 && zrows % G == 0);
+  bool real = true;
   for (int i = t; i < G; i += kK1hThreads) {
     const int64_t r = grp * G + i;
     const int64_t src = r < zrows ? src_row[r] : -1;
     CVG_DCHECK(src < nsrc);
     s_src[i] = src;
+    real &= src >= 0;
   }
-  __syncthreads();
-  bool all_real = true;
-#pragma unroll
-  for (int j = 0; j < NJ; ++j)
-#pragma unroll
-    for (int p = 0; p < 2; ++p) all_real &= s_src[2 * (slot + 32 * j) + p] >= 0;
+  const bool all_real = __syncthreads_and(real);
   // 16-byte row loads need 16-byte aligned rows
   const bool vec_ok = (ldx * (int64_t)sizeof(T)) % 16 == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0;
+  uint8_t* plane_hi = tiles + w * (2 * NB * 1024);
+  uint8_t* plane_lo = plane_hi + NB * 1024;
   float nan_acc = 0.f;  // v * 0 is NaN exactly when v is not finite
   bool too_big = false;
-  float v[NJ][2][4];
-  // Fast chunks (every column an X column, every row real, aligned rows): no per-element checks.
-  auto fast_chunk = [&](int64_t c0) { return all_real && vec_ok && c0 + kK1hCols <= k; };
-  auto load_chunk = [&](int64_t c0) {
-    if (fast_chunk(c0)) {
-#pragma unroll
-      for (int j = 0; j < NJ; ++j)
-#pragma unroll
-        for (int p = 0; p < 2; ++p)
-          load4(x + (int64_t)(int32_t)s_src[2 * (slot + 32 * j) + p] * ldx + c0 + 4 * cq, v[j][p]);
-      return;
-    }
-#pragma unroll
-    for (int j = 0; j < NJ; ++j)
-#pragma unroll
-      for (int p = 0; p < 2; ++p) {
-        const int64_t src = s_src[2 * (slot + 32 * j) + p];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const int64_t ce = c0 + 4 * cq + e;
-          float val = 0.f;
-          if (src >= 0) {
-            if (ce < k)
-              val = (float)__ldg(x + src * ldx + ce);
-            else if (ce < wd)
-              val = (float)__ldg(y + src * ldy + (ce - k));
-            else if (ce == wd)
-              val = 1.f;  // ones column: column sums ride in the Gram
-          }
-          v[j][p][e] = val;
-        }
-      }
-  };
-  load_chunk(c_begin);
   for (int64_t c0 = c_begin; c0 < c_end; c0 += kK1hCols) {
-    // shift; per-column max |z| over this thread's rows
-    const bool fast = fast_chunk(c0);
+    const int64_t cw = c0 + 8 * w;  // the warp's columns
+    const int64_t cb = cw + 4 * h;  // this thread's
+    // Fast warps (every column an X column, every row real, aligned rows): no per-element checks.
+    const bool fast = all_real && vec_ok && cw + 8 <= k;
+    float z[NI][2][4];
+    if (fast) {
+#pragma unroll
+      for (int i = 0; i < NI; ++i)
+#pragma unroll
+        for (int p = 0; p < 2; ++p) load4(x + (int64_t)(int32_t)s_src[32 * i + 2 * rq + p] * ldx + cb, z[i][p]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < NI; ++i)
+#pragma unroll
+        for (int p = 0; p < 2; ++p) {
+          const int64_t src = s_src[32 * i + 2 * rq + p];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int64_t ce = cb + e;
+            float val = 0.f;
+            if (src >= 0) {
+              if (ce < k)
+                val = (float)__ldg(x + src * ldx + ce);
+              else if (ce < wd)
+                val = (float)__ldg(y + src * ldy + (ce - k));
+              else if (ce == wd)
+                val = 1.f;  // ones column: column sums ride in the Gram
+            }
+            z[i][p][e] = val;
+          }
+        }
+    }
+    // shift; per-column max |z| over the group's rows (this thread's, then the 16 lanes of its column half)
+    float sc[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      const int64_t ce = c0 + 4 * cq + e;
+      const int64_t ce = cb + e;
       const float sh = ce < wd ? (float)__ldg(shift + ce) : 0.f;  // ones / padding columns: no shift
       float mx = 0.f;
 #pragma unroll
-      for (int j = 0; j < NJ; ++j)
+      for (int i = 0; i < NI; ++i)
 #pragma unroll
         for (int p = 0; p < 2; ++p) {
-          nan_acc = fmaf(v[j][p][e], 0.f, nan_acc);
-          const bool shifted = fast || (s_src[2 * (slot + 32 * j) + p] >= 0 && ce < wd);
-          const float z = shifted ? v[j][p][e] - sh : v[j][p][e];
-          v[j][p][e] = z;
-          mx = fmaxf(mx, fabsf(z));
+          nan_acc = fmaf(z[i][p][e], 0.f, nan_acc);
+          const bool shifted = fast || (s_src[32 * i + 2 * rq + p] >= 0 && ce < wd);
+          if (shifted) z[i][p][e] -= sh;
+          mx = fmaxf(mx, fabsf(z[i][p][e]));
         }
-      s_max[slot * kK1hCols + 4 * cq + e] = mx;
-    }
-    __syncthreads();
-    if (t < kK1hCols) {
-      float mx = 0.f;
 #pragma unroll
-      for (int i = 0; i < kSlots; ++i) mx = fmaxf(mx, s_max[i * kK1hCols + t]);
+      for (int o = 2; o < 32; o <<= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
       // e: the group's max |z| scaled into [2^14, 2^15); zero / non-finite columns keep e = 0
       int ex = 0;
       if (mx > 0.f && isfinite(mx)) {
@@ -370,76 +359,70 @@ __global__ void __launch_bounds__(kK1hThreads, 2) reorder_split_h_kernel(
         too_big |= ex < -64;  // |z| >= 2^79: products beyond the fp32 accumulation range
         ex = max(-64, min(64, ex));
       }
-      s_scale[t] = __uint_as_float((uint32_t)(127 + ex) << 23);
-      unscale[grp * kp + c0 + t] = __uint_as_float((uint32_t)(127 - ex) << 23);
+      sc[e] = __uint_as_float((uint32_t)(127 + ex) << 23);
+      if (rq == 0) unscale[grp * kp + ce] = __uint_as_float((uint32_t)(127 - ex) << 23);
     }
-    __syncthreads();
-    // scale (exact) and split: hi = fp16_rn(z'), lo = fp16_rn(z' - hi); one word per row pair,
-    // at col * S + (rp ^ 2cq) (col >> 2 == cq)
+    // this warp's previous TMA stores have finished reading its tile
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+    __syncwarp();
+    // scale (exact) and split: hi = fp16_rn(z'), lo = fp16_rn(z' - hi); row pair rp = 16 i + rq is word
+    // rp & 31 of block rp >> 5 = i >> 1, line (block, column 4h + e), 16-byte chunk (word >> 2) ^ column
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const int col = 4 * cq + e;
-      const float sc = s_scale[col];
+    for (int i = 0; i < NI; ++i) {
+      const int word = 16 * (i & 1) + rq;
 #pragma unroll
-      for (int j = 0; j < NJ; ++j) {
-        const float z0 = v[j][0][e] * sc, z1 = v[j][1][e] * sc;
+      for (int e = 0; e < 4; ++e) {
+        const int col = 4 * h + e;
+        const float z0 = z[i][0][e] * sc[e], z1 = z[i][1][e] * sc[e];
         const __half2 hi = __floats2half2_rn(z0, z1);
         const float2 hf = __half22float2(hi);
         const __half2 lo = __floats2half2_rn(z0 - hf.x, z1 - hf.y);
-        const int word = col * S + ((slot + 32 * j) ^ (2 * cq));
-        s_hi[word] = *reinterpret_cast<const uint32_t*>(&hi);
-        s_lo[word] = *reinterpret_cast<const uint32_t*>(&lo);
+        const int off = ((i >> 1) * 8 + col) * 128 + (((word >> 2) ^ col) << 4) + ((word & 3) << 2);
+        *reinterpret_cast<uint32_t*>(plane_hi + off) = *reinterpret_cast<const uint32_t*>(&hi);
+        *reinterpret_cast<uint32_t*>(plane_lo + off) = *reinterpret_cast<const uint32_t*>(&lo);
       }
     }
-    __syncthreads();
-    if (c0 + kK1hCols < c_end) load_chunk(c0 + kK1hCols);  // in flight while the stores below drain
-    // write: task = (64-row block b, column quad q): lane i -> column 4q + i / 8, words 4(i % 8) .. + 3
-    // of the block (16 B; a warp stores 4 columns x 128 B contiguous) for hi and for lo.
-    const int mq = lane & 7, cl = lane >> 3;
-#pragma unroll 2
-    for (int task = w; task < (G / 64) * (kK1hCols / 4); task += kK1hWarps) {
-      const int b = task / (kK1hCols / 4), q = task - b * (kK1hCols / 4);
-      const int col = 4 * q + cl;
-      // row pairs 32b + 4mq + r (r < 4) are stored at 32b + ((4mq + r) ^ 2q): one 16-B block, words permuted
-      const int word = col * S + 32 * b + 4 * (mq ^ (q >> 1));
-      const uint4 hv = *reinterpret_cast<const uint4*>(s_hi + word);
-      const uint4 lv = *reinterpret_cast<const uint4*>(s_lo + word);
-      const bool sw = q & 1;  // warp-uniform: words r ^ 2
-      const uint4 ho = sw ? make_uint4(hv.z, hv.w, hv.x, hv.y) : hv;
-      const uint4 lo = sw ? make_uint4(lv.z, lv.w, lv.x, lv.y) : lv;
-      const int64_t off = ((grp * (G / 64) + b) * kp + c0 + col) * 32 + 4 * mq;  // words
-      *reinterpret_cast<uint4*>(reinterpret_cast<uint32_t*>(zh_hi) + off) = ho;
-      *reinterpret_cast<uint4*>(reinterpret_cast<uint32_t*>(zh_lo) + off) = lo;
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    __syncwarp();
+    if (lane == 0) {
+      tma_store_3d(&map_hi, plane_hi, 0, (int)cw, (int)(grp * NB));
+      tma_store_3d(&map_lo, plane_lo, 0, (int)cw, (int)(grp * NB));
+      asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
     }
-    __syncthreads();
   }
+  if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
   // bit 0: a non-finite input; bit 1: a finite magnitude the fp32 accumulation cannot hold
   const unsigned bad = __ballot_sync(0xffffffffu, nan_acc != 0.f), big = __ballot_sync(0xffffffffu, too_big);
   if (lane == 0 && (bad | big)) atomicOr(nonfinite, (bad ? 1 : 0) | (big ? 2 : 0));
 }
 
 template <typename T, int G>
-void launch_k1h(const void* x, int64_t ldx, const void* y, int64_t ldy, int64_t k, int64_t m, const int64_t* src_row,
+bool launch_k1h(const void* x, int64_t ldx, const void* y, int64_t ldy, int64_t k, int64_t m, const int64_t* src_row,
                 int64_t zrows, int64_t kp, int64_t c_begin, int64_t c_end, int64_t nsrc, const double* shift,
                 __half* zh_hi, __half* zh_lo, float* unscale, int* nonfinite, cudaStream_t s) {
+  CUtensorMap mh, ml;
+  if (!make_blocked_map(&mh, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, zh_hi, 2, zrows, kp, 8, G / 64) ||
+      !make_blocked_map(&ml, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, zh_lo, 2, zrows, kp, 8, G / 64))
+    return false;
   constexpr int smem = k1h_smem_bytes<G>();
   cudaFuncSetAttribute(reorder_split_h_kernel<T, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   reorder_split_h_kernel<T, G><<<(unsigned)(zrows / G), kK1hThreads, smem, s>>>(
-      (const T*)x, ldx, (const T*)y, ldy, k, m, src_row, zrows, kp, c_begin, c_end, nsrc, shift, zh_hi, zh_lo,
-      unscale, nonfinite);
+      mh, ml, (const T*)x, ldx, (const T*)y, ldy, k, m, src_row, zrows, kp, c_begin, c_end, nsrc, shift, unscale,
+      nonfinite);
+  return true;
 }
 
 }  // namespace
 
-void launch_reorder_split_h(int dtype, const void* x, int64_t ldx, const void* y, int64_t ldy, int64_t k, int64_t m,
+bool launch_reorder_split_h(int dtype, const void* x, int64_t ldx, const void* y, int64_t ldy, int64_t k, int64_t m,
                             const int64_t* src_row, int64_t zrows, int64_t kp, int64_t c_begin, int64_t c_end,
                             int64_t nsrc, const double* shift, int group_rows, void* zh_hi, void* zh_lo,
                             float* unscale, int* nonfinite, cudaStream_t s) {
-  if (zrows <= 0 || c_end <= c_begin) return;
+  if (zrows <= 0 || c_end <= c_begin) return true;
   __half* hi = static_cast<__half*>(zh_hi);
   __half* lo = static_cast<__half*>(zh_lo);
 #define CVG_K1H(T, G)                                                                                         \
-  launch_k1h<T, G>(x, ldx, y, ldy, k, m, src_row, zrows, kp, c_begin, c_end, nsrc, shift, hi, lo, unscale, \
+  return launch_k1h<T, G>(x, ldx, y, ldy, k, m, src_row, zrows, kp, c_begin, c_end, nsrc, shift, hi, lo, unscale, \
                    nonfinite, s)
   if (dtype == 0) {
     if (group_rows == 256) CVG_K1H(double, 256);

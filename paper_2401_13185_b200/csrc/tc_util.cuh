@@ -134,13 +134,13 @@ inline EncodeTiledFn encode_fn() {
 // Blocked-transposed operand Zt[block][col][rows_per_block] (rows_per_block * elem = 128 B):
 // 3-D map {rows_per_block, kp, nblocks}, box {rows_per_block, box_cols, 1}, 128B swizzle.
 inline bool make_blocked_map(CUtensorMap* map, CUtensorMapDataType dt, const void* base, int elem_bytes,
-                             int64_t zrows, int64_t kp, int box_cols) {
+                             int64_t zrows, int64_t kp, int box_cols, int box_blocks = 1) {
   EncodeTiledFn enc = encode_fn();
   if (!enc) return false;
   const int rpb = 128 / elem_bytes;
   const cuuint64_t dims[3] = {(cuuint64_t)rpb, (cuuint64_t)kp, (cuuint64_t)(zrows / rpb)};
   const cuuint64_t strides[2] = {(cuuint64_t)128, (cuuint64_t)kp * 128};
-  const cuuint32_t box[3] = {(cuuint32_t)rpb, (cuuint32_t)box_cols, 1};
+  const cuuint32_t box[3] = {(cuuint32_t)rpb, (cuuint32_t)box_cols, (cuuint32_t)box_blocks};
   const cuuint32_t estr[3] = {1, 1, 1};
   return enc(map, dt, 3, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
              CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
