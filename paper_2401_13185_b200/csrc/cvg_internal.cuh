@@ -138,10 +138,11 @@ void launch_fold_stats(const double* total, const double* const* foldG, const in
                        int64_t k, int64_t m, int64_t kp, const double* shift, FoldStatsDev st, double* mean_x,
                        double* mean_y, double* std_x, double* std_y, int* nonfinite, cudaStream_t s,
                        SmallFolds sf = SmallFolds());
-void launch_products(const double* total, const double* const* foldG, const int64_t* n_val, int nfold, int64_t n,
-                     int64_t k, int64_t m, int64_t kp, const double* shift, FoldStatsDev st, const int2* tiles,
-                     int ntiles, const uint32_t* cfgs, int ncfg, double* xtx, double* xty, cudaStream_t s,
-                     SmallFolds sf = SmallFolds());
+// tiles[0, ndiag) are the diagonal tiles; returns the number of kernels launched.
+int launch_products(const double* total, const double* const* foldG, const int64_t* n_val, int nfold, int64_t n,
+                    int64_t k, int64_t m, int64_t kp, const double* shift, FoldStatsDev st, const int2* tiles,
+                    int ntiles, int ndiag, const uint32_t* cfgs, int ncfg, double* xtx, double* xty, cudaStream_t s,
+                    SmallFolds sf = SmallFolds());
 // div_rn_fast vs __ddiv_rn over n hashed operand pairs: counts[0] += mismatches, counts[1] += fast-path quotients.
 void launch_selftest_division(uint64_t seed, int64_t n, unsigned long long* counts, cudaStream_t s);
 void launch_unshift_global(const double* total, int64_t n, int64_t k, int64_t m, int64_t kp, const double* shift,

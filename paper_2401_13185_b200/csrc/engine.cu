@@ -337,9 +337,13 @@ Status Plan::create(cvg_context* ctx, int dtype, int64_t n, int64_t k, int64_t m
     CVG_CK(cudaMemcpyAsync(tilesq_d_.as<int2>(), tilesq_.data(), tilesq_.size() * sizeof(int2), cudaMemcpyHostToDevice,
                            ctx->stream));
   }
+  // output tiles, the diagonal ones first (launch_products sends the rest to the warp-owned kernel)
   out_tiles_.clear();
   for (const int2& t : tiles_)
-    if ((int64_t)t.x * kTile < k) out_tiles_.push_back(t);
+    if ((int64_t)t.x * kTile < k && t.x == t.y) out_tiles_.push_back(t);
+  out_ndiag_ = (int)out_tiles_.size();
+  for (const int2& t : tiles_)
+    if ((int64_t)t.x * kTile < k && t.x != t.y) out_tiles_.push_back(t);
   CVG_CK(cudaSetDevice(ctx->device));
   CVG_TRY(tiles_d_.ensure(tiles_.size() * sizeof(int2)));
   CVG_TRY(out_tiles_d_.ensure(out_tiles_.size() * sizeof(int2)));
@@ -963,12 +967,13 @@ Status Plan::finish(const double* d_rank_partials, int32_t n_ranks, const double
   if (ncfg > 0) {
     CVG_TRY(cfg_d_.ensure(sizeof(uint32_t) * ncfg));
     CVG_TRY(cfg_stage_.upload({{cfgs, sizeof(uint32_t) * ncfg, cfg_d_.as<void>()}}, s));
+    int nl = 0;
     {
       Timed t(ctx_, kProducts);
-      launch_products(total, fptr, nval, nown, n_, k_, m_, kp_, shift_.as<double>(), st, out_tiles_d_.as<int2>(),
-                      (int)out_tiles_.size(), cfg_d_.as<uint32_t>(), ncfg, d_xtx, d_xty, s, sf);
+      nl = launch_products(total, fptr, nval, nown, n_, k_, m_, kp_, shift_.as<double>(), st, out_tiles_d_.as<int2>(),
+                           (int)out_tiles_.size(), out_ndiag_, cfg_d_.as<uint32_t>(), ncfg, d_xtx, d_xty, s, sf);
     }
-    CVG_TRY(count_launch());
+    CVG_TRY(count_launch(nl));
   }
   int flag = 0;
   CVG_CK(cudaMemcpyAsync(&flag, flag_.as<int>(), sizeof flag, cudaMemcpyDeviceToHost, s));
@@ -1007,13 +1012,14 @@ Status Plan::finish_direct(const uint32_t* cfgs, int32_t ncfg, double* d_xtx, do
     if (rc.ok()) rc = cuda_status(cudaMemcpyAsync(cfg_d_.as<void>(), cfgs, sizeof(uint32_t) * ncfg,
                                                   cudaMemcpyHostToDevice, s), "H2D cfgs");
     if (rc.ok()) {
+      int nl = 0;
       {
         Timed t(ctx_, kProducts);
-        launch_products(local_.as<double>(), zero_ptr_.as<const double*>(), zero_nval_.as<int64_t>(), 1, n_, k_, m_,
-                        kp_, shift_.as<double>(), st, out_tiles_d_.as<int2>(), (int)out_tiles_.size(),
-                        cfg_d_.as<uint32_t>(), ncfg, d_xtx, d_xty, s);
+        nl = launch_products(local_.as<double>(), zero_ptr_.as<const double*>(), zero_nval_.as<int64_t>(), 1, n_, k_,
+                             m_, kp_, shift_.as<double>(), st, out_tiles_d_.as<int2>(), (int)out_tiles_.size(),
+                             out_ndiag_, cfg_d_.as<uint32_t>(), ncfg, d_xtx, d_xty, s);
       }
-      rc = count_launch();
+      rc = count_launch(nl);
     }
   }
   n_ = n_saved;

@@ -180,6 +180,7 @@ class Plan {
   int64_t n_ = 0, k_ = 0, m_ = 0, w_ = 0, kp_ = 0;
   int32_t p_ = 0, fb_ = 0, fe_ = 0;
   std::vector<int2> tiles_, out_tiles_, tiles128_;
+  int out_ndiag_ = 0;  // out_tiles_[0, out_ndiag_) are diagonal tiles
   std::vector<int2> tilesq_;    // int8 Gram tiles {I (128 rows), J (64 columns) | write mask << 16}
   bool i8_ = false;             // int8 digit slices: fp64 default (CVG_FP64_KIND=dmma: DMMA); fp32 with CVG_FP32_KIND=i8
   int sample_ = 16;             // int8 path: segment maxima over every sample_-th row (CVG_I8_SAMPLE; 1 = exact)
