@@ -159,6 +159,11 @@ __device__ __forceinline__ double i2d_exact(uint32_t v) {
   return __hiloint2double(0x43300000, (int)(v ^ 0x80000000u)) - 4503601774854144.0;  // 2^52 + 2^31
 }
 
+// 256-bit global store (sm_100): four doubles, 32-byte aligned
+__device__ __forceinline__ void stg_v4_f64(double* p, double a, double b, double c, double d) {
+  asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};\n" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d) : "memory");
+}
+
 __device__ __forceinline__ double pow2(int e) {  // 2^e for e in [-1022, 1023]
   return __hiloint2double((1023 + e) << 20, 0);
 }
@@ -350,9 +355,11 @@ __global__ void __launch_bounds__(kQThreads, 1)
         }
         if (write) {
 #pragma unroll
-          for (int j = 0; j < 16; j += 2) {
+          for (int j = 0; j < 16; j += 4) {  // 32-byte stores: a lane's row segment is whole sectors
             const int e0 = __shfl_sync(0xffffffffu, ecol, c0 + j), e1 = __shfl_sync(0xffffffffu, ecol, c0 + j + 1);
-            *reinterpret_cast<double2*>(out + c0 + j) = make_double2(unscale(f[j], erow + e0), unscale(f[j + 1], erow + e1));
+            const int e2 = __shfl_sync(0xffffffffu, ecol, c0 + j + 2), e3 = __shfl_sync(0xffffffffu, ecol, c0 + j + 3);
+            stg_v4_f64(out + c0 + j, unscale(f[j], erow + e0), unscale(f[j + 1], erow + e1), unscale(f[j + 2], erow + e2),
+                       unscale(f[j + 3], erow + e3));
           }
         } else {
 #pragma unroll
