@@ -132,6 +132,71 @@ void DevBuf::release() {
   bytes_ = 0;
 }
 
+// int8 Gram items (k_gram_i8.cu): one 64-column block c as B, two 64-row blocks as the A halves, each half
+// direct (the upper tile (a, c), a <= c) or transposed (the upper tile (c, a), a > c, computed as its
+// transpose).  Column c starts with its needed tiles (a, c); a column with an odd count would leave a half
+// unused, so odd columns are paired (c1 < c2) by moving the tile (c1, c2) into column c1 as a transposed half.
+// Each column is then cut into halves: 128-aligned pairs (2i, 2i + 1) first (one TMA box), the rest in order.
+// Every needed tile is produced exactly once; at most one half of the whole cover is unused when the tile
+// count is odd (configs[1]: 36 tiles in 18 items; the 128-aligned tiling needed 20, four of them half below
+// the diagonal).
+std::vector<int2> i8_items(const std::vector<int2>& tiles, int nb) {
+  std::vector<std::vector<std::pair<int, int>>> col(nb);  // (row block, mode 1 direct | 2 transposed)
+  std::vector<std::vector<bool>> need(nb, std::vector<bool>(nb, false));
+  for (const int2& t : tiles) {
+    col[t.y].push_back({t.x, 1});
+    need[t.x][t.y] = true;
+  }
+  std::vector<int> odd;
+  for (int c = 0; c < nb; ++c)
+    if (col[c].size() % 2) odd.push_back(c);
+  std::vector<bool> done(odd.size(), false);
+  for (size_t p = 0; p < odd.size(); ++p) {
+    if (done[p]) continue;
+    for (size_t q = p + 1; q < odd.size(); ++q) {
+      const int c1 = odd[p], c2 = odd[q];
+      if (done[q] || !need[c1][c2]) continue;
+      auto& v = col[c2];
+      for (size_t i = 0; i < v.size(); ++i)
+        if (v[i].first == c1 && v[i].second == 1) {
+          v.erase(v.begin() + (long)i);
+          break;
+        }
+      col[c1].push_back({c2, 2});
+      done[p] = done[q] = true;
+      break;
+    }
+  }
+  std::vector<int2> items;
+  for (int c = 0; c < nb; ++c) {
+    auto v = col[c];
+    std::sort(v.begin(), v.end());
+    std::vector<bool> taken(v.size(), false);
+    auto emit = [&](size_t i, long j) {  // j < 0: half 1 unused
+      const auto& h0 = v[i];
+      const int a1 = j >= 0 ? v[(size_t)j].first : h0.first;
+      const int m1 = j >= 0 ? v[(size_t)j].second : 0;
+      items.push_back(make_int2(h0.first | (a1 << 16), c | (h0.second << 16) | (m1 << 18)));
+      taken[i] = true;
+      if (j >= 0) taken[(size_t)j] = true;
+    };
+    for (size_t i = 0; i + 1 < v.size(); ++i)
+      if (!taken[i] && !taken[i + 1] && v[i].first % 2 == 0 && v[i + 1].first == v[i].first + 1) emit(i, (long)i + 1);
+    long pend = -1;
+    for (size_t i = 0; i < v.size(); ++i) {
+      if (taken[i]) continue;
+      if (pend < 0) {
+        pend = (long)i;
+      } else {
+        emit((size_t)pend, (long)i);
+        pend = -1;
+      }
+    }
+    if (pend >= 0) emit((size_t)pend, -1);
+  }
+  return items;
+}
+
 std::vector<int2> gram_tiles(int64_t k, int64_t m, int64_t kp, int edge) {
   const int nt = (int)(kp / edge);
   const int tx = (int)((k - 1) / edge);  // last tile holding X columns
@@ -322,17 +387,8 @@ Status Plan::create(cvg_context* ctx, int dtype, int64_t n, int64_t k, int64_t m
   slices_ = i8_slices_env();
   sample_ = i8_sample_env();
   tilesq_.clear();
-  if (i8_) {  // 128 x 64 int8-Gram tiles covering the needed upper 64-tiles (i, j): I = i / 2, J = j
-    for (const int2& t : tiles_) {
-      const int I = t.x / 2, bit = 1 << (t.x & 1);
-      int2* hit = nullptr;
-      for (int2& q : tilesq_)
-        if (q.x == I && (q.y & 0xffff) == t.y) hit = &q;
-      if (hit)
-        hit->y |= bit << 16;
-      else
-        tilesq_.push_back(make_int2(I, t.y | (bit << 16)));
-    }
+  if (i8_) {  // 128 x 64 int8-Gram items covering the needed upper 64-tiles exactly once
+    tilesq_ = i8_items(tiles_, (int)(kp_ / kTile));
     CVG_TRY(tilesq_d_.ensure(tilesq_.size() * sizeof(int2)));
     CVG_CK(cudaMemcpyAsync(tilesq_d_.as<int2>(), tilesq_.data(), tilesq_.size() * sizeof(int2), cudaMemcpyHostToDevice,
                            ctx->stream));
@@ -813,8 +869,8 @@ Status Plan::gram_host(const void* h_x, const void* h_y, void* d_x, void* d_y, c
   // the last 64-column block a tile reads (int8 tiles: the A rows they write, and J)
   auto last_col = [&](const int2& t) {
     if (!i8_path()) return t.y;
-    const int j = t.y & 0xffff;
-    return std::max(j, 2 * t.x + ((t.y >> 17) & 1));
+    const int c = t.y & 0xffff, a0 = t.x & 0xffff, a1 = t.x >> 16;
+    return std::max(c, std::max(a0, ((t.y >> 18) & 3) ? a1 : a0));
   };
   // Slabs (in tile columns): [0, nt/2), [nt/2, nt-1), [nt-1, nt).  Tiles touching
   // the last-arriving column are the only Gram work exposed after the final copy

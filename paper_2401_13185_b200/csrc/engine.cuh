@@ -181,7 +181,7 @@ class Plan {
   int32_t p_ = 0, fb_ = 0, fe_ = 0;
   std::vector<int2> tiles_, out_tiles_, tiles128_;
   int out_ndiag_ = 0;  // out_tiles_[0, out_ndiag_) are diagonal tiles
-  std::vector<int2> tilesq_;    // int8 Gram tiles {I (128 rows), J (64 columns) | write mask << 16}
+  std::vector<int2> tilesq_;    // int8 Gram items {a0 | a1 << 16, c | mode0 << 16 | mode1 << 18} (i8_items)
   bool i8_ = false;             // int8 digit slices: fp64 default (CVG_FP64_KIND=dmma: DMMA); fp32 with CVG_FP32_KIND=i8
   int sample_ = 16;             // int8 path: segment maxima over every sample_-th row (CVG_I8_SAMPLE; 1 = exact)
   int64_t exact_segments_ = 0;  // segments the last gram redid from their exact max

@@ -206,8 +206,13 @@ __device__ __forceinline__ double unscale(double f, int E) {
   return (E <= 1022 && E >= -1022) ? f * pow2(-E) : scalbn(f, -E);
 }
 
-// tiles[i] = {I, J | wmask << 16}: rows 128I .. +128 (Z columns), columns 64J .. +64; wmask bit h:
-// the 64 x 64 sub-tile of rows 128I + 64h is needed downstream (an upper 64-tile of the plan).
+// Items: tiles[i] = {a0 | a1 << 16, c | mode0 << 16 | mode1 << 18}.  B = the 64 Gram columns of block c; A = two
+// 64-row halves, half h = Z columns of block a_h (64 a_h .. +64); mode 1: the half's 64 x 64 result is the upper
+// tile (a_h, c) (a_h <= c), stored as is; mode 2: a_h > c, it is the transpose of the upper tile (c, a_h), stored
+// transposed; mode 0: unused half (not loaded, not stored).  An aligned item (a1 = a0 + 1, a0 even, both used)
+// loads A with one TMA box of 128 columns; other items load each used half slice by slice.  The host cover
+// (engine.cu i8_items) produces every needed upper tile exactly once with at most one unused half, where 128-row
+// aligned tiles left a 64 x 64 sub-tile below the diagonal on every diagonal tile (c1: 18 items instead of 20).
 //
 // Persistent: one CTA per SM walks the (segment, tile) items round-robin (item = blockIdx.x + i gridDim.x,
 // segment-major, so the CTAs running at once share a segment's digits in L2).  The TMA ring runs on across
@@ -217,7 +222,8 @@ __device__ __forceinline__ double unscale(double f, int E) {
 // short folds (the paper's P = 1000 at N = 1e5: 20,000 items of 2 K-steps).
 template <int S, int KS, int kMaxSt = 8>
 __global__ void __launch_bounds__(kQThreads, 1)
-    gram_i8_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+    gram_i8_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_a64,
+                   const __grid_constant__ CUtensorMap map_b,
                    const unsigned long long* __restrict__ segmax, const GramTask* __restrict__ segs,
                    const int2* __restrict__ tiles, int ntiles, int64_t nitems, int64_t seg_base, int64_t kp,
                    double* __restrict__ part, int headroom) {
@@ -252,27 +258,30 @@ __global__ void __launch_bounds__(kQThreads, 1)
 
   auto opA = [&](int s) { return smem + s * C::kStage; };
   auto opB = [&](int s) { return smem + s * C::kStage + S * C::kA; };
-  // item -> (segment, tile)
-  auto item = [&](int64_t it, int& seg, int& ti, int& tj, int& wmask, GramTask& task) {
+  // item -> (segment, A halves a0 / a1, B block c, half modes)
+  auto item = [&](int64_t it, int& seg, int& a0, int& a1, int& c, int& modes, GramTask& task) {
     const int64_t sl = it / ntiles;  // segment within this launch's range [seg_base, seg_base + nitems / ntiles)
     seg = (int)(seg_base + sl);
     const int2 tile0 = tiles[it - sl * ntiles];
-    ti = uniform(tile0.x);
-    tj = uniform(tile0.y & 0xffff);
-    wmask = uniform(tile0.y >> 16);
+    a0 = uniform(tile0.x & 0xffff);
+    a1 = uniform(tile0.x >> 16);
+    c = uniform(tile0.y & 0xffff);
+    modes = uniform(tile0.y >> 16);
     const GramTask task0 = segs[seg];
     task = GramTask{uniform(task0.zrow), uniform(task0.rows)};
     CVG_DCHECK(task.zrow % QK == 0 && task.rows % QK == 0 && task.rows > 0);
-    CVG_DCHECK(ti >= 0 && 2 * ti <= tj && (int64_t)tj * QB < kp);
+    CVG_DCHECK((int64_t)c * QB < kp && (int64_t)a0 * QB < kp && (int64_t)a1 * QB < kp && (modes & 3) != 0);
   };
 
   if (warp == 0) {  // ---- TMA producer (whole warp waits; one elected lane issues)
-    const uint32_t bytes = (uint32_t)(S * (C::kA + C::kB));
     int64_t g = 0;  // stage-ring position, continuous across items
     for (int64_t it = blockIdx.x; it < nitems; it += G) {
-      int seg, ti, tj, wmask;
+      int seg, a0, a1, c, modes;
       GramTask task;
-      item(it, seg, ti, tj, wmask, task);
+      item(it, seg, a0, a1, c, modes, task);
+      const bool use0 = (modes & 3) != 0, use1 = ((modes >> 2) & 3) != 0;
+      const bool aligned = use0 && use1 && a1 == a0 + 1 && (a0 & 1) == 0;
+      const uint32_t bytes = (uint32_t)(S * ((use0 + use1) * (C::kA / 2) + C::kB));
       const int nsteps = (int)(task.rows / KS);
       for (int st = 0; st < nsteps; ++st, ++g) {
         const int s = (int)(g % NST);
@@ -280,8 +289,16 @@ __global__ void __launch_bounds__(kQThreads, 1)
         const int blk = (int)(task.zrow / QK) + st / kPer, r0 = (st % kPer) * KS;
         if (elect_one()) {
           mbar_expect_tx(&full_bar[s], bytes);
-          tma_load_4d(opA(s), &map_a, &full_bar[s], r0, ti * QA, blk, 0);
-          tma_load_4d(opB(s), &map_b, &full_bar[s], r0, tj * QB, blk, 0);
+          if (aligned) {
+            tma_load_4d(opA(s), &map_a, &full_bar[s], r0, a0 * QB, blk, 0);
+          } else {
+#pragma unroll
+            for (int t = 0; t < S; ++t) {
+              if (use0) tma_load_4d(opA(s) + t * C::kA, &map_a64, &full_bar[s], r0, a0 * QB, blk, t);
+              if (use1) tma_load_4d(opA(s) + t * C::kA + C::kA / 2, &map_a64, &full_bar[s], r0, a1 * QB, blk, t);
+            }
+          }
+          tma_load_4d(opB(s), &map_b, &full_bar[s], r0, c * QB, blk, 0);
         }
         __syncwarp();
       }
@@ -290,9 +307,9 @@ __global__ void __launch_bounds__(kQThreads, 1)
     int64_t g = 0;
     int t = 0;  // items of this CTA
     for (int64_t it = blockIdx.x; it < nitems; it += G, ++t) {
-      int seg, ti, tj, wmask;
+      int seg, a0, a1, c, modes;
       GramTask task;
-      item(it, seg, ti, tj, wmask, task);
+      item(it, seg, a0, a1, c, modes, task);
       const int nsteps = (int)(task.rows / KS);
       if (t > 0) {  // the drain warps have read the previous item's accumulators
         mbar_wait(&tmem_empty, (uint32_t)(t - 1) & 1u);
@@ -321,18 +338,20 @@ __global__ void __launch_bounds__(kQThreads, 1)
     const int h = dw >> 2;   // columns [32h, 32h + 32) of the 64-wide tile
     int t = 0;
     for (int64_t it = blockIdx.x; it < nitems; it += G, ++t) {
-      int seg, ti, tj, wmask;
+      int seg, a0, a1, c, modes;
       GramTask task;
-      item(it, seg, ti, tj, wmask, task);
-      const int64_t row = (int64_t)ti * QA + 32 * q + lane;  // this thread's Gram row (a Z column)
-      const int64_t col0 = (int64_t)tj * QB + 32 * h;
-      const bool write = row < kp && ((wmask >> (q >> 1)) & 1);
+      item(it, seg, a0, a1, c, modes, task);
+      const int half = q >> 1;  // TMEM lanes 0-63: A half 0, 64-127: half 1
+      const int mode = (modes >> (2 * half)) & 3;
+      const int64_t row = (int64_t)(half ? a1 : a0) * QB + 32 * (q & 1) + lane;  // this thread's Gram row (a Z column)
+      const int64_t col0 = (int64_t)c * QB + 32 * h;
       const unsigned long long* mx = segmax + (int64_t)seg * kp;
-      const int erow = seg_exponent(__longlong_as_double((long long)mx[row < kp ? row : 0]), headroom);
+      const int erow = seg_exponent(__longlong_as_double((long long)mx[row]), headroom);
       const int ecol = seg_exponent(__longlong_as_double((long long)mx[col0 + lane]), headroom);  // lane j: column col0 + j
       mbar_wait(&acc_full, (uint32_t)t & 1u);
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
       double* out = part + (int64_t)seg * kp * kp + row * kp + col0;
+      double* out_t = part + (int64_t)seg * kp * kp + col0 * kp + row;  // mode 2: element (row, col0 + j) at (col0 + j, row)
 #pragma unroll
       for (int c0 = 0; c0 < 32; c0 += 16) {
         // all accumulators' 16 columns in one batch of TMEM loads (one wait: the item's MMAs restart sooner)
@@ -353,13 +372,20 @@ __global__ void __launch_bounds__(kQThreads, 1)
           __syncwarp();
           if (lane == 0) mbar_arrive(&tmem_empty);
         }
-        if (write) {
+        if (mode == 1) {
 #pragma unroll
           for (int j = 0; j < 16; j += 4) {  // 32-byte stores: a lane's row segment is whole sectors
             const int e0 = __shfl_sync(0xffffffffu, ecol, c0 + j), e1 = __shfl_sync(0xffffffffu, ecol, c0 + j + 1);
             const int e2 = __shfl_sync(0xffffffffu, ecol, c0 + j + 2), e3 = __shfl_sync(0xffffffffu, ecol, c0 + j + 3);
             stg_v4_f64(out + c0 + j, unscale(f[j], erow + e0), unscale(f[j + 1], erow + e1), unscale(f[j + 2], erow + e2),
                        unscale(f[j + 3], erow + e3));
+          }
+        } else if (mode == 2) {
+#pragma unroll
+          for (int j = 0; j < 16; j += 2) {  // transposed: the warp's 32 rows are 256 contiguous bytes of one row
+            const int e0 = __shfl_sync(0xffffffffu, ecol, c0 + j), e1 = __shfl_sync(0xffffffffu, ecol, c0 + j + 1);
+            out_t[(int64_t)(c0 + j) * kp] = unscale(f[j], erow + e0);
+            out_t[(int64_t)(c0 + j + 1) * kp] = unscale(f[j + 1], erow + e1);
           }
         } else {
 #pragma unroll
@@ -670,14 +696,15 @@ __global__ void __launch_bounds__(kQ1Threads, CVG_K1Q_MIN_BLOCKS)
   if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
 }
 
-// 4-D map over Zq: {64 rows, kp, zrows / 64, S} bytes, box {64, box_cols, 1, S}, SWIZZLE_64B.
+// 4-D map over Zq: {64 rows, kp, zrows / 64, S} bytes, box {64, box_cols, 1, box_slices (default S)}, SWIZZLE_64B.
 inline bool make_zq_map(CUtensorMap* map, const int8_t* zq, int64_t zrows, int64_t kp, int slices, int box_cols,
-                        int box_rows = QK) {
+                        int box_rows = QK, int box_slices = 0) {
   EncodeTiledFn enc = encode_fn();
   if (!enc) return false;
   const cuuint64_t dims[4] = {(cuuint64_t)QK, (cuuint64_t)kp, (cuuint64_t)(zrows / QK), (cuuint64_t)slices};
   const cuuint64_t strides[3] = {(cuuint64_t)QK, (cuuint64_t)kp * QK, (cuuint64_t)zrows * kp};
-  const cuuint32_t box[4] = {(cuuint32_t)box_rows, (cuuint32_t)box_cols, 1, (cuuint32_t)slices};
+  const cuuint32_t box[4] = {(cuuint32_t)box_rows, (cuuint32_t)box_cols, 1,
+                             (cuuint32_t)(box_slices > 0 ? box_slices : slices)};
   const cuuint32_t estr[4] = {1, 1, 1, 1};
   return enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<int8_t*>(zq), dims, strides, box, estr,
              CU_TENSOR_MAP_INTERLEAVE_NONE, box_rows == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -688,8 +715,10 @@ template <int S, int KS, int kMaxSt = 8>
 bool launch_gram_i8_s(const int8_t* zq, const unsigned long long* segmax, int headroom, int64_t zrows, int64_t kp,
                       const GramTask* segs, int64_t seg_base, int64_t nseg, const int2* tiles, int ntiles, double* part,
                       int max_ctas, cudaStream_t s) {
-  CUtensorMap ma, mb;
-  if (!make_zq_map(&ma, zq, zrows, kp, S, QA, KS) || !make_zq_map(&mb, zq, zrows, kp, S, QB, KS)) return false;
+  CUtensorMap ma, ma64, mb;
+  if (!make_zq_map(&ma, zq, zrows, kp, S, QA, KS) || !make_zq_map(&ma64, zq, zrows, kp, S, QB, KS, 1) ||
+      !make_zq_map(&mb, zq, zrows, kp, S, QB, KS))
+    return false;
   using C = QCfg<S, KS, kMaxSt>;
   cudaFuncSetAttribute(gram_i8_kernel<S, KS, kMaxSt>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
   int dev = 0, sms = 0;
@@ -699,7 +728,7 @@ bool launch_gram_i8_s(const int8_t* zq, const unsigned long long* segmax, int he
   // persistent: one CTA per SM (1 fits: shared memory), or max_ctas to leave SMs to a concurrent K1Q
   const int64_t blocks = std::min<int64_t>(nitems, max_ctas > 0 ? std::min(max_ctas, sms) : sms);
   if (blocks > 0)
-    gram_i8_kernel<S, KS, kMaxSt><<<(unsigned)blocks, kQThreads, C::kSmem, s>>>(ma, mb, segmax, segs, tiles, ntiles,
+    gram_i8_kernel<S, KS, kMaxSt><<<(unsigned)blocks, kQThreads, C::kSmem, s>>>(ma, ma64, mb, segmax, segs, tiles, ntiles,
                                                                                 nitems, seg_base, kp, part, headroom);
   return true;
 }
