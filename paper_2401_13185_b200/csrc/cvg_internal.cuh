@@ -107,17 +107,19 @@ struct GramTask {
 void launch_gram_f64(const double* z, int64_t kp, int64_t zrows, const GramTask* segs, int64_t nseg,
                      const int2* tiles, int ntiles, double* part, cudaStream_t s);
 
-// K4: fixed-order (midpoint-tree) sums of kp x kp matrices over upper tiles,
-// one launch per tree level.  d = a + b; b == null copies a; a == null zeroes d.
-// One node of a midpoint tree whose children are leaves or leaf pairs, fused:
-//   L = in[1] ? in[0] + in[1] : in[0];  R = in[3] ? in[2] + in[3] : in[2];
-//   d = in[2] ? L + R : L   (all null: d = 0)
-// -- the same additions, in the same order, as the unfused binary tree.
-struct PairOp {
-  const double* in[4];
+// K4: fixed-order (midpoint-tree) sums of kp x kp matrices over upper tiles.  One op is a node S(a, b) of a
+// midpoint tree evaluated down to depth kTreeFanDepth in registers: its inputs are the node's frontier at that
+// depth, left to right (leaves, or nodes computed by deeper ops), and
+//   S(size) = in  if depth == kTreeFanDepth or size == 1,  else S(size / 2) + S(size - size / 2)
+// -- the same additions, in the same order, as the unfused binary tree; size 0 zeroes d.
+constexpr int kTreeFanDepth = 4;
+constexpr int kTreeFanIn = 1 << kTreeFanDepth;
+struct TreeOp {
+  const double* in[kTreeFanIn];
   double* d;
+  int size;  // leaves under the node (the recursion's shape)
 };
-void launch_pair_sums(const PairOp* ops, int nops, int64_t kp, const int2* tiles, int ntiles, cudaStream_t s);
+void launch_tree_ops(const TreeOp* ops, int nops, int64_t kp, const int2* tiles, int ntiles, cudaStream_t s);
 // g[0] = NaN when *flag has bit 0 set (non-finite input seen by K1): the flag rides in the partial.
 void launch_poison_if_flag(const int* flag, double* g, cudaStream_t s);
 

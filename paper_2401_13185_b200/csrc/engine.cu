@@ -14,6 +14,7 @@
 #include <climits>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <string>
 
 #include "engine.cuh"
@@ -211,29 +212,28 @@ std::vector<int2> gram_tiles(int64_t k, int64_t m, int64_t kp, int edge) {
 
 
 const double* TreeProgram::emit(const std::vector<const double*>& leaves, int a, int b, int depth, double* root_dst,
-                                std::vector<std::vector<PairOp>>& by_depth, int64_t kp) {
+                                std::vector<std::vector<TreeOp>>& by_depth, int64_t kp) {
   if ((int)by_depth.size() <= depth) by_depth.resize(depth + 1);
   if (b - a <= 1 && !root_dst) return leaves[a];  // interior leaf: read in place
   double* out = root_dst ? root_dst : scratch_.as<double>() + (next_slot_++) * kp * kp;
-  PairOp op{{nullptr, nullptr, nullptr, nullptr}, out};
-  if (b - a == 1) {
-    op.in[0] = leaves[a];
-  } else if (b - a >= 2) {
-    // S(a,b) = S(a,mid) + S(mid,b); a child of <= 2 leaves is folded into this op
-    const int mid = a + (b - a) / 2;
-    auto child = [&](int lo, int hi, int slot) {
-      if (hi - lo == 1) {
-        op.in[slot] = leaves[lo];
-      } else if (hi - lo == 2) {
-        op.in[slot] = leaves[lo];  // S(lo, lo+2) = leaf lo + leaf lo+1
-        op.in[slot + 1] = leaves[lo + 1];
-      } else {
-        op.in[slot] = emit(leaves, lo, hi, depth + 1, nullptr, by_depth, kp);
-      }
-    };
-    child(a, mid, 0);
-    child(mid, b, 2);
-  }
+  TreeOp op{};
+  op.d = out;
+  op.size = b - a;
+  int cnt = 0;
+  // the node's frontier kTreeFanDepth levels down (S(a,b) = S(a,mid) + S(mid,b)), left to right: leaves, or
+  // nodes evaluated by ops one level deeper
+  std::function<void(int, int, int)> frontier = [&](int lo, int hi, int d) {
+    if (hi - lo == 1) {
+      op.in[cnt++] = leaves[lo];
+    } else if (d == kTreeFanDepth) {
+      op.in[cnt++] = emit(leaves, lo, hi, depth + 1, nullptr, by_depth, kp);
+    } else {
+      const int mid = lo + (hi - lo) / 2;
+      frontier(lo, mid, d + 1);
+      frontier(mid, hi, d + 1);
+    }
+  };
+  if (b > a) frontier(a, b, 0);
   by_depth[depth].push_back(op);
   return out;
 }
@@ -243,7 +243,7 @@ Status TreeProgram::build(const std::vector<TreeGroup>& groups, int64_t kp, cuda
   for (const auto& g : groups) slots += std::max<int64_t>((int64_t)g.leaves.size() - 2, 0);
   CVG_TRY(scratch_.ensure(sizeof(double) * std::max<int64_t>(slots, 1) * kp * kp));
   next_slot_ = 0;
-  std::vector<std::vector<PairOp>> by_depth;
+  std::vector<std::vector<TreeOp>> by_depth;
   for (const auto& g : groups) emit(g.leaves, 0, (int)g.leaves.size(), 0, g.dst, by_depth, kp);
   flat_.clear();
   level_off_.assign(1, 0);
@@ -252,9 +252,9 @@ Status TreeProgram::build(const std::vector<TreeGroup>& groups, int64_t kp, cuda
     flat_.insert(flat_.end(), by_depth[d].begin(), by_depth[d].end());
     level_off_.push_back((int)flat_.size());
   }
-  CVG_TRY(ops_d_.ensure(sizeof(PairOp) * std::max<size_t>(flat_.size(), 1)));
+  CVG_TRY(ops_d_.ensure(sizeof(TreeOp) * std::max<size_t>(flat_.size(), 1)));
   if (!flat_.empty())
-    CVG_TRY(stage_.upload({{flat_.data(), sizeof(PairOp) * flat_.size(), ops_d_.as<void>()}}, s));
+    CVG_TRY(stage_.upload({{flat_.data(), sizeof(TreeOp) * flat_.size(), ops_d_.as<void>()}}, s));
   return Status::Ok();
 }
 
@@ -262,7 +262,7 @@ Status TreeProgram::run(cvg_context* ctx, const int2* tiles, int ntiles, int64_t
   for (int l = 0; l + 1 < (int)level_off_.size(); ++l) {
     {
       Timed t(ctx, kTree);
-      launch_pair_sums(ops_d_.as<PairOp>() + level_off_[l], level_off_[l + 1] - level_off_[l], kp, tiles, ntiles,
+      launch_tree_ops(ops_d_.as<TreeOp>() + level_off_[l], level_off_[l + 1] - level_off_[l], kp, tiles, ntiles,
                        ctx->stream);
     }
     ctx->launches += 1;

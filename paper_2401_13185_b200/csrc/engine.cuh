@@ -72,9 +72,9 @@ class TreeProgram {
 
  private:
   const double* emit(const std::vector<const double*>& leaves, int a, int b, int depth, double* root_dst,
-                     std::vector<std::vector<PairOp>>& by_depth, int64_t kp);
+                     std::vector<std::vector<TreeOp>>& by_depth, int64_t kp);
   std::vector<int> level_off_;
-  std::vector<PairOp> flat_;
+  std::vector<TreeOp> flat_;
   DevBuf scratch_, ops_d_;
   PinnedStage stage_;
   int64_t next_slot_ = 0;

@@ -10,47 +10,48 @@
 // tree's top levels.  This keeps the reference's bitwise thread-count
 // invariance (threading.hpp:8-10, test_fast.cpp:217-229).  No float atomics.
 //
-// The host flattens the trees into levels of independent ops (TreeProgram,
-// engine.cu); a node whose children are leaves or leaf pairs is ONE op,
-// ((a + b) + (c + d)) evaluated in registers -- the same additions in the same
-// order, so two tree levels cost one pass (intermediate nodes are not written
-// and re-read).  Each level is one launch over (tile, op) with 16-byte loads,
-// streaming at HBM speed.  Only the tiles the Gram wrote are touched.
+// The host flattens the trees into levels of independent ops (TreeProgram, engine.cu); an op evaluates a node
+// down to kTreeFanDepth levels in registers (up to 16 inputs) -- the same additions in the same order, so four
+// tree levels cost one pass (intermediate nodes are not written and re-read; configs[1]'s 100-fold tree is 2
+// launches instead of 6).  Each level is one launch over (tile, op) with 16-byte loads, streaming at HBM speed.
+// Only the tiles the Gram wrote are touched.
 #include "cvg_internal.cuh"
 
 namespace cvg {
 namespace {
 
-__global__ void __launch_bounds__(256) pair_sum_kernel(const PairOp* __restrict__ ops, int64_t kp,
-                                                       const int2* __restrict__ tiles) {
+__device__ __forceinline__ double2 ld2(const double* p) { return *reinterpret_cast<const double2*>(p); }
+
+// S(size) of the op's subtree at depth kTreeFanDepth - D, consuming inputs left to right.  The op (and so every
+// branch on size) is uniform across the CTA.
+template <int D>
+__device__ __forceinline__ double2 tree_node(const TreeOp* __restrict__ op, int size, int& idx, int64_t off) {
+  if constexpr (D == 0) {
+    return ld2(op->in[idx++] + off);
+  } else {
+    if (size == 1) return ld2(op->in[idx++] + off);
+    const int l = size / 2;
+    const double2 a = tree_node<D - 1>(op, l, idx, off);
+    const double2 b = tree_node<D - 1>(op, size - l, idx, off);
+    return make_double2(__dadd_rn(a.x, b.x), __dadd_rn(a.y, b.y));
+  }
+}
+
+__global__ void __launch_bounds__(256) tree_op_kernel(const TreeOp* __restrict__ ops, int64_t kp,
+                                                      const int2* __restrict__ tiles) {
   const int2 tile = tiles[blockIdx.x];
-  const PairOp op = ops[blockIdx.y];
-  CVG_DCHECK(op.d != nullptr && (op.in[0] != nullptr || op.in[2] == nullptr));
+  const TreeOp* op = ops + blockIdx.y;
+  const int size = op->size;
+  double* d = op->d;
+  CVG_DCHECK(d != nullptr && size >= 0);
   CVG_DCHECK(tile.x >= 0 && tile.x <= tile.y && (int64_t)(tile.y + 1) * kTile <= kp);
   const int c2 = (threadIdx.x & 31) * 2;  // column pair within the tile
-#pragma unroll 4
+#pragma unroll 2
   for (int r = threadIdx.x >> 5; r < kTile; r += 8) {
     const int64_t off = ((int64_t)tile.x * kTile + r) * kp + (int64_t)tile.y * kTile + c2;
-    double2 v = make_double2(0.0, 0.0);
-    if (op.in[0]) {
-      v = *reinterpret_cast<const double2*>(op.in[0] + off);
-      if (op.in[1]) {
-        const double2 u = *reinterpret_cast<const double2*>(op.in[1] + off);
-        v.x = __dadd_rn(v.x, u.x);
-        v.y = __dadd_rn(v.y, u.y);
-      }
-      if (op.in[2]) {
-        double2 r = *reinterpret_cast<const double2*>(op.in[2] + off);
-        if (op.in[3]) {
-          const double2 u = *reinterpret_cast<const double2*>(op.in[3] + off);
-          r.x = __dadd_rn(r.x, u.x);
-          r.y = __dadd_rn(r.y, u.y);
-        }
-        v.x = __dadd_rn(v.x, r.x);
-        v.y = __dadd_rn(v.y, r.y);
-      }
-    }
-    *reinterpret_cast<double2*>(op.d + off) = v;
+    int idx = 0;
+    const double2 v = size > 0 ? tree_node<kTreeFanDepth>(op, size, idx, off) : make_double2(0.0, 0.0);
+    *reinterpret_cast<double2*>(d + off) = v;
   }
 }
 
@@ -65,11 +66,11 @@ __global__ void poison_if_flag_kernel(const int* __restrict__ flag, double* __re
 
 void launch_poison_if_flag(const int* flag, double* g, cudaStream_t s) { poison_if_flag_kernel<<<1, 1, 0, s>>>(flag, g); }
 
-void launch_pair_sums(const PairOp* ops, int nops, int64_t kp, const int2* tiles, int ntiles, cudaStream_t s) {
+void launch_tree_ops(const TreeOp* ops, int nops, int64_t kp, const int2* tiles, int ntiles, cudaStream_t s) {
   if (nops <= 0 || ntiles <= 0) return;
   for (int o = 0; o < nops; o += 65535) {  // gridDim.y <= 65535 (a level of a leave-one-out tree can hold N ops)
     dim3 grid((unsigned)ntiles, (unsigned)(nops - o < 65535 ? nops - o : 65535));
-    pair_sum_kernel<<<grid, 256, 0, s>>>(ops + o, kp, tiles);
+    tree_op_kernel<<<grid, 256, 0, s>>>(ops + o, kp, tiles);
   }
 }
 
