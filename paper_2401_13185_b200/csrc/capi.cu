@@ -307,6 +307,10 @@ void cvg_context_destroy(cvg_context* ctx) {
   if (ctx->copy_stream) cudaStreamSynchronize(ctx->copy_stream);
   for (cudaEvent_t e : ctx->sync_events) cudaEventDestroy(e);
   if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
+  if (ctx->aux_stream) {
+    cudaStreamSynchronize(ctx->aux_stream);
+    cudaStreamDestroy(ctx->aux_stream);
+  }
   ctx->scratch.reset();
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
   delete ctx;

@@ -198,12 +198,17 @@ bool launch_reorder_q(int dtype, int slices, const void* x, int64_t ldx, const v
                       int64_t m, const int64_t* src_row, int64_t zrows, int64_t kp, int64_t c_begin, int64_t c_end,
                       int64_t nsrc, const double* shift, const int* blkseg, const unsigned long long* segmax,
                       int headroom, int* ovf, int8_t* zq, int* nonfinite, cudaStream_t s, int64_t blk_lo = 0,
-                      int64_t blk_hi = -1, int max_sms = 0);
+                      int64_t blk_hi = -1, int max_sms = 0, int direct_ctas_per_sm = 0, unsigned* seg_ready = nullptr);
+// direct_ctas_per_sm > 0: the register-only cut (no shared-memory tile, no TMA) on that many persistent CTAs per
+// SM; it counts every finished 64-row block into seg_ready[its segment] (release) when seg_ready != null.
+//
 // Segments [seg_base, seg_base + nseg) of segs (absolute indices into segs / segmax / part); max_ctas > 0 caps
-// the persistent grid.
+// the persistent grid.  lean: the 96-register kernel that shares its SM with a cut CTA; seg_ready + abort_flag:
+// each item waits for its segment's block count from a concurrent cut (k_gram_i8.cu).
 bool launch_gram_i8(int slices, const int8_t* zq, const unsigned long long* segmax, int headroom, int64_t zrows,
                     int64_t kp, const GramTask* segs, int64_t nseg, const int2* tiles, int ntiles, double* part,
-                    cudaStream_t s, int64_t seg_base = 0, int max_ctas = 0);
+                    cudaStream_t s, int64_t seg_base = 0, int max_ctas = 0, int lean = 0,
+                    const unsigned* seg_ready = nullptr, int* abort_flag = nullptr);
 
 inline int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
 inline int64_t padded_cols(int64_t k, int64_t m, int dtype = 0) {

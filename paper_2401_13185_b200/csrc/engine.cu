@@ -17,6 +17,8 @@
 #include <functional>
 #include <string>
 
+#include <cstdio>
+
 #include "engine.cuh"
 
 cudaEvent_t cvg_context::take_event() {
@@ -33,6 +35,11 @@ cudaEvent_t cvg_context::take_event() {
 cvg::Status cvg_context::ensure_copy_stream() {
   if (copy_stream) return cvg::Status::Ok();
   return cvg::cuda_status(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking), "copy stream");
+}
+
+cvg::Status cvg_context::ensure_aux_stream() {
+  if (aux_stream) return cvg::Status::Ok();
+  return cvg::cuda_status(cudaStreamCreateWithFlags(&aux_stream, cudaStreamNonBlocking), "aux stream");
 }
 
 cudaEvent_t cvg_context::stream_event(size_t i) {
@@ -753,8 +760,13 @@ Status Plan::gram(const void* d_x, int64_t ldx, const void* d_y, int64_t ldy, co
       CVG_CK(cudaMemsetAsync(segmax_.as<void>(), 0, sizeof(unsigned long long) * segs_.size() * kp_, s));
       if (sample_ > 1) CVG_CK(cudaMemsetAsync(ovf_.as<void>(), 0, sizeof(int) * segs_.size(), s));
     }
-    if (zrows_ > 0) CVG_TRY(i8_prep(d_x, ldx, d_y, ldy, rows, nsrc, 0, kp_, false));
-    CVG_TRY(i8_gram(tilesq_d_.as<int2>(), (int)tilesq_.size()));
+    overlapped_ = false;
+    if (zrows_ > 0 && !segs_.empty() && !tilesq_.empty() && i8_overlap_enabled() && !ctx_->overlap_failed) {
+      CVG_TRY(i8_overlapped(d_x, ldx, d_y, ldy, rows, nsrc));
+    } else {
+      if (zrows_ > 0) CVG_TRY(i8_prep(d_x, ldx, d_y, ldy, rows, nsrc, 0, kp_, false));
+      CVG_TRY(i8_gram(tilesq_d_.as<int2>(), (int)tilesq_.size()));
+    }
     CVG_TRY(gram_trees());
     CVG_TRY(i8_exact_pass(d_x, ldx, d_y, ldy, rows, nsrc));
     return poison_local();
@@ -825,17 +837,78 @@ Status Plan::i8_gram(const int2* tiles, int ntiles) {
   return count_launch();
 }
 
+// K1Q's HBM-bound cut runs beside the tensor-bound Gram instead of before it when the segments are long
+// enough (>= 1024 rows on average: short segments pay the per-item acquire and keep the 16-column drain);
+// CVG_I8_OVERLAP=0 keeps the serial schedule, =1 forces the overlap.  Read per call (tests A/B both).
+bool Plan::i8_overlap_enabled() const {
+  const char* v = std::getenv("CVG_I8_OVERLAP");
+  if (v && (v[0] == '0' || v[0] == '1')) return v[0] == '1';
+  return !segs_.empty() && zrows_ / (int64_t)segs_.size() >= 1024;
+}
+
+// The cut beside the Gram.  The aux stream runs the direct-store cut on one persistent CTA per SM (Z order);
+// the main stream runs the lean Gram, whose items (segment-major, the same order) each wait for their
+// segment's published block count.  Same digits, same MMAs, same drain: bit-identical to the serial path.
+Status Plan::i8_overlapped(const void* d_x, int64_t ldx, const void* d_y, int64_t ldy, const int64_t* rows,
+                           int64_t nsrc) {
+  cudaStream_t s = ctx_->stream;
+  CVG_TRY(ctx_->ensure_aux_stream());
+  const bool sampled = sample_ > 1;
+  const size_t nseg = segs_.size();
+  CVG_TRY(seg_ready_.ensure(sizeof(unsigned) * (nseg + 1)));
+  CVG_CK(cudaMemsetAsync(seg_ready_.as<void>(), 0, sizeof(unsigned) * (nseg + 1), s));
+  {
+    Timed t(ctx_, kReorder);
+    launch_segmax(dtype_, d_x, ldx, d_y, ldy, k_, m_, rows, segs_d_.as<GramTask>(), (int64_t)nseg, max_seg_rows(), kp_,
+                  0, kp_, nsrc, shift_.as<double>(), sample_, nullptr, segmax_.as<unsigned long long>(), s);
+  }
+  CVG_TRY(count_launch());
+  cudaEvent_t ev0 = ctx_->stream_event(0), ev1 = ctx_->stream_event(1);
+  CVG_CK(cudaEventRecord(ev0, s));
+  CVG_CK(cudaStreamWaitEvent(ctx_->aux_stream, ev0, 0));
+  bool ok;
+  {
+    Timed t(ctx_, kGram);  // the overlapped region: cut and Gram
+    ok = launch_reorder_q(dtype_, slices_, d_x, ldx, d_y, ldy, k_, m_, rows, zrows_, kp_, 0, kp_, nsrc,
+                          shift_.as<double>(), blkseg_.as<int>(), segmax_.as<unsigned long long>(), sampled ? 1 : 0,
+                          sampled ? ovf_.as<int>() : nullptr, zq_.as<int8_t>(), flag_.as<int>(), ctx_->aux_stream, 0,
+                          -1, 0, 1, seg_ready_.as<unsigned>());
+    CVG_CK(cudaEventRecord(ev1, ctx_->aux_stream));
+    ok = ok && launch_gram_i8(slices_, zq_.as<int8_t>(), segmax_.as<unsigned long long>(), sampled ? 1 : 0, zrows_, kp_,
+                              segs_d_.as<GramTask>(), (int64_t)nseg, tilesq_d_.as<int2>(), (int)tilesq_.size(),
+                              part_.as<double>(), s, 0, 0, 1, seg_ready_.as<unsigned>(),
+                              reinterpret_cast<int*>(seg_ready_.as<unsigned>() + nseg));
+    CVG_CK(cudaStreamWaitEvent(s, ev1, 0));
+  }
+  if (!ok) return Status::Err(5, "cuTensorMapEncodeTiled unavailable or rejected the operand layout");
+  overlapped_ = true;
+  return count_launch(2);
+}
+
 // Sampled exponents only: if any segment held a value beyond 2x its sampled max (or a nonzero value
 // in a column whose sample was all zero), redo those segments' maxima over every row, then K1Q and the
 // Gram for all columns (unflagged segments reproduce the same bits) and the trees.  The decision is per
 // segment and depends on the segment's rows only, so results stay bit-identical across GPU counts.
 Status Plan::i8_exact_pass(const void* d_x, int64_t ldx, const void* d_y, int64_t ldy, const int64_t* rows,
                            int64_t nsrc) {
-  if (sample_ <= 1 || segs_.empty()) return Status::Ok();
+  if ((sample_ <= 1 && !overlapped_) || segs_.empty()) return Status::Ok();
   cudaStream_t s = ctx_->stream;
-  ovf_host_.resize(segs_.size());
-  CVG_CK(cudaMemcpyAsync(ovf_host_.data(), ovf_.as<int>(), sizeof(int) * segs_.size(), cudaMemcpyDeviceToHost, s));
+  ovf_host_.assign(segs_.size(), 0);
+  int aborted = 0;
+  if (sample_ > 1)
+    CVG_CK(cudaMemcpyAsync(ovf_host_.data(), ovf_.as<int>(), sizeof(int) * segs_.size(), cudaMemcpyDeviceToHost, s));
+  if (overlapped_)
+    CVG_CK(cudaMemcpyAsync(&aborted, seg_ready_.as<unsigned>() + segs_.size(), sizeof(int), cudaMemcpyDeviceToHost, s));
   CVG_CK(cudaStreamSynchronize(s));
+  overlapped_ = false;
+  if (aborted) {
+    // A Gram item gave up waiting for the cut (the two kernels did not share the SMs): the digits are complete
+    // by now (the cut never waits), so redo the Gram alone, and keep this context on the serial path.
+    ctx_->overlap_failed = true;
+    std::fprintf(stderr, "cvgram: the cut did not run beside the Gram (a Gram item waited %d ms); serial schedule from here on\n", 1000);
+    CVG_TRY(i8_gram(tilesq_d_.as<int2>(), (int)tilesq_.size()));
+    CVG_TRY(gram_trees());
+  }
   int64_t flagged = 0;
   for (int v : ovf_host_) flagged += v != 0;
   exact_segments_ = flagged;

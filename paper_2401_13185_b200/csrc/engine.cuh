@@ -143,6 +143,9 @@ class Plan {
                  int64_t c0, int64_t c1, bool exact);
   Status i8_gram(const int2* tiles, int ntiles);
   Status i8_exact_pass(const void* d_x, int64_t ldx, const void* d_y, int64_t ldy, const int64_t* rows, int64_t nsrc);
+  // the cut beside the Gram (engine.cu; CVG_I8_OVERLAP=0|1 overrides the segment-length rule): one direct-store cut CTA and one lean Gram CTA per SM
+  Status i8_overlapped(const void* d_x, int64_t ldx, const void* d_y, int64_t ldy, const int64_t* rows, int64_t nsrc);
+  bool i8_overlap_enabled() const;
   static bool small_folds_enabled();
 
  public:
@@ -186,6 +189,8 @@ class Plan {
   int sample_ = 16;             // int8 path: segment maxima over every sample_-th row (CVG_I8_SAMPLE; 1 = exact)
   int64_t exact_segments_ = 0;  // segments the last gram redid from their exact max
   std::vector<int> ovf_host_;
+  DevBuf seg_ready_;            // overlapped cut: per-segment finished-block counts + the abort flag (last word)
+  bool overlapped_ = false;     // the last gram ran the cut beside the Gram (its abort flag is pending)
   int slices_ = 6;              // base-256 int8 digits per value (fp64: CVG_I8_SLICES = 5 | 6; fp32: CVG_I8_SLICES_F32 = 3 | 4)
   std::vector<int64_t> counts_;  // per fold (all p) validation sizes
   std::vector<GramTask> segs_;
@@ -247,8 +252,11 @@ struct cvg_context {
   cudaEvent_t take_event();
   // host-input streaming (Plan::gram_host): a copy stream and reusable events
   cudaStream_t copy_stream = nullptr;
+  cudaStream_t aux_stream = nullptr;  // the cut that runs beside the int8 Gram
+  bool overlap_failed = false;        // a Gram waited out its timeout once: stay on the serial path
   std::vector<cudaEvent_t> sync_events;
   cvg::Status ensure_copy_stream();
+  cvg::Status ensure_aux_stream();
   cudaEvent_t stream_event(size_t i);
   void begin(int cls);
   void end();

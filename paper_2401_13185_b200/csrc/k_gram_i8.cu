@@ -220,13 +220,33 @@ __device__ __forceinline__ double unscale(double f, int E) {
 // starts an item once the drain warps have read the previous item's accumulators (tmem_empty).  A launch per
 // item paid its TMEM allocation, barrier setup and pipeline fill every time: ~9 us per item, which dominated
 // short folds (the paper's P = 1000 at N = 1e5: 20,000 items of 2 K-steps).
-template <int S, int KS, int kMaxSt = 8>
-__global__ void __launch_bounds__(kQThreads, 1)
+//
+// LEAN (the Gram that runs beside the direct cut): the drain reads its accumulators 8 columns at a time and the
+// kernel is held to 96 registers (launch bounds of two CTAs per SM; shared memory admits one), so a 256-thread
+// cut CTA fits on the same SM; the TMA producer acquires seg_ready[seg] (one count per cut 64-row block) before
+// an item's first stage.  A producer that waits longer than kReadyTimeoutNs sets *abort_flag and stops
+// waiting (so does every other producer): the launch then finishes on whatever digits are there and the host
+// redoes the pass serially -- the cut does not depend on the Gram, so a missing co-residency cannot hang.
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;\n" : "=l"(t));
+  return t;
+}
+constexpr unsigned long long kReadyTimeoutNs = 1000000000ull;
+
+template <int S, int KS, int kMaxSt = 8, bool LEAN = false>
+__global__ void __launch_bounds__(kQThreads, LEAN ? 2 : 1)
     gram_i8_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_a64,
                    const __grid_constant__ CUtensorMap map_b,
                    const unsigned long long* __restrict__ segmax, const GramTask* __restrict__ segs,
                    const int2* __restrict__ tiles, int ntiles, int64_t nitems, int64_t seg_base, int64_t kp,
-                   double* __restrict__ part, int headroom) {
+                   double* __restrict__ part, int headroom, const unsigned* __restrict__ seg_ready,
+                   int* __restrict__ abort_flag) {
   using C = QCfg<S, KS, kMaxSt>;
   constexpr int NST = C::kNst;
   constexpr int kPer = QK / KS;  // stages per 64-row block
@@ -283,6 +303,22 @@ __global__ void __launch_bounds__(kQThreads, 1)
       const bool aligned = use0 && use1 && a1 == a0 + 1 && (a0 & 1) == 0;
       const uint32_t bytes = (uint32_t)(S * ((use0 + use1) * (C::kA / 2) + C::kB));
       const int nsteps = (int)(task.rows / KS);
+      if (seg_ready) {  // the concurrent cut has published every 64-row block of this segment
+        const unsigned need = (unsigned)(task.rows / QK);
+        if (ld_acquire_u32(seg_ready + seg) < need) {
+          const unsigned long long t0 = global_ns();
+          while (ld_acquire_u32(seg_ready + seg) < need) {
+            __nanosleep(256);
+            if (*reinterpret_cast<volatile int*>(abort_flag)) break;
+            if (global_ns() - t0 > kReadyTimeoutNs) {
+              atomicExch(abort_flag, 1);
+              break;
+            }
+          }
+        }
+        asm volatile("fence.proxy.async.global;\n" ::: "memory");  // generic-proxy digits -> TMA reads
+        __syncwarp();
+      }
       for (int st = 0; st < nsteps; ++st, ++g) {
         const int s = (int)(g % NST);
         mbar_wait(&empty_bar[s], ((uint32_t)(g / NST) & 1u) ^ 1u);
@@ -352,29 +388,33 @@ __global__ void __launch_bounds__(kQThreads, 1)
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
       double* out = part + (int64_t)seg * kp * kp + row * kp + col0;
       double* out_t = part + (int64_t)seg * kp * kp + col0 * kp + row;  // mode 2: element (row, col0 + j) at (col0 + j, row)
+      constexpr int DB = LEAN ? 8 : 16;  // accumulator columns per batch
 #pragma unroll
-      for (int c0 = 0; c0 < 32; c0 += 16) {
-        // all accumulators' 16 columns in one batch of TMEM loads (one wait: the item's MMAs restart sooner)
-        uint32_t r[kNAcc<S>][16];
+      for (int c0 = 0; c0 < 32; c0 += DB) {
+        // all accumulators' DB columns in one batch of TMEM loads (one wait: the item's MMAs restart sooner)
+        uint32_t r[kNAcc<S>][DB];
 #pragma unroll
-        for (int d = 0; d < kNAcc<S>; ++d)
-          tmem_ld16_nowait(tmem_d + ((uint32_t)(32 * q) << 16) + (uint32_t)(d * QB + 32 * h + c0), r[d]);
+        for (int d = 0; d < kNAcc<S>; ++d) {
+          const uint32_t ta = tmem_d + ((uint32_t)(32 * q) << 16) + (uint32_t)(d * QB + 32 * h + c0);
+          if constexpr (LEAN) tmem_ld8_nowait(ta, r[d]);
+          else tmem_ld16_nowait(ta, r[d]);
+        }
         tmem_ld_wait();
-        double f[16];
+        double f[DB];
 #pragma unroll
-        for (int j = 0; j < 16; ++j) f[j] = i2d_exact(r[kNAcc<S> - 1][j]);
+        for (int j = 0; j < DB; ++j) f[j] = i2d_exact(r[kNAcc<S> - 1][j]);
 #pragma unroll
         for (int d = kNAcc<S> - 2; d >= 0; --d)
 #pragma unroll
-          for (int j = 0; j < 16; ++j) f[j] = fma(f[j], 0x1p-8, i2d_exact(r[d][j]));  // f * 2^-8 exact
-        if (c0 == 16) {  // every accumulator column of this thread has been read: the MMA warp may go on
+          for (int j = 0; j < DB; ++j) f[j] = fma(f[j], 0x1p-8, i2d_exact(r[d][j]));  // f * 2^-8 exact
+        if (c0 == 32 - DB) {  // every accumulator column of this thread has been read: the MMA warp may go on
           asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
           __syncwarp();
           if (lane == 0) mbar_arrive(&tmem_empty);
         }
         if (mode == 1) {
 #pragma unroll
-          for (int j = 0; j < 16; j += 4) {  // 32-byte stores: a lane's row segment is whole sectors
+          for (int j = 0; j < DB; j += 4) {  // 32-byte stores: a lane's row segment is whole sectors
             const int e0 = __shfl_sync(0xffffffffu, ecol, c0 + j), e1 = __shfl_sync(0xffffffffu, ecol, c0 + j + 1);
             const int e2 = __shfl_sync(0xffffffffu, ecol, c0 + j + 2), e3 = __shfl_sync(0xffffffffu, ecol, c0 + j + 3);
             stg_v4_f64(out + c0 + j, unscale(f[j], erow + e0), unscale(f[j + 1], erow + e1), unscale(f[j + 2], erow + e2),
@@ -382,14 +422,14 @@ __global__ void __launch_bounds__(kQThreads, 1)
           }
         } else if (mode == 2) {
 #pragma unroll
-          for (int j = 0; j < 16; j += 2) {  // transposed: the warp's 32 rows are 256 contiguous bytes of one row
+          for (int j = 0; j < DB; j += 2) {  // transposed: the warp's 32 rows are 256 contiguous bytes of one row
             const int e0 = __shfl_sync(0xffffffffu, ecol, c0 + j), e1 = __shfl_sync(0xffffffffu, ecol, c0 + j + 1);
             out_t[(int64_t)(c0 + j) * kp] = unscale(f[j], erow + e0);
             out_t[(int64_t)(c0 + j + 1) * kp] = unscale(f[j + 1], erow + e1);
           }
         } else {
 #pragma unroll
-          for (int j = 0; j < 16; j += 2) {  // keep the shuffles converged
+          for (int j = 0; j < DB; j += 2) {  // keep the shuffles converged
             __shfl_sync(0xffffffffu, ecol, c0 + j);
             __shfl_sync(0xffffffffu, ecol, c0 + j + 1);
           }
@@ -537,14 +577,24 @@ __device__ __forceinline__ void tma_store_4d(const CUtensorMap* map, const void*
       : "memory");
 }
 
-template <typename T, int S>
-__global__ void __launch_bounds__(kQ1Threads, CVG_K1Q_MIN_BLOCKS)
+//
+// DIRECT (the cut that runs beside the Gram, one CTA per SM): no shared-memory tile and no TMA -- on an SM whose
+// TMA queue and shared memory belong to a Gram CTA both would wait behind the Gram's operand stages.  A thread
+// then holds two runs of 8 consecutive rows (8 qq .. + 7 and 32 + 8 qq ..), so the 4 lanes of a column write 32
+// contiguous bytes of its 64-byte line per store instruction (whole sectors) straight from registers, and the
+// CTA publishes each finished 64-row block with a release increment of its segment's counter (seg_ready),
+// which the Gram's TMA producer acquires before the segment's first stage.  Same digits, bit for bit.
+// Registers: an SM sub-partition (16K registers) holds 3 of the lean Gram's 10 warps (96 registers) and 2 of the
+// direct cut's 8, so the cut must stay at 112 -- launch bounds of 2 x 288 threads make ptxas cap it there.
+template <typename T, int S, bool DIRECT>
+__global__ void __launch_bounds__(DIRECT ? 288 : kQ1Threads, CVG_K1Q_MIN_BLOCKS)
     reorder_q_kernel(const __grid_constant__ CUtensorMap map_out, const T* __restrict__ x, int64_t ldx,
                      const T* __restrict__ y, int64_t ldy, int64_t k, int64_t m, const int64_t* __restrict__ src_row,
                      int64_t zrows, int64_t kp, int64_t c_begin, int64_t c_end, int64_t nsrc,
                      const double* __restrict__ shift, const int* __restrict__ blkseg,
                      const unsigned long long* __restrict__ segmax, int headroom, int* __restrict__ ovf,
-                     int* __restrict__ nonfinite, int64_t blk_lo, int64_t blk_hi) {
+                     int* __restrict__ nonfinite, int64_t blk_lo, int64_t blk_hi, int8_t* __restrict__ zq,
+                     unsigned* __restrict__ seg_ready) {
   // Blocks [blk_lo, blk_hi) of Z.  map_out's box is {64, 8, 1, S}: one warp's columns.
   // Out of range: tt outside [2^52, 2^53) (a non-finite z, or w below the digits' range) or V >= 2^(7S)
   // (w above it).  With sampled exponents (ovf != null) that marks the block's segment for the exact
@@ -564,6 +614,8 @@ __global__ void __launch_bounds__(kQ1Threads, CVG_K1Q_MIN_BLOCKS)
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int j = lane >> 2, qq = lane & 3;
   const int col = 8 * w + j;  // column within the 64-column chunk
+  // row quad of batch pp: TMA tile: qq + 4 pp; DIRECT: 2 qq + (pp & 1) + 8 (pp >> 1) (8-row runs)
+  auto quad = [&](int pp) { return DIRECT ? 2 * qq + (pp & 1) + 8 * (pp >> 1) : qq + 4 * pp; };
   const int64_t wd = k + m;
   CVG_DCHECK(c_begin >= 0 && c_end <= kp && c_begin % 64 == 0 && zrows % QK == 0);
   const int64_t nchunk = (c_end - c_begin) / 64;
@@ -595,7 +647,7 @@ __global__ void __launch_bounds__(kQ1Threads, CVG_K1Q_MIN_BLOCKS)
 #pragma unroll
       for (int pp = 0; pp < kQ1PQ; ++pp)
 #pragma unroll
-        for (int i = 0; i < 4; ++i) v[4 * pp + i] = __ldg(s_row[rb][h][4 * (qq + 4 * pp) + i] + cc);
+        for (int i = 0; i < 4; ++i) v[4 * pp + i] = __ldg(s_row[rb][h][4 * quad(pp) + i] + cc);
     } else {
       shn = 0.0;
       const uint64_t pad = s_pad[rb][0] | (uint64_t)s_pad[rb][1] << 32;
@@ -603,7 +655,7 @@ __global__ void __launch_bounds__(kQ1Threads, CVG_K1Q_MIN_BLOCKS)
       for (int pp = 0; pp < kQ1PQ; ++pp)
 #pragma unroll
         for (int i = 0; i < 4; ++i)
-          v[4 * pp + i] = c == wd && !((pad >> (4 * (qq + 4 * pp) + i)) & 1) ? 1.0 : 0.0;  // ones / padding
+          v[4 * pp + i] = c == wd && !((pad >> (4 * quad(pp) + i)) & 1) ? 1.0 : 0.0;  // ones / padding
     }
   };
   int64_t blk = blk_lo + blockIdx.x;
@@ -651,9 +703,14 @@ __global__ void __launch_bounds__(kQ1Threads, CVG_K1Q_MIN_BLOCKS)
       else if (blk + grid < nblk)
         load_chunk(rn, c_begin);
       uint8_t* region = tiles + buf * (8 * kRegion) + w * kRegion;
-      // this warp's previous TMA store from this buffer has finished reading shared memory
-      if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");
-      __syncwarp();
+      if constexpr (!DIRECT) {
+        // this warp's previous TMA store from this buffer has finished reading shared memory
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");
+        __syncwarp();
+      }
+      // DIRECT: this column's 64-byte line of slice 0; slices are zrows * kp bytes apart
+      int8_t* line = zq + (blk * kp + c0 + col) * QK + 8 * qq;
+      uint32_t prev[S];
 #pragma unroll
       for (int pp = 0; pp < kQ1PQ; ++pp) {
         // quad q = qq + 4 pp of line j, SWIZZLE_64B: 16-byte chunk (q >> 2) ^ ((j >> 1) & 3)
@@ -675,15 +732,27 @@ __global__ void __launch_bounds__(kQ1Threads, CVG_K1Q_MIN_BLOCKS)
           wb[4] = __byte_perm(x0, y0, 0x5410);
           wb[5] = __byte_perm(x0, y0, 0x7632);
         }
+        if constexpr (!DIRECT) {
 #pragma unroll
-        for (int d = 0; d < S; ++d)  // digit d = byte S-1-d; offset binary -> two's complement: ^ 0x80
-          *reinterpret_cast<uint32_t*>(region + d * 512 + off) = wb[S - 1 - d] ^ 0x80808080u;
+          for (int d = 0; d < S; ++d)  // digit d = byte S-1-d; offset binary -> two's complement: ^ 0x80
+            *reinterpret_cast<uint32_t*>(region + d * 512 + off) = wb[S - 1 - d] ^ 0x80808080u;
+        } else if (pp & 1) {  // rows 8 qq + 32 (pp >> 1) .. + 7 of the line: two quads, 8 bytes
+#pragma unroll
+          for (int d = 0; d < S; ++d)
+            *reinterpret_cast<uint2*>(line + (int64_t)d * zrows * kp + 32 * (pp >> 1)) =
+                make_uint2(prev[d], wb[S - 1 - d] ^ 0x80808080u);
+        } else {
+#pragma unroll
+          for (int d = 0; d < S; ++d) prev[d] = wb[S - 1 - d] ^ 0x80808080u;
+        }
       }
-      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-      __syncwarp();
-      if (lane == 0) {
-        tma_store_4d(&map_out, region, 0, (int)c0 + 8 * w, (int)blk, 0);
-        asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+      if constexpr (!DIRECT) {
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_4d(&map_out, region, 0, (int)c0 + 8 * w, (int)blk, 0);
+          asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+        }
       }
     }
     const uint32_t oor = (oor_hi & kHiMask) | (oor_lo & kLoMask);
@@ -691,9 +760,18 @@ __global__ void __launch_bounds__(kQ1Threads, CVG_K1Q_MIN_BLOCKS)
     oor_hi = oor_lo = 0;
     // every warp is past its reads of the block before this one: its buffer takes the block two ahead
     load_src(blk + 2 * grid, rb == 0 ? 2 : rb - 1);
+    if constexpr (DIRECT) asm volatile("fence.proxy.async.global;\n" ::: "memory");  // these digits are read by TMA
     __syncthreads();
+    if constexpr (DIRECT) {
+      if (threadIdx.x == 0 && seg_ready) {  // every thread's stores of this block precede the barrier
+        __threadfence();
+        atomicAdd(seg_ready + seg, 1u);
+      }
+    }
   }
-  if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
+  if constexpr (!DIRECT) {
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
+  }
 }
 
 // 4-D map over Zq: {64 rows, kp, zrows / 64, S} bytes, box {64, box_cols, 1, box_slices (default S)}, SWIZZLE_64B.
@@ -711,25 +789,25 @@ inline bool make_zq_map(CUtensorMap* map, const int8_t* zq, int64_t zrows, int64
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int S, int KS, int kMaxSt = 8>
+template <int S, int KS, bool LEAN>
 bool launch_gram_i8_s(const int8_t* zq, const unsigned long long* segmax, int headroom, int64_t zrows, int64_t kp,
                       const GramTask* segs, int64_t seg_base, int64_t nseg, const int2* tiles, int ntiles, double* part,
-                      int max_ctas, cudaStream_t s) {
+                      int max_ctas, const unsigned* seg_ready, int* abort_flag, cudaStream_t s) {
   CUtensorMap ma, ma64, mb;
   if (!make_zq_map(&ma, zq, zrows, kp, S, QA, KS) || !make_zq_map(&ma64, zq, zrows, kp, S, QB, KS, 1) ||
       !make_zq_map(&mb, zq, zrows, kp, S, QB, KS))
     return false;
-  using C = QCfg<S, KS, kMaxSt>;
-  cudaFuncSetAttribute(gram_i8_kernel<S, KS, kMaxSt>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
+  using C = QCfg<S, KS, 8>;
+  cudaFuncSetAttribute(gram_i8_kernel<S, KS, 8, LEAN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int64_t nitems = nseg * (int64_t)ntiles;
-  // persistent: one CTA per SM (1 fits: shared memory), or max_ctas to leave SMs to a concurrent K1Q
+  // persistent: one CTA per SM (1 fits: shared memory), or max_ctas
   const int64_t blocks = std::min<int64_t>(nitems, max_ctas > 0 ? std::min(max_ctas, sms) : sms);
   if (blocks > 0)
-    gram_i8_kernel<S, KS, kMaxSt><<<(unsigned)blocks, kQThreads, C::kSmem, s>>>(ma, ma64, mb, segmax, segs, tiles, ntiles,
-                                                                                nitems, seg_base, kp, part, headroom);
+    gram_i8_kernel<S, KS, 8, LEAN><<<(unsigned)blocks, kQThreads, C::kSmem, s>>>(
+        ma, ma64, mb, segmax, segs, tiles, ntiles, nitems, seg_base, kp, part, headroom, seg_ready, abort_flag);
   return true;
 }
 
@@ -737,33 +815,43 @@ template <typename T, int S>
 bool launch_k1q(const void* x, int64_t ldx, const void* y, int64_t ldy, int64_t k, int64_t m, const int64_t* src_row,
                 int64_t zrows, int64_t kp, int64_t c_begin, int64_t c_end, int64_t nsrc, const double* shift,
                 const int* blkseg, const unsigned long long* segmax, int headroom, int* ovf, int8_t* zq, int* nonfinite,
-                int64_t blk_lo, int64_t blk_hi, int max_sms, cudaStream_t s) {
+                int64_t blk_lo, int64_t blk_hi, int max_sms, int direct_ctas_per_sm, unsigned* seg_ready,
+                cudaStream_t s) {
+  int dev = 0, sms_all = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms_all, cudaDevAttrMultiProcessorCount, dev);
+  if (direct_ctas_per_sm > 0) {  // the register-only cut (beside the Gram: one CTA per SM)
+    CUtensorMap none{};
+    const int64_t blocks = std::min<int64_t>(blk_hi - blk_lo, (int64_t)direct_ctas_per_sm * sms_all);
+    if (blocks <= 0) return true;
+    // same shared-memory carveout as the Gram it shares the SM with (an SM holds one configuration at a time)
+    cudaFuncSetAttribute(reorder_q_kernel<T, S, true>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         cudaSharedmemCarveoutMaxShared);
+    reorder_q_kernel<T, S, true><<<(unsigned)blocks, kQ1Threads, 0, s>>>(
+        none, (const T*)x, ldx, (const T*)y, ldy, k, m, src_row, zrows, kp, c_begin, c_end, nsrc, shift, blkseg, segmax,
+        headroom, ovf, nonfinite, blk_lo, blk_hi, zq, seg_ready);
+    return true;
+  }
   CUtensorMap mo;
   if (!make_zq_map(&mo, zq, zrows, kp, S, 8)) return false;
   constexpr int smem = k1q_smem_bytes<S>();
   // grid-stride over one wave of resident CTAs.  Function attributes are per device (one process may drive
   // several: cvg_context_create_multi), so they are set on every launch; the occupancy query is cached per device.
   static std::atomic<int> wave_cache[64];
-  int dev = 0;
-  cudaGetDevice(&dev);
-  cudaFuncSetAttribute(reorder_q_kernel<T, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(reorder_q_kernel<T, S, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   int wave = wave_cache[dev & 63].load(std::memory_order_relaxed);
   if (!wave) {
-    int sms = 0, per_sm = 0;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, reorder_q_kernel<T, S>, kQ1Threads, smem);
-    wave = (per_sm > 0 ? per_sm : 1) * sms;
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, reorder_q_kernel<T, S, false>, kQ1Threads, smem);
+    wave = (per_sm > 0 ? per_sm : 1) * sms_all;
     wave_cache[dev & 63].store(wave, std::memory_order_relaxed);
   }
-  int sms_all = 0;
-  cudaDeviceGetAttribute(&sms_all, cudaDevAttrMultiProcessorCount, dev);
   if (max_sms > 0 && max_sms < sms_all) wave = wave / sms_all * max_sms;  // confine to max_sms SMs' worth
   const int64_t blocks = std::min<int64_t>(blk_hi - blk_lo, (int64_t)std::max(wave, 1));
   if (blocks <= 0) return true;
-  reorder_q_kernel<T, S><<<(unsigned)blocks, kQ1Threads, smem, s>>>(mo, (const T*)x, ldx, (const T*)y, ldy, k, m,
-                                                                    src_row, zrows, kp, c_begin, c_end, nsrc, shift,
-                                                                    blkseg, segmax, headroom, ovf, nonfinite, blk_lo,
-                                                                    blk_hi);
+  reorder_q_kernel<T, S, false><<<(unsigned)blocks, kQ1Threads, smem, s>>>(
+      mo, (const T*)x, ldx, (const T*)y, ldy, k, m, src_row, zrows, kp, c_begin, c_end, nsrc, shift, blkseg, segmax,
+      headroom, ovf, nonfinite, blk_lo, blk_hi, zq, nullptr);
   return true;
 }
 
@@ -794,12 +882,12 @@ bool launch_reorder_q(int dtype, int slices, const void* x, int64_t ldx, const v
                       int64_t m, const int64_t* src_row, int64_t zrows, int64_t kp, int64_t c_begin, int64_t c_end,
                       int64_t nsrc, const double* shift, const int* blkseg, const unsigned long long* segmax,
                       int headroom, int* ovf, int8_t* zq, int* nonfinite, cudaStream_t s, int64_t blk_lo,
-                      int64_t blk_hi, int max_sms) {
+                      int64_t blk_hi, int max_sms, int direct_ctas_per_sm, unsigned* seg_ready) {
   if (zrows <= 0 || c_end <= c_begin) return true;
   if (blk_hi < 0) blk_hi = zrows / QK;
 #define CVG_K1Q(T, S)                                                                                              \
   return launch_k1q<T, S>(x, ldx, y, ldy, k, m, src_row, zrows, kp, c_begin, c_end, nsrc, shift, blkseg, segmax, \
-                          headroom, ovf, zq, nonfinite, blk_lo, blk_hi, max_sms, s)
+                          headroom, ovf, zq, nonfinite, blk_lo, blk_hi, max_sms, direct_ctas_per_sm, seg_ready, s)
   (void)dtype;  // fp64 inputs only (fp32 inputs take the fp16-split Gram)
   if (slices == 5) CVG_K1Q(double, 5);
   CVG_K1Q(double, 6);
@@ -816,17 +904,25 @@ static int i8_stage_rows() {
   return v;
 }
 
+// lean != 0: the 96-register kernel that leaves room for a cut CTA on the same SM; seg_ready / abort_flag (both
+// or neither): wait for the concurrent cut's per-segment block counts.
 bool launch_gram_i8(int slices, const int8_t* zq, const unsigned long long* segmax, int headroom, int64_t zrows,
                     int64_t kp, const GramTask* segs, int64_t nseg, const int2* tiles, int ntiles, double* part,
-                    cudaStream_t s, int64_t seg_base, int max_ctas) {
-#define CVG_GRAM_I8(S)                                                                                             \
-  return i8_stage_rows() == 64                                                                                     \
-             ? launch_gram_i8_s<S, 64>(zq, segmax, headroom, zrows, kp, segs, seg_base, nseg, tiles, ntiles, part, \
-                                       max_ctas, s)                                                                \
-             : launch_gram_i8_s<S, 32>(zq, segmax, headroom, zrows, kp, segs, seg_base, nseg, tiles, ntiles, part, \
-                                       max_ctas, s)
-  if (slices == 5) CVG_GRAM_I8(5);
-  CVG_GRAM_I8(6);
+                    cudaStream_t s, int64_t seg_base, int max_ctas, int lean, const unsigned* seg_ready,
+                    int* abort_flag) {
+#define CVG_GRAM_I8(S, KS, LEAN)                                                                                \
+  return launch_gram_i8_s<S, KS, LEAN>(zq, segmax, headroom, zrows, kp, segs, seg_base, nseg, tiles, ntiles, part, \
+                                       max_ctas, seg_ready, abort_flag, s)
+  if (lean) {
+    if (slices == 5) CVG_GRAM_I8(5, 64, true);
+    CVG_GRAM_I8(6, 64, true);
+  }
+  if (i8_stage_rows() == 64) {
+    if (slices == 5) CVG_GRAM_I8(5, 64, false);
+    CVG_GRAM_I8(6, 64, false);
+  }
+  if (slices == 5) CVG_GRAM_I8(5, 32, false);
+  CVG_GRAM_I8(6, 32, false);
 #undef CVG_GRAM_I8
 }
 
