@@ -376,21 +376,36 @@ def run_ours(args):
     launches = ctx.launches - launches0
     # per-kernel times: the same K steps again, untimed, with an event pair around every launch (the events
     # would add their own gaps to the timed region above)
-    L.lib().cvg_context_enable_timing(ctx.handle, 1)
-    for _ in range(args.steps):
-        step()
-    torch.cuda.synchronize(dev)
-    kms = np.zeros(6)
-    kcnt = np.zeros(6, np.int64)
-    L.lib().cvg_context_kernel_times(ctx.handle, kms.ctypes.data, kcnt.ctypes.data)
-    L.lib().cvg_context_enable_timing(ctx.handle, 0)
+    # The fp64 path's timed steps run K1Q's cut beside the Gram (one launch region); each kernel's own duration
+    # (the rooflines) comes from this pass in the serial schedule (CVG_I8_OVERLAP=0: every kernel alone on the
+    # GPU), and a second pass in the step's own schedule times the shared region.
+    def kernel_pass(overlap):
+        prev = os.environ.get("CVG_I8_OVERLAP")
+        if overlap is not None:
+            os.environ["CVG_I8_OVERLAP"] = overlap
+        L.lib().cvg_context_enable_timing(ctx.handle, 1)
+        for _ in range(args.steps):
+            step()
+        torch.cuda.synchronize(dev)
+        t, c = np.zeros(6), np.zeros(6, np.int64)
+        L.lib().cvg_context_kernel_times(ctx.handle, t.ctypes.data, c.ctypes.data)
+        L.lib().cvg_context_enable_timing(ctx.handle, 0)
+        if overlap is not None:
+            if prev is None:
+                del os.environ["CVG_I8_OVERLAP"]
+            else:
+                os.environ["CVG_I8_OVERLAP"] = prev
+        return t, c
+
+    kms, kcnt = kernel_pass("0")
+    kms_step, _ = kernel_pass(None) if x.dtype == torch.float64 else (kms, None)
     if world > 1:
         t = torch.tensor([ms], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-        kt = torch.tensor(kms, device=dev)
+        kt = torch.tensor(np.stack([kms, kms_step]), device=dev)
         dist.all_reduce(kt, op=dist.ReduceOp.MAX)
-        kms = kt.cpu().numpy()
+        kms, kms_step = kt.cpu().numpy()
     value = flops / (ms * 1e-3) / 1e9
     x_elt = x.element_size()
 
@@ -503,6 +518,16 @@ def run_ours(args):
                f"step, steps timed individually"),
     }
     line.update(rooflines(cid, n, k, m, p, masks, world, flops, kms, kcnt, args.steps, x_elt))
+    if kms_step is not kms and kms_step[1] < 0.5 * kms[1]:  # the step's schedule merged K1Q into the Gram region
+        region = float(kms_step[2]) / args.steps
+        line["schedule"] = {
+            "cut_beside_gram_ms": round(region, 4),
+            "serial_cut_plus_gram_ms": round(float(kms[1] + kms[2]) / args.steps - float(kms_step[1]) / args.steps, 4),
+            "note": "timed steps: the int8 digit cut (direct-store K1Q, one CTA per SM) runs beside the lean Gram "
+                    "(CVG_I8_OVERLAP=0 restores K1Q -> Gram); roofline / hbm_rooflines / kernels_ms_per_step time "
+                    "each kernel alone (serial-schedule pass), cut_beside_gram_ms is the shared region of the "
+                    "step's own schedule, serial_cut_plus_gram_ms the same two kernels back to back"}
+        line["roofline"]["launch_ms_in_step"] = round(region, 4)
     line["gpu_launches"] = int(launches)
     line["clocks"] = clocks.summary()
     if e2e:

@@ -528,7 +528,19 @@ Status Plan::bind_labels(const int32_t* d_labels, bool validate, bool require_sc
     for (int32_t f = 0; f < p_; ++f) mx = std::max(mx, counts_[f]);
     small_ = mx <= kSmallFoldRows;
   }
-  CVG_TRY(plan_segments());
+  {
+    // The segment plan (Z layout, segment list, block -> segment table, tree ops, fold pointers and their
+    // device copies) is a function of the fold sizes and this plan's window only: binding another
+    // partitioning with the same sizes (repeated CV over equal-sized folds) reuses it, which takes the host
+    // planning and its uploads out of the gap between the fold counts' read-back and the scatter.
+    PlanKey key{counts_, fb_, fe_, seg_lo_, seg_hi_, row_step_, small_, i8_path()};
+    if (!(planned_ && key == plan_key_)) {
+      planned_ = false;
+      CVG_TRY(plan_segments());
+      plan_key_ = std::move(key);
+      planned_ = true;
+    }
+  }
   CVG_CK(cudaMemsetAsync(src_row_.as<void>(), 0xff, sizeof(int64_t) * std::max<int64_t>(zrows_, 1), s));
   {
     Timed t(ctx_, kBucket);
@@ -567,6 +579,7 @@ Status Plan::bind_rows(const int64_t* rows, int64_t nrows, int64_t n_src) {
     if (rows[i] < 0 || rows[i] >= src_n_) return Status::Err(4, "bind_rows: row index outside the source matrix");
   counts_.assign(1, nrows);
   choose_row_step();
+  planned_ = false;
   CVG_TRY(plan_segments());
   std::vector<int64_t> src(std::max<int64_t>(zrows_, 1), -1);
   std::copy(rows, rows + nrows, src.begin());

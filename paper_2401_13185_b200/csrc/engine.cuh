@@ -189,6 +189,18 @@ class Plan {
   int sample_ = 16;             // int8 path: segment maxima over every sample_-th row (CVG_I8_SAMPLE; 1 = exact)
   int64_t exact_segments_ = 0;  // segments the last gram redid from their exact max
   std::vector<int> ovf_host_;
+  struct PlanKey {  // what plan_segments() depends on
+    std::vector<int64_t> counts;
+    int32_t fb = 0, fe = 0;
+    int64_t seg_lo = 0, seg_hi = 0, row_step = 0;
+    bool small = false, i8 = false;
+    bool operator==(const PlanKey& o) const {
+      return fb == o.fb && fe == o.fe && seg_lo == o.seg_lo && seg_hi == o.seg_hi && row_step == o.row_step &&
+             small == o.small && i8 == o.i8 && counts == o.counts;
+    }
+  };
+  PlanKey plan_key_;
+  bool planned_ = false;        // plan_key_ describes the segment plan the device buffers hold
   DevBuf seg_ready_;            // overlapped cut: per-segment finished-block counts + the abort flag (last word)
   bool overlapped_ = false;     // the last gram ran the cut beside the Gram (its abort flag is pending)
   int slices_ = 6;              // base-256 int8 digits per value (fp64: CVG_I8_SLICES = 5 | 6; fp32: CVG_I8_SLICES_F32 = 3 | 4)
