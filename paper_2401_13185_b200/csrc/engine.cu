@@ -851,12 +851,17 @@ Status Plan::i8_gram(const int2* tiles, int ntiles) {
 }
 
 // K1Q's HBM-bound cut runs beside the tensor-bound Gram instead of before it when the segments are long
-// enough (>= 1024 rows on average: short segments pay the per-item acquire and keep the 16-column drain);
+// enough (>= 1024 rows on average: short segments pay the per-item acquire and keep the 16-column drain)
 // CVG_I8_OVERLAP=0 keeps the serial schedule, =1 forces the overlap.  Read per call (tests A/B both).
 bool Plan::i8_overlap_enabled() const {
   const char* v = std::getenv("CVG_I8_OVERLAP");
   if (v && (v[0] == '0' || v[0] == '1')) return v[0] == '1';
-  return !segs_.empty() && zrows_ / (int64_t)segs_.size() >= 1024;
+  if (segs_.empty() || zrows_ / (int64_t)segs_.size() < 1024) return false;
+  // ... and with at least ~2.5 waves of Gram items: below that (c1 on 8 GPUs: 12 folds = 216 items) the Gram's
+  // first wave only waits for the cut (measured per rank: 0.78-0.82 ms together, 0.75-0.77 ms back to back)
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx_->device);
+  return (int64_t)segs_.size() * (int64_t)tilesq_.size() * 2 >= 5 * (int64_t)sms;
 }
 
 // The cut beside the Gram.  The aux stream runs the direct-store cut on one persistent CTA per SM (Z order);

@@ -46,8 +46,10 @@ __global__ void __launch_bounds__(256) tree_op_kernel(const TreeOp* __restrict__
   CVG_DCHECK(d != nullptr && size >= 0);
   CVG_DCHECK(tile.x >= 0 && tile.x <= tile.y && (int64_t)(tile.y + 1) * kTile <= kp);
   const int c2 = (threadIdx.x & 31) * 2;  // column pair within the tile
+  // gridDim.z row slices of the tile: a level with few ops (a tree's top) still spreads over the SMs
+  const int rows = kTile / (int)gridDim.z, r0 = (int)blockIdx.z * rows;
 #pragma unroll 2
-  for (int r = threadIdx.x >> 5; r < kTile; r += 8) {
+  for (int r = r0 + (threadIdx.x >> 5); r < r0 + rows; r += 8) {
     const int64_t off = ((int64_t)tile.x * kTile + r) * kp + (int64_t)tile.y * kTile + c2;
     int idx = 0;
     const double2 v = size > 0 ? tree_node<kTreeFanDepth>(op, size, idx, off) : make_double2(0.0, 0.0);
@@ -68,8 +70,10 @@ void launch_poison_if_flag(const int* flag, double* g, cudaStream_t s) { poison_
 
 void launch_tree_ops(const TreeOp* ops, int nops, int64_t kp, const int2* tiles, int ntiles, cudaStream_t s) {
   if (nops <= 0 || ntiles <= 0) return;
+  int slices = 1;  // 8 .. 64 rows per CTA: at least ~4 CTAs per SM while the level is small
+  while (slices < 8 && (int64_t)ntiles * nops * slices < 600) slices *= 2;
   for (int o = 0; o < nops; o += 65535) {  // gridDim.y <= 65535 (a level of a leave-one-out tree can hold N ops)
-    dim3 grid((unsigned)ntiles, (unsigned)(nops - o < 65535 ? nops - o : 65535));
+    dim3 grid((unsigned)ntiles, (unsigned)(nops - o < 65535 ? nops - o : 65535), (unsigned)slices);
     tree_op_kernel<<<grid, 256, 0, s>>>(ops + o, kp, tiles);
   }
 }
