@@ -208,7 +208,12 @@ bool launch_reorder_q(int dtype, int slices, const void* x, int64_t ldx, const v
 bool launch_gram_i8(int slices, const int8_t* zq, const unsigned long long* segmax, int headroom, int64_t zrows,
                     int64_t kp, const GramTask* segs, int64_t nseg, const int2* tiles, int ntiles, double* part,
                     cudaStream_t s, int64_t seg_base = 0, int max_ctas = 0, int lean = 0,
-                    const unsigned* seg_ready = nullptr, int* abort_flag = nullptr);
+                    const unsigned* seg_ready = nullptr, int* abort_flag = nullptr, int32_t* split_ws = nullptr,
+                    unsigned* split_cnt = nullptr, int64_t min_seg_rows = 0);
+// split_ws (gram_i8_split_ws_bytes(SM count) bytes) + split_cnt (SM count words): the items past the grid's last
+// full round are cut into row parts whose exact int32 sums are added by the part that finishes last (bit-identical
+// to the unsplit item); min_seg_rows bounds the split so every part keeps a few stages.
+size_t gram_i8_split_ws_bytes(int ctas);
 
 inline int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
 inline int64_t padded_cols(int64_t k, int64_t m, int dtype = 0) {

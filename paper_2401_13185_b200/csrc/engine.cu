@@ -837,14 +837,30 @@ Status Plan::i8_prep(const void* d_x, int64_t ldx, const void* d_y, int64_t ldy,
   return count_launch();
 }
 
+// The int8 Gram's tail-split workspace (k_gram_i8.cu): sized for one part per SM.  CVG_I8_SPLIT=0 disables it.
+Status Plan::ensure_split_ws() {
+  const char* v = std::getenv("CVG_I8_SPLIT");
+  if (v && v[0] == '0') {
+    split_ws_.release();
+    split_cnt_.release();
+    return Status::Ok();
+  }
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx_->device);
+  CVG_TRY(split_ws_.ensure(gram_i8_split_ws_bytes(sms)));
+  return split_cnt_.ensure(sizeof(unsigned) * (size_t)sms);
+}
+
 Status Plan::i8_gram(const int2* tiles, int ntiles) {
   if (segs_.empty() || ntiles == 0) return Status::Ok();
   bool ok;
   {
     Timed t(ctx_, kGram);
+    CVG_TRY(ensure_split_ws());
     ok = launch_gram_i8(slices_, zq_.as<int8_t>(), segmax_.as<unsigned long long>(), sample_ > 1 ? 1 : 0, zrows_, kp_,
                         segs_d_.as<GramTask>(), (int64_t)segs_.size(), tiles, ntiles, part_.as<double>(),
-                        ctx_->stream);
+                        ctx_->stream, 0, 0, 0, nullptr, nullptr, split_ws_.as<int32_t>(), split_cnt_.as<unsigned>(),
+                        min_seg_rows());
   }
   if (!ok) return Status::Err(5, "cuTensorMapEncodeTiled unavailable or rejected the operand layout");
   return count_launch();
@@ -871,6 +887,7 @@ Status Plan::i8_overlapped(const void* d_x, int64_t ldx, const void* d_y, int64_
                            int64_t nsrc) {
   cudaStream_t s = ctx_->stream;
   CVG_TRY(ctx_->ensure_aux_stream());
+  CVG_TRY(ensure_split_ws());
   const bool sampled = sample_ > 1;
   const size_t nseg = segs_.size();
   CVG_TRY(seg_ready_.ensure(sizeof(unsigned) * (nseg + 1)));
@@ -899,7 +916,8 @@ Status Plan::i8_overlapped(const void* d_x, int64_t ldx, const void* d_y, int64_
     ok = ok && launch_gram_i8(slices_, zq_.as<int8_t>(), segmax_.as<unsigned long long>(), sampled ? 1 : 0, zrows_, kp_,
                               segs_d_.as<GramTask>(), (int64_t)nseg, tilesq_d_.as<int2>(), (int)tilesq_.size(),
                               part_.as<double>(), s, 0, 0, 1, seg_ready_.as<unsigned>(),
-                              reinterpret_cast<int*>(seg_ready_.as<unsigned>() + nseg));
+                              reinterpret_cast<int*>(seg_ready_.as<unsigned>() + nseg), split_ws_.as<int32_t>(),
+                              split_cnt_.as<unsigned>(), min_seg_rows());
     CVG_CK(cudaStreamWaitEvent(s, ev1, 0));
   }
   if (!ok) return Status::Err(5, "cuTensorMapEncodeTiled unavailable or rejected the operand layout");

@@ -142,6 +142,7 @@ class Plan {
   Status i8_prep(const void* d_x, int64_t ldx, const void* d_y, int64_t ldy, const int64_t* rows, int64_t nsrc,
                  int64_t c0, int64_t c1, bool exact);
   Status i8_gram(const int2* tiles, int ntiles);
+  Status ensure_split_ws();
   Status i8_exact_pass(const void* d_x, int64_t ldx, const void* d_y, int64_t ldy, const int64_t* rows, int64_t nsrc);
   // the cut beside the Gram (engine.cu; CVG_I8_OVERLAP=0|1 overrides the segment-length rule): one direct-store cut CTA and one lean Gram CTA per SM
   Status i8_overlapped(const void* d_x, int64_t ldx, const void* d_y, int64_t ldy, const int64_t* rows, int64_t nsrc);
@@ -166,6 +167,11 @@ class Plan {
   void assign_rank();  // rank mode: fb_/fe_, segment window, fold group
   int64_t chunk_rows() const;
   int64_t seg_rows(int64_t count) const;
+  int64_t min_seg_rows() const {
+    int64_t r = INT64_MAX;
+    for (const GramTask& g : segs_) r = std::min(r, g.rows);
+    return segs_.empty() ? 0 : r;
+  }
   int64_t max_seg_rows() const {
     int64_t r = 0;
     for (const GramTask& g : segs_) r = std::max(r, g.rows);
@@ -201,6 +207,7 @@ class Plan {
   };
   PlanKey plan_key_;
   bool planned_ = false;        // plan_key_ describes the segment plan the device buffers hold
+  DevBuf split_ws_, split_cnt_;  // int8 Gram tail split: int32 dumps and per-item arrival counters
   DevBuf seg_ready_;            // overlapped cut: per-segment finished-block counts + the abort flag (last word)
   bool overlapped_ = false;     // the last gram ran the cut beside the Gram (its abort flag is pending)
   int slices_ = 6;              // base-256 int8 digits per value (fp64: CVG_I8_SLICES = 5 | 6; fp32: CVG_I8_SLICES_F32 = 3 | 4)

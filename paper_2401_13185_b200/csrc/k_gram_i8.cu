@@ -246,7 +246,8 @@ __global__ void __launch_bounds__(kQThreads, LEAN ? 2 : 1)
                    const unsigned long long* __restrict__ segmax, const GramTask* __restrict__ segs,
                    const int2* __restrict__ tiles, int ntiles, int64_t nitems, int64_t seg_base, int64_t kp,
                    double* __restrict__ part, int headroom, const unsigned* __restrict__ seg_ready,
-                   int* __restrict__ abort_flag) {
+                   int* __restrict__ abort_flag, int64_t split_from, int split_f, int32_t* __restrict__ split_ws,
+                   unsigned* __restrict__ split_cnt) {
   using C = QCfg<S, KS, kMaxSt>;
   constexpr int NST = C::kNst;
   constexpr int kPer = QK / KS;  // stages per 64-row block
@@ -254,6 +255,7 @@ __global__ void __launch_bounds__(kQThreads, LEAN ? 2 : 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   __shared__ __align__(8) uint64_t full_bar[NST], empty_bar[NST], acc_full, tmem_empty;
   __shared__ uint32_t tmem_base;
+  __shared__ bool s_last;  // tail split: this CTA's part arrived last
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t G = gridDim.x;
 
@@ -279,7 +281,22 @@ __global__ void __launch_bounds__(kQThreads, LEAN ? 2 : 1)
   auto opA = [&](int s) { return smem + s * C::kStage; };
   auto opB = [&](int s) { return smem + s * C::kStage + S * C::kA; };
   // item -> (segment, A halves a0 / a1, B block c, half modes)
+  // Tail split (split_f > 1): the items past the last full round of the grid (virtual indices >= split_from) are
+  // each cut into split_f row parts, so the partial last round fills the SMs with short parts instead of running
+  // a few whole items.  A part accumulates its rows' exact int32 sums and dumps them; the part that arrives last
+  // adds all dumps -- integer adds, so the order does not matter and the total is the un-split item's own
+  // accumulator, bit for bit -- and drains as usual.  Nobody waits for anybody.
+  int tail = -1, rpart = 0;  // tail item index (else -1) and row part of the item decoded last
+  int st0 = 0, st1 = 0;      // its stage range
   auto item = [&](int64_t it, int& seg, int& a0, int& a1, int& c, int& modes, GramTask& task) {
+    tail = -1;
+    rpart = 0;
+    if (split_f > 1 && it >= split_from) {
+      const int64_t v = it - split_from;
+      tail = (int)(v / split_f);
+      rpart = (int)(v - (int64_t)tail * split_f);
+      it = split_from + tail;
+    }
     const int64_t sl = it / ntiles;  // segment within this launch's range [seg_base, seg_base + nitems / ntiles)
     seg = (int)(seg_base + sl);
     const int2 tile0 = tiles[it - sl * ntiles];
@@ -291,6 +308,10 @@ __global__ void __launch_bounds__(kQThreads, LEAN ? 2 : 1)
     task = GramTask{uniform(task0.zrow), uniform(task0.rows)};
     CVG_DCHECK(task.zrow % QK == 0 && task.rows % QK == 0 && task.rows > 0);
     CVG_DCHECK((int64_t)c * QB < kp && (int64_t)a0 * QB < kp && (int64_t)a1 * QB < kp && (modes & 3) != 0);
+    const int nst = (int)(task.rows / KS);
+    st0 = tail < 0 ? 0 : (int)((int64_t)nst * rpart / split_f);
+    st1 = tail < 0 ? nst : (int)((int64_t)nst * (rpart + 1) / split_f);
+    CVG_DCHECK(st1 > st0);
   };
 
   if (warp == 0) {  // ---- TMA producer (whole warp waits; one elected lane issues)
@@ -302,7 +323,6 @@ __global__ void __launch_bounds__(kQThreads, LEAN ? 2 : 1)
       const bool use0 = (modes & 3) != 0, use1 = ((modes >> 2) & 3) != 0;
       const bool aligned = use0 && use1 && a1 == a0 + 1 && (a0 & 1) == 0;
       const uint32_t bytes = (uint32_t)(S * ((use0 + use1) * (C::kA / 2) + C::kB));
-      const int nsteps = (int)(task.rows / KS);
       if (seg_ready) {  // the concurrent cut has published every 64-row block of this segment
         const unsigned need = (unsigned)(task.rows / QK);
         if (ld_acquire_u32(seg_ready + seg) < need) {
@@ -319,7 +339,7 @@ __global__ void __launch_bounds__(kQThreads, LEAN ? 2 : 1)
         asm volatile("fence.proxy.async.global;\n" ::: "memory");  // generic-proxy digits -> TMA reads
         __syncwarp();
       }
-      for (int st = 0; st < nsteps; ++st, ++g) {
+      for (int st = st0; st < st1; ++st, ++g) {
         const int s = (int)(g % NST);
         mbar_wait(&empty_bar[s], ((uint32_t)(g / NST) & 1u) ^ 1u);
         const int blk = (int)(task.zrow / QK) + st / kPer, r0 = (st % kPer) * KS;
@@ -346,12 +366,11 @@ __global__ void __launch_bounds__(kQThreads, LEAN ? 2 : 1)
       int seg, a0, a1, c, modes;
       GramTask task;
       item(it, seg, a0, a1, c, modes, task);
-      const int nsteps = (int)(task.rows / KS);
       if (t > 0) {  // the drain warps have read the previous item's accumulators
         mbar_wait(&tmem_empty, (uint32_t)(t - 1) & 1u);
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
       }
-      for (int st = 0; st < nsteps; ++st, ++g) {
+      for (int st = st0; st < st1; ++st, ++g) {
         const int s = (int)(g % NST);
         mbar_wait(&full_bar[s], (uint32_t)(g / NST) & 1u);
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
@@ -361,9 +380,9 @@ __global__ void __launch_bounds__(kQThreads, LEAN ? 2 : 1)
         if (elect_one()) {
 #pragma unroll
           for (int k = 0; k < KS / 32; ++k)  // K = 32 int8 = 32 B per MMA: +2 in 16-byte descriptor units
-            mma_slices<S, 0>(tmem_d, a0 + 2ull * k, a_step, b0 + 2ull * k, b_step, st == 0 && k == 0);
+            mma_slices<S, 0>(tmem_d, a0 + 2ull * k, a_step, b0 + 2ull * k, b_step, st == st0 && k == 0);
           mma_commit(&empty_bar[s]);  // frees the stage once these MMAs have read it
-          if (st == nsteps - 1) mma_commit(&acc_full);
+          if (st == st1 - 1) mma_commit(&acc_full);
         }
         __syncwarp();
       }
@@ -389,29 +408,31 @@ __global__ void __launch_bounds__(kQThreads, LEAN ? 2 : 1)
       double* out = part + (int64_t)seg * kp * kp + row * kp + col0;
       double* out_t = part + (int64_t)seg * kp * kp + col0 * kp + row;  // mode 2: element (row, col0 + j) at (col0 + j, row)
       constexpr int DB = LEAN ? 8 : 16;  // accumulator columns per batch
+      constexpr int NACC = kNAcc<S>;
+      // TMEM -> registers: all accumulators' DB columns in one batch of loads (one wait: the MMAs restart sooner)
+      auto load_acc = [&](uint32_t (&r)[NACC][DB], int c0) {
 #pragma unroll
-      for (int c0 = 0; c0 < 32; c0 += DB) {
-        // all accumulators' DB columns in one batch of TMEM loads (one wait: the item's MMAs restart sooner)
-        uint32_t r[kNAcc<S>][DB];
-#pragma unroll
-        for (int d = 0; d < kNAcc<S>; ++d) {
+        for (int d = 0; d < NACC; ++d) {
           const uint32_t ta = tmem_d + ((uint32_t)(32 * q) << 16) + (uint32_t)(d * QB + 32 * h + c0);
           if constexpr (LEAN) tmem_ld8_nowait(ta, r[d]);
           else tmem_ld16_nowait(ta, r[d]);
         }
         tmem_ld_wait();
+      };
+      auto release_tmem = [&]() {  // every accumulator column of this thread has been read: the MMA warp may go on
+        asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tmem_empty);
+      };
+      // exact Horner over the diagonal accumulators, unscale, store this thread's DB entries of its row
+      auto emit = [&](uint32_t (&r)[NACC][DB], int c0) {
         double f[DB];
 #pragma unroll
-        for (int j = 0; j < DB; ++j) f[j] = i2d_exact(r[kNAcc<S> - 1][j]);
+        for (int j = 0; j < DB; ++j) f[j] = i2d_exact(r[NACC - 1][j]);
 #pragma unroll
-        for (int d = kNAcc<S> - 2; d >= 0; --d)
+        for (int d = NACC - 2; d >= 0; --d)
 #pragma unroll
           for (int j = 0; j < DB; ++j) f[j] = fma(f[j], 0x1p-8, i2d_exact(r[d][j]));  // f * 2^-8 exact
-        if (c0 == 32 - DB) {  // every accumulator column of this thread has been read: the MMA warp may go on
-          asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&tmem_empty);
-        }
         if (mode == 1) {
 #pragma unroll
           for (int j = 0; j < DB; j += 4) {  // 32-byte stores: a lane's row segment is whole sectors
@@ -432,6 +453,59 @@ __global__ void __launch_bounds__(kQThreads, LEAN ? 2 : 1)
           for (int j = 0; j < DB; j += 2) {  // keep the shuffles converged
             __shfl_sync(0xffffffffu, ecol, c0 + j);
             __shfl_sync(0xffffffffu, ecol, c0 + j + 1);
+          }
+        }
+      };
+      if (tail < 0) {
+#pragma unroll
+        for (int c0 = 0; c0 < 32; c0 += DB) {
+          uint32_t r[NACC][DB];
+          load_acc(r, c0);
+          if (c0 == 32 - DB) release_tmem();
+          emit(r, c0);
+        }
+      } else {
+        // a row part of a tail item: dump the exact int32 sums ([accumulator][column][tile row], coalesced over
+        // the lanes' rows); the part that arrives last adds every part's dump and drains
+        constexpr int64_t kDump = (int64_t)NACC * QB * QA;
+        int32_t* ws = split_ws + (int64_t)tail * split_f * kDump;
+        const int trow = 32 * q + lane;
+#pragma unroll
+        for (int c0 = 0; c0 < 32; c0 += DB) {
+          uint32_t r[NACC][DB];
+          load_acc(r, c0);
+          if (c0 == 32 - DB) release_tmem();
+          int32_t* my = ws + (int64_t)rpart * kDump + (int64_t)(32 * h + c0) * QA + trow;
+#pragma unroll
+          for (int d = 0; d < NACC; ++d)
+#pragma unroll
+            for (int j = 0; j < DB; ++j) my[((int64_t)d * QB + j) * QA] = (int32_t)r[d][j];
+        }
+        __threadfence();
+        asm volatile("bar.sync 1, %0;\n" ::"n"(32 * kQEpiWarps) : "memory");  // the drain warps' dumps are out
+        if (threadIdx.x == 64) {
+          const unsigned prev = atomicAdd(split_cnt + tail, 1u);
+          s_last = prev + 1u == (unsigned)split_f;
+          if (s_last) split_cnt[tail] = 0u;  // ready for the next launch
+        }
+        asm volatile("bar.sync 1, %0;\n" ::"n"(32 * kQEpiWarps) : "memory");
+        if (s_last) {
+          __threadfence();
+#pragma unroll
+          for (int c0 = 0; c0 < 32; c0 += DB) {
+            uint32_t r[NACC][DB];
+#pragma unroll
+            for (int d = 0; d < NACC; ++d)
+#pragma unroll
+              for (int j = 0; j < DB; ++j) r[d][j] = 0u;
+            for (int pf = 0; pf < split_f; ++pf) {
+              const int32_t* src = ws + (int64_t)pf * kDump + (int64_t)(32 * h + c0) * QA + trow;
+#pragma unroll
+              for (int d = 0; d < NACC; ++d)
+#pragma unroll
+                for (int j = 0; j < DB; ++j) r[d][j] += (uint32_t)__ldcg(src + ((int64_t)d * QB + j) * QA);
+            }
+            emit(r, c0);
           }
         }
       }
@@ -792,7 +866,8 @@ inline bool make_zq_map(CUtensorMap* map, const int8_t* zq, int64_t zrows, int64
 template <int S, int KS, bool LEAN>
 bool launch_gram_i8_s(const int8_t* zq, const unsigned long long* segmax, int headroom, int64_t zrows, int64_t kp,
                       const GramTask* segs, int64_t seg_base, int64_t nseg, const int2* tiles, int ntiles, double* part,
-                      int max_ctas, const unsigned* seg_ready, int* abort_flag, cudaStream_t s) {
+                      int max_ctas, const unsigned* seg_ready, int* abort_flag, int32_t* split_ws, unsigned* split_cnt,
+                      int64_t min_seg_rows, cudaStream_t s) {
   CUtensorMap ma, ma64, mb;
   if (!make_zq_map(&ma, zq, zrows, kp, S, QA, KS) || !make_zq_map(&ma64, zq, zrows, kp, S, QB, KS, 1) ||
       !make_zq_map(&mb, zq, zrows, kp, S, QB, KS))
@@ -805,9 +880,20 @@ bool launch_gram_i8_s(const int8_t* zq, const unsigned long long* segmax, int he
   const int64_t nitems = nseg * (int64_t)ntiles;
   // persistent: one CTA per SM (1 fits: shared memory), or max_ctas
   const int64_t blocks = std::min<int64_t>(nitems, max_ctas > 0 ? std::min(max_ctas, sms) : sms);
-  if (blocks > 0)
-    gram_i8_kernel<S, KS, 8, LEAN><<<(unsigned)blocks, kQThreads, C::kSmem, s>>>(
-        ma, ma64, mb, segmax, segs, tiles, ntiles, nitems, seg_base, kp, part, headroom, seg_ready, abort_flag);
+  if (blocks <= 0) return true;
+  // Tail split (kernel comment): the `tail` items past the last full round become tail * f row parts, at most one
+  // more round of the grid; only when they fill at most half of it and every part keeps >= 4 stages.
+  const int64_t tail = nitems % blocks;
+  int64_t f = 1;
+  if (split_ws && split_cnt && tail > 0 && 2 * tail <= blocks) {
+    f = std::min<int64_t>(blocks / tail, 8);
+    while (f > 1 && min_seg_rows / KS / f < 4) --f;
+  }
+  const int64_t split_from = nitems - tail;
+  if (f > 1) cudaMemsetAsync(split_cnt, 0, sizeof(unsigned) * tail, s);
+  gram_i8_kernel<S, KS, 8, LEAN><<<(unsigned)blocks, kQThreads, C::kSmem, s>>>(
+      ma, ma64, mb, segmax, segs, tiles, ntiles, f > 1 ? split_from + tail * f : nitems, seg_base, kp, part, headroom,
+      seg_ready, abort_flag, split_from, (int)f, split_ws, split_cnt);
   return true;
 }
 
@@ -904,15 +990,19 @@ static int i8_stage_rows() {
   return v;
 }
 
+// Workspace of the tail split for a grid of `ctas` CTAs: one int32 dump per part (<= ctas parts) and one counter
+// per tail item; 7 accumulators of 128 x 64 int32 per dump (S = 6).
+size_t gram_i8_split_ws_bytes(int ctas) { return (size_t)ctas * (7 * QA * QB * sizeof(int32_t)); }
+
 // lean != 0: the 96-register kernel that leaves room for a cut CTA on the same SM; seg_ready / abort_flag (both
 // or neither): wait for the concurrent cut's per-segment block counts.
 bool launch_gram_i8(int slices, const int8_t* zq, const unsigned long long* segmax, int headroom, int64_t zrows,
                     int64_t kp, const GramTask* segs, int64_t nseg, const int2* tiles, int ntiles, double* part,
                     cudaStream_t s, int64_t seg_base, int max_ctas, int lean, const unsigned* seg_ready,
-                    int* abort_flag) {
+                    int* abort_flag, int32_t* split_ws, unsigned* split_cnt, int64_t min_seg_rows) {
 #define CVG_GRAM_I8(S, KS, LEAN)                                                                                \
   return launch_gram_i8_s<S, KS, LEAN>(zq, segmax, headroom, zrows, kp, segs, seg_base, nseg, tiles, ntiles, part, \
-                                       max_ctas, seg_ready, abort_flag, s)
+                                       max_ctas, seg_ready, abort_flag, split_ws, split_cnt, min_seg_rows, s)
   if (lean) {
     if (slices == 5) CVG_GRAM_I8(5, 64, true);
     CVG_GRAM_I8(6, 64, true);
