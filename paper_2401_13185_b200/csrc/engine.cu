@@ -780,6 +780,7 @@ Status Plan::gram(const void* d_x, int64_t ldx, const void* d_y, int64_t ldy, co
       if (zrows_ > 0) CVG_TRY(i8_prep(d_x, ldx, d_y, ldy, rows, nsrc, 0, kp_, false));
       CVG_TRY(i8_gram(tilesq_d_.as<int2>(), (int)tilesq_.size()));
     }
+    CVG_TRY(i8_flags_to_host());
     CVG_TRY(gram_trees());
     CVG_TRY(i8_exact_pass(d_x, ldx, d_y, ldy, rows, nsrc));
     return poison_local();
@@ -931,15 +932,14 @@ Status Plan::i8_overlapped(const void* d_x, int64_t ldx, const void* d_y, int64_
 // segment and depends on the segment's rows only, so results stay bit-identical across GPU counts.
 Status Plan::i8_exact_pass(const void* d_x, int64_t ldx, const void* d_y, int64_t ldy, const int64_t* rows,
                            int64_t nsrc) {
-  if ((sample_ <= 1 && !overlapped_) || segs_.empty()) return Status::Ok();
-  cudaStream_t s = ctx_->stream;
-  ovf_host_.assign(segs_.size(), 0);
-  int aborted = 0;
-  if (sample_ > 1)
-    CVG_CK(cudaMemcpyAsync(ovf_host_.data(), ovf_.as<int>(), sizeof(int) * segs_.size(), cudaMemcpyDeviceToHost, s));
-  if (overlapped_)
-    CVG_CK(cudaMemcpyAsync(&aborted, seg_ready_.as<unsigned>() + segs_.size(), sizeof(int), cudaMemcpyDeviceToHost, s));
-  CVG_CK(cudaStreamSynchronize(s));
+  if (!flags_pending_) return Status::Ok();
+  flags_pending_ = false;
+  // wait for the flags' copy only (i8_flags_to_host): the trees queued behind it keep the GPU busy meanwhile
+  CVG_CK(cudaEventSynchronize(flags_ev_.get()));
+  const size_t nseg = segs_.size();
+  ovf_host_.assign(nseg, 0);
+  if (sample_ > 1) std::copy(flags_host_.get(), flags_host_.get() + nseg, ovf_host_.begin());
+  const int aborted = overlapped_ ? flags_host_.get()[nseg] : 0;
   overlapped_ = false;
   if (aborted) {
     // A Gram item gave up waiting for the cut (the two kernels did not share the SMs): the digits are complete
@@ -956,6 +956,26 @@ Status Plan::i8_exact_pass(const void* d_x, int64_t ldx, const void* d_y, int64_
   CVG_TRY(i8_prep(d_x, ldx, d_y, ldy, rows, nsrc, 0, kp_, true));
   CVG_TRY(i8_gram(tilesq_d_.as<int2>(), (int)tilesq_.size()));
   return gram_trees();
+}
+
+// The int8 path's host decisions (segments to redo from exact maxima; the overlapped Gram's abort flag) are
+// final once the cut and the Gram are done: copy them into pinned memory right there and record an event, so
+// that the host waits for that copy while the fold trees run, not for the whole stream.
+Status Plan::i8_flags_to_host() {
+  flags_pending_ = false;
+  if ((sample_ <= 1 && !overlapped_) || segs_.empty()) return Status::Ok();
+  cudaStream_t s = ctx_->stream;
+  const size_t nseg = segs_.size();
+  CVG_TRY(flags_host_.ensure(nseg + 1));
+  CVG_TRY(flags_ev_.ensure());
+  if (sample_ > 1)
+    CVG_CK(cudaMemcpyAsync(flags_host_.get(), ovf_.as<int>(), sizeof(int) * nseg, cudaMemcpyDeviceToHost, s));
+  if (overlapped_)
+    CVG_CK(cudaMemcpyAsync(flags_host_.get() + nseg, seg_ready_.as<unsigned>() + nseg, sizeof(int),
+                           cudaMemcpyDeviceToHost, s));
+  CVG_CK(cudaEventRecord(flags_ev_.get(), s));
+  flags_pending_ = true;
+  return Status::Ok();
 }
 
 Status Plan::gram_trees() {
@@ -1075,6 +1095,7 @@ Status Plan::gram_host(const void* h_x, const void* h_y, void* d_x, void* d_y, c
       CVG_TRY(count_launch());
     }
   }
+  if (i8_path()) CVG_TRY(i8_flags_to_host());
   CVG_TRY(gram_trees());
   if (i8_path()) CVG_TRY(i8_exact_pass(d_x, k_, d_y, m_, src_row_.as<int64_t>(), src_n_));
   return poison_local();

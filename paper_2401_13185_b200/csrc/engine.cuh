@@ -142,6 +142,7 @@ class Plan {
   Status i8_prep(const void* d_x, int64_t ldx, const void* d_y, int64_t ldy, const int64_t* rows, int64_t nsrc,
                  int64_t c0, int64_t c1, bool exact);
   Status i8_gram(const int2* tiles, int ntiles);
+  Status i8_flags_to_host();
   Status ensure_split_ws();
   Status i8_exact_pass(const void* d_x, int64_t ldx, const void* d_y, int64_t ldy, const int64_t* rows, int64_t nsrc);
   // the cut beside the Gram (engine.cu; CVG_I8_OVERLAP=0|1 overrides the segment-length rule): one direct-store cut CTA and one lean Gram CTA per SM
@@ -207,6 +208,37 @@ class Plan {
   };
   PlanKey plan_key_;
   bool planned_ = false;        // plan_key_ describes the segment plan the device buffers hold
+  struct PinnedInts {  // pinned host words for small device -> host flag copies
+    int* p = nullptr;
+    size_t cap = 0;
+    ~PinnedInts() {
+      if (p) cudaFreeHost(p);
+    }
+    Status ensure(size_t n) {
+      if (n <= cap) return Status::Ok();
+      if (p) cudaFreeHost(p);
+      p = nullptr;
+      cap = 0;
+      Status st = cuda_status(cudaHostAlloc(reinterpret_cast<void**>(&p), sizeof(int) * n, cudaHostAllocDefault),
+                              "cudaHostAlloc (flags)");
+      if (st.ok()) cap = n;
+      return st;
+    }
+    int* get() const { return p; }
+  };
+  struct OwnedEvent {
+    cudaEvent_t e = nullptr;
+    ~OwnedEvent() {
+      if (e) cudaEventDestroy(e);
+    }
+    Status ensure() {
+      return e ? Status::Ok() : cuda_status(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+    }
+    cudaEvent_t get() const { return e; }
+  };
+  PinnedInts flags_host_;       // int8 path: ovf[nseg] + the overlapped Gram's abort flag
+  OwnedEvent flags_ev_;
+  bool flags_pending_ = false;
   DevBuf split_ws_, split_cnt_;  // int8 Gram tail split: int32 dumps and per-item arrival counters
   DevBuf seg_ready_;            // overlapped cut: per-segment finished-block counts + the abort flag (last word)
   bool overlapped_ = false;     // the last gram ran the cut beside the Gram (its abort flag is pending)
