@@ -13,6 +13,7 @@
 // Gram[j][j] the sum of squares: the per-fold statistics ride in the Gram pass.
 #pragma once
 
+#include <atomic>
 #include <cstdio>
 
 #include <cuda_runtime.h>
@@ -214,6 +215,17 @@ bool launch_gram_i8(int slices, const int8_t* zq, const unsigned long long* segm
 // full round are cut into row parts whose exact int32 sums are added by the part that finishes last (bit-identical
 // to the unsplit item); min_seg_rows bounds the split so every part keeps a few stages.
 size_t gram_i8_split_ws_bytes(int ctas);
+
+// Function attributes are per device (one process may drive several: cvg_context_create_multi) but never
+// change: a launcher sets them the first time it runs on a device.  `done` is the launcher's own static mask
+// (bit = device ordinal, devices beyond 63 simply set them every time).
+inline bool first_on_device(std::atomic<uint64_t>& done) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev > 63) return true;
+  const uint64_t bit = 1ull << dev;
+  return !(done.fetch_or(bit, std::memory_order_relaxed) & bit);
+}
 
 inline int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
 inline int64_t padded_cols(int64_t k, int64_t m, int dtype = 0) {

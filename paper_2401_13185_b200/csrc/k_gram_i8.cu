@@ -873,7 +873,9 @@ bool launch_gram_i8_s(const int8_t* zq, const unsigned long long* segmax, int he
       !make_zq_map(&mb, zq, zrows, kp, S, QB, KS))
     return false;
   using C = QCfg<S, KS, 8>;
-  cudaFuncSetAttribute(gram_i8_kernel<S, KS, 8, LEAN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
+  static std::atomic<uint64_t> attrs_done{0};  // one per <S, KS, LEAN> instantiation
+  if (first_on_device(attrs_done))
+    cudaFuncSetAttribute(gram_i8_kernel<S, KS, 8, LEAN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -911,8 +913,10 @@ bool launch_k1q(const void* x, int64_t ldx, const void* y, int64_t ldy, int64_t 
     const int64_t blocks = std::min<int64_t>(blk_hi - blk_lo, (int64_t)direct_ctas_per_sm * sms_all);
     if (blocks <= 0) return true;
     // same shared-memory carveout as the Gram it shares the SM with (an SM holds one configuration at a time)
-    cudaFuncSetAttribute(reorder_q_kernel<T, S, true>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                         cudaSharedmemCarveoutMaxShared);
+    static std::atomic<uint64_t> direct_done{0};
+    if (first_on_device(direct_done))
+      cudaFuncSetAttribute(reorder_q_kernel<T, S, true>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                           cudaSharedmemCarveoutMaxShared);
     reorder_q_kernel<T, S, true><<<(unsigned)blocks, kQ1Threads, 0, s>>>(
         none, (const T*)x, ldx, (const T*)y, ldy, k, m, src_row, zrows, kp, c_begin, c_end, nsrc, shift, blkseg, segmax,
         headroom, ovf, nonfinite, blk_lo, blk_hi, zq, seg_ready);
@@ -924,7 +928,9 @@ bool launch_k1q(const void* x, int64_t ldx, const void* y, int64_t ldy, int64_t 
   // grid-stride over one wave of resident CTAs.  Function attributes are per device (one process may drive
   // several: cvg_context_create_multi), so they are set on every launch; the occupancy query is cached per device.
   static std::atomic<int> wave_cache[64];
-  cudaFuncSetAttribute(reorder_q_kernel<T, S, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  static std::atomic<uint64_t> attrs_done{0};
+  if (first_on_device(attrs_done))
+    cudaFuncSetAttribute(reorder_q_kernel<T, S, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   int wave = wave_cache[dev & 63].load(std::memory_order_relaxed);
   if (!wave) {
     int per_sm = 0;
